@@ -1,0 +1,181 @@
+/*
+ * svgear.h — C ABI of libsvgear.so: the B200 (sm_100a) implementation of the SVG-EAR
+ * attention hot path.
+ *
+ * The reference (`routedattn`, numpy/CPU, /root/reference/pkg/src/routedattn) has no FFI: the
+ * operator is the four-call Python composition
+ *     prepare -> build_error_table -> route_error_aware -> sparse_attend
+ * (README.md:94-98, cli.py:119-134).  Each entry point below replaces one of those calls (cited
+ * per function) for a BATCH of independent (Q,K,V) instances ("heads"; `bh` = batch*heads), so a
+ * maintainer can bind it from Python with ctypes.
+ *
+ * Conventions
+ *  - plain pointers and sizes only; every pointer is a CUDA DEVICE pointer unless named `host_*`;
+ *  - the caller owns every buffer including the workspace; the library allocates nothing that
+ *    outlives a call and keeps no global state; outputs are written exactly once;
+ *  - all work is enqueued on `stream` (a cudaStream_t passed as void*), nothing synchronises the
+ *    host; results are deterministic run to run (no floating-point atomics);
+ *  - token matrices are row-major bf16 `[bh][n][d]`, d in {64,128}, d_v == d;
+ *  - index outputs are int32; block tables are row-major `[bh][c_q][c_k]`;
+ *  - return value: SVGEAR_OK (0) or a negative status; svgear_strerror() names it.
+ *  - there is NO CPU fallback: without a CUDA device every compute entry returns SVGEAR_ECUDA.
+ */
+#ifndef SVGEAR_H_
+#define SVGEAR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVGEAR_VERSION 100 /* 0.1.0 */
+
+enum {
+  SVGEAR_OK = 0,
+  SVGEAR_EINVAL = -1,      /* bad argument value (null pointer, budget, mode, iteration count)   */
+  SVGEAR_ESHAPE = -2,      /* unsupported / inconsistent shape (d, cluster counts vs tokens)      */
+  SVGEAR_ECUDA = -3,       /* a CUDA call failed (or no device)                                   */
+  SVGEAR_EWORKSPACE = -4,  /* workspace too small; see svgear_workspace_bytes                     */
+  SVGEAR_EUNSUPPORTED = -5 /* valid in the reference but not implemented on this path             */
+};
+
+/* estimator modes — analysis.build_error_table(mode) (analysis.py:242-249) */
+enum { SVGEAR_EST_VALUE_AWARE = 0, SVGEAR_EST_PLAIN = 1 };
+/* greedy walk policy — router.DensityBudget.overshoot (router.py:29-30, 100-110) */
+enum { SVGEAR_FILL_REMAINDER = 0, SVGEAR_STOP_AT_FIRST_OVERFLOW = 1 };
+/* executor arithmetic — sparse_attend(dtype=...) (attention.py:160-168) */
+enum {
+  SVGEAR_EXEC_BF16_TENSOR = 0, /* tcgen05 bf16 MMA, fp32 softmax/accumulate, bf16 output          */
+  SVGEAR_EXEC_FP32_CHECK = 1   /* CUDA-core fp32 everywhere, fp32 output (the "fp32 check mode")  */
+};
+
+/* Problem shape of one call (all `bh` instances share it). */
+typedef struct SvgEarShape {
+  int32_t bh;  /* number of independent (Q,K,V) instances = batch * heads                         */
+  int32_t n_q; /* query tokens per instance                                                       */
+  int32_t n_k; /* key/value tokens per instance                                                   */
+  int32_t d;   /* head dimension, 64 or 128                                                       */
+  int32_t c_q; /* query clusters, 1 <= c_q <= n_q                                                 */
+  int32_t c_k; /* key clusters,   1 <= c_k <= n_k, c_k <= 4096                                    */
+} SvgEarShape;
+
+/* Optional extra outputs of svgear_forward (any member may be NULL).  These are the fields of the
+ * reference's ClusterModel (clustering.py:29-39), BlockErrorTable (estimator.py:50-73) and
+ * AttentionResult (attention.py:48-54) that the parity tests compare. */
+typedef struct SvgEarAux {
+  int32_t* q_assign;    /* [bh][n_q]  raw-order cluster id                                         */
+  int32_t* k_assign;    /* [bh][n_k]                                                               */
+  int32_t* q_perm;      /* [bh][n_q]  permuted[i] = tokens[perm[i]] (stable sort by cluster)       */
+  int32_t* k_perm;      /* [bh][n_k]                                                               */
+  int32_t* q_sizes;     /* [bh][c_q]                                                               */
+  int32_t* k_sizes;     /* [bh][c_k]                                                               */
+  int32_t* q_offsets;   /* [bh][c_q]  exclusive cumsum of sizes                                    */
+  int32_t* k_offsets;   /* [bh][c_k]                                                               */
+  float* q_centroids;   /* [bh][c_q][d]                                                            */
+  float* k_centroids;   /* [bh][c_k][d]                                                            */
+  float* v_centroids;   /* [bh][c_k][d]                                                            */
+  int32_t* q_iters;     /* [bh] Lloyd iterations executed                                          */
+  int32_t* k_iters;     /* [bh]                                                                    */
+  double* error_table;  /* [bh][c_q][c_k] stabilised block error sums                              */
+  float* stabilizers;   /* [bh][c_q] per-row reference logit the sums were taken at                */
+  int64_t* mask_entries;/* [bh] entries covered by selected blocks (BlockMask.density_entries)     */
+  float* lse;           /* [bh][n_q] final log-sum-exp per query, ORIGINAL token order             */
+} SvgEarAux;
+
+const char* svgear_strerror(int status);
+int svgear_version(void);
+/* Diagnostic: number of CUDA kernels this library has launched in this process so far. */
+int64_t svgear_launch_count(void);
+
+/* Bytes of device workspace sufficient for ANY entry point below at this shape. */
+int svgear_workspace_bytes(const SvgEarShape* shape, size_t* bytes);
+
+/* Lloyd k-means for `bh` token matrices from explicit start centres.
+ * Replaces clustering.kmeans / _lloyd (clustering.py:104-207) for restarts=1 with the start
+ * centres given (the reference draws them with host-side numpy k-means++, clustering.py:65-84;
+ * the Python shim reproduces that draw or accepts warm-start centres).
+ * Semantics kept: distance = max(|x|^2 - 2x.c + |c|^2, 0); ties -> lowest cluster index; empty
+ * clusters repaired in ascending order from the farthest token of a cluster with >=2 members;
+ * convergence is tested before the centroid update; final centroids are the member means;
+ * permutation = stable sort by cluster.  Distances are evaluated in fp32 (reference: float64).
+ *   x            [bh][n][d] bf16          init_centroids [bh][c][d] f32
+ *   assign,perm  [bh][n] i32              sizes,offsets  [bh][c] i32
+ *   centroids    [bh][c][d] f32           iters [bh] i32, inertia [bh] f64 (either may be NULL) */
+int svgear_kmeans(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
+                  const float* init_centroids, int32_t max_iters, int32_t* assign, int32_t* perm,
+                  int32_t* sizes, int32_t* offsets, float* centroids, int32_t* iters,
+                  double* inertia, void* workspace, size_t workspace_bytes, void* stream);
+
+/* out[b][i][:] = x[b][perm[b][i]][:]   — clustering.permute_rows (clustering.py:210-212). */
+int svgear_permute_rows(int32_t bh, int32_t n, int32_t d, const void* x, const int32_t* perm,
+                        void* out, void* stream);
+
+/* Per-cluster means of a cluster-contiguous bf16 matrix, accumulated in ascending row order in
+ * float64 and rounded once to f32 — clustering.segment_means (clustering.py:247-257). */
+int svgear_segment_means(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x_permuted,
+                         const int32_t* sizes, const int32_t* offsets, float* means, void* stream);
+
+/* Block error table — estimator.estimate_errors_streaming / estimate_errors
+ * (estimator.py:187-253, 120-148) selected by `mode` as analysis.build_error_table does.
+ *   k_permuted, v_permuted [bh][n_k][d] bf16 cluster-contiguous (v may be NULL for PLAIN)
+ *   error_table [bh][c_q][c_k] f64 (stabilised at `stabilizers`, multiplied by |q_c|)
+ *   stabilizers [bh][c_q] f32 = row max of centroid logits                                      */
+int svgear_error_table(const SvgEarShape* shape, int32_t mode, const float* q_centroids,
+                       const float* k_centroids, const float* v_centroids, const void* k_permuted,
+                       const void* v_permuted, const int32_t* q_sizes, const int32_t* k_sizes,
+                       const int32_t* k_offsets, double* error_table, float* stabilizers,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* Greedy error-to-cost routing under an entry budget — router.route_error_aware_entries
+ * (router.py:124-142): order (-ratio,-error,qc,kc) (estimator.py:83-96), walk with
+ * fillRemainder / stopAtFirstOverflow (router.py:100-110), best-single-block fallback
+ * (router.py:113-121).  `capacity_entries` = entry_capacity(rho, n_q*n_k) (router.py:93-97),
+ * computed by the caller in double precision exactly as the reference does.
+ *   mask [bh][c_q][c_k] u8 (1 = exact block)      entries [bh] i64 (may be NULL)               */
+int svgear_route_error_aware(int32_t bh, int32_t c_q, int32_t c_k, const double* error_table,
+                             const int32_t* q_sizes, const int32_t* k_sizes,
+                             int64_t capacity_entries, int32_t overshoot,
+                             int32_t single_item_fallback, uint8_t* mask, int64_t* entries,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* Cluster-mass (SVG2-style) routing at the same entry budget — router.route_score
+ * (router.py:253-280): per-row softmax of q̄.k̄/sqrt(d) + ln|k_c|, order (-mass, index).        */
+int svgear_route_score(const SvgEarShape* shape, const float* q_centroids,
+                       const float* k_centroids, const int32_t* q_sizes, const int32_t* k_sizes,
+                       int64_t capacity_entries, int32_t overshoot, uint8_t* mask,
+                       int64_t* entries, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Block-sparse executor with centroid compensation folded into one online softmax —
+ * attention.sparse_attend = exact_block_pass + compensation_pass (attention.py:57-192).
+ *   q_permuted/k_permuted/v_permuted cluster-contiguous bf16; mask [bh][c_q][c_k] u8
+ *   q_perm: if non-NULL, output row i is scattered to original index q_perm[i]
+ *           (clustering.inverse_permute_rows, clustering.py:215-219); if NULL the output keeps
+ *           the reference's permuted row order.
+ *   out: bf16 [bh][n_q][d] for SVGEAR_EXEC_BF16_TENSOR, f32 for SVGEAR_EXEC_FP32_CHECK
+ *   lse: [bh][n_q] f32 or NULL (same row order as out)                                          */
+int svgear_sparse_attend(const SvgEarShape* shape, int32_t exec_mode, const void* q_permuted,
+                         const void* k_permuted, const void* v_permuted, const int32_t* q_perm,
+                         const int32_t* q_sizes, const int32_t* q_offsets, const int32_t* k_sizes,
+                         const int32_t* k_offsets, const float* k_centroids,
+                         const float* v_centroids, const uint8_t* mask, void* out, float* lse,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* The whole operator on one stream: k-means(Q), k-means(K), permute, error table, routing,
+ * fused attention; output in ORIGINAL token order.  Equivalent per instance to
+ * prepare -> build_error_table -> route_error_aware(global density) -> sparse_attend ->
+ * inverse_permute_rows (cli.py:119-134).
+ *   q,k,v [bh][n][d] bf16      q_init [bh][c_q][d] f32, k_init [bh][c_k][d] f32
+ *   out  [bh][n_q][d] (bf16 / f32 per exec_mode)     mask [bh][c_q][c_k] u8
+ *   aux may be NULL                                                                              */
+int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const void* v,
+                   const float* q_init, const float* k_init, int32_t kmeans_iters,
+                   int32_t estimator_mode, int64_t capacity_entries, int32_t overshoot,
+                   int32_t single_item_fallback, int32_t exec_mode, void* out, uint8_t* mask,
+                   const SvgEarAux* aux, void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVGEAR_H_ */

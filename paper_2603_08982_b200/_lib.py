@@ -1,0 +1,118 @@
+"""ctypes binding of libsvgear.so (C ABI in include/svgear.h).
+
+The shared library is built in-tree from csrc/*.cu by `build_library()` (nvcc, sm_100a only) and
+loaded by `lib()`.  There is no fallback of any kind: if the library is missing or a call fails,
+an exception is raised.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(PKG_DIR, "csrc")
+LIB_PATH = os.path.join(PKG_DIR, "libsvgear.so")
+SOURCES = ("api.cu", "kmeans.cu", "stats_route.cu", "attend_ref.cu", "attend_tc.cu")
+NVCC_FLAGS = (
+    "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+    "-shared", "-Xcompiler", "-fPIC",
+)
+
+OK, EINVAL, ESHAPE, ECUDA, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4, -5
+EST_VALUE_AWARE, EST_PLAIN = 0, 1
+FILL_REMAINDER, STOP_AT_FIRST_OVERFLOW = 0, 1
+EXEC_BF16_TENSOR, EXEC_FP32_CHECK = 0, 1
+
+
+class SvgEarError(RuntimeError):
+    """A libsvgear entry point returned a negative status."""
+
+    def __init__(self, fn, status, text):
+        super().__init__(f"{fn} failed: {text} (status {status})")
+        self.status = status
+
+
+class Shape(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("bh", "n_q", "n_k", "d", "c_q", "c_k")]
+
+
+class Aux(C.Structure):
+    FIELDS = ("q_assign", "k_assign", "q_perm", "k_perm", "q_sizes", "k_sizes", "q_offsets",
+              "k_offsets", "q_centroids", "k_centroids", "v_centroids", "q_iters", "k_iters",
+              "error_table", "stabilizers", "mask_entries", "lse")
+    _fields_ = [(n, C.c_void_p) for n in FIELDS]
+
+
+# symbol -> argtypes; every symbol include/svgear.h declares must appear here
+_P, _I32, _I64, _SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_size_t
+SIGNATURES = {
+    "svgear_strerror": ([C.c_int], C.c_char_p),
+    "svgear_version": ([], C.c_int),
+    "svgear_launch_count": ([], C.c_int64),
+    "svgear_workspace_bytes": ([C.POINTER(Shape), C.POINTER(_SZ)], C.c_int),
+    "svgear_kmeans": ([_I32, _I32, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "svgear_permute_rows": ([_I32, _I32, _I32, _P, _P, _P, _P], C.c_int),
+    "svgear_segment_means": ([_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P], C.c_int),
+    "svgear_error_table": ([C.POINTER(Shape), _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "svgear_route_error_aware": ([_I32, _I32, _I32, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _SZ, _P], C.c_int),
+    "svgear_route_score": ([C.POINTER(Shape), _P, _P, _P, _P, _I64, _I32, _P, _P, _P, _SZ, _P], C.c_int),
+    "svgear_sparse_attend": ([C.POINTER(Shape), _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "svgear_forward": ([C.POINTER(Shape), _P, _P, _P, _P, _P, _I32, _I32, _I64, _I32, _I32, _I32, _P, _P, C.POINTER(Aux), _P, _SZ, _P], C.c_int),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def _stale():
+    if not os.path.exists(LIB_PATH):
+        return True
+    t = os.path.getmtime(LIB_PATH)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [
+        os.path.join(os.path.dirname(PKG_DIR), "include", "svgear.h")]
+    return any(os.path.getmtime(p) > t for p in deps)
+
+
+def build_library(force=False, verbose=False):
+    """Compile csrc/*.cu into libsvgear.so for sm_100a (nvcc cross-compiles without a GPU)."""
+    if not force and not _stale():
+        return LIB_PATH
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *[os.path.join(CSRC, s) for s in SOURCES]]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    if verbose:
+        print(res.stderr)
+    return LIB_PATH
+
+
+def lib():
+    """Load libsvgear.so (building it first only if nvcc is available and it is missing)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                build_library()
+            handle = C.CDLL(LIB_PATH)
+            for name, (args, res) in SIGNATURES.items():
+                fn = getattr(handle, name)  # AttributeError if the symbol is not exported
+                fn.argtypes = args
+                fn.restype = res
+            _lib = handle
+        return _lib
+
+
+def check(fn_name, status):
+    if status != OK:
+        raise SvgEarError(fn_name, status, lib().svgear_strerror(status).decode())
+
+
+def workspace_bytes(shape: Shape) -> int:
+    out = _SZ(0)
+    check("svgear_workspace_bytes", lib().svgear_workspace_bytes(C.byref(shape), C.byref(out)))
+    return int(out.value)

@@ -1,0 +1,215 @@
+"""GPU k-means + cluster-contiguous permutation — host mirror of routedattn.clustering.
+
+Same names and argument meaning as the reference (clustering.py:144-257); arrays are torch CUDA
+tensors.  `kmeans` accepts one instance [n, d] (as the reference) or a batch [bh, n, d].
+The k-means++ seeding is host-side numpy with the reference's RNG call sequence
+(clustering.py:65-84, 178-180) so a given `seed` starts from the identical centres; Lloyd
+iterations, repair, permutation and means run in libsvgear (svgear_kmeans).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._tensors import ShapeError, as_f32, as_tokens, stream_ptr, workspace
+
+
+@dataclass(frozen=True)
+class ClusterModel:
+    """Result of clustering (clustering.py:29-39).  Tensors live on the GPU; a model fitted on a
+    batch keeps the leading [bh] dimension on every field."""
+
+    num_clusters: int
+    assignments: torch.Tensor  # (n,) int32, raw token order
+    centroids: torch.Tensor    # (num_clusters, d) float32
+    sizes: torch.Tensor        # (num_clusters,) int32, all >= 1
+    permutation: torch.Tensor  # (n,) int32; permuted[i] = tokens[permutation[i]]
+    offsets: torch.Tensor      # (num_clusters,) int32
+    flops: int = 0
+    iters: object = None       # Lloyd iterations executed (int, or tensor for a batch)
+    inertia: object = None
+
+
+def kmeans_pp_init(tokens, k, rng):
+    """k-means++ centres with the reference's draw sequence (clustering.py:65-84), float64 numpy."""
+    x = np.ascontiguousarray(tokens, dtype=np.float64)
+    n = x.shape[0]
+    centres = np.empty((k, x.shape[1]), dtype=np.float64)
+    taken = np.zeros(n, dtype=bool)
+    i = int(rng.integers(n))
+    centres[0] = x[i]
+    taken[i] = True
+    near = ((x - centres[0]) ** 2).sum(axis=1)
+    for c in range(1, k):
+        tot = near.sum()
+        i = int(rng.choice(n, p=near / tot)) if tot > 0.0 else int(np.flatnonzero(~taken)[0])
+        centres[c] = x[i]
+        taken[i] = True
+        near = np.minimum(near, ((x - centres[c]) ** 2).sum(axis=1))
+    return centres
+
+
+def seeded_start(tokens, k, seed, restart=0):
+    """Start centres of restart `restart` for `seed` (clustering.py:178-180)."""
+    rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(restart,)))
+    return kmeans_pp_init(tokens, k, rng)
+
+
+def strided_start(tokens, k):
+    """Deterministic device-side start: k evenly strided tokens.  NOT the reference's seeding —
+    used when no seed-faithful start is needed (benchmarks, warm-up of a centroid cache)."""
+    n = tokens.shape[-2]
+    idx = torch.div(torch.arange(k, device=tokens.device) * n, k, rounding_mode="floor")
+    return tokens.index_select(-2, idx).float().contiguous()
+
+
+def _pad_centers(tok_f32, centers, k):
+    """Grow a centre set to k rows by farthest-token selection (clustering.py:87-101)."""
+    centers = torch.as_tensor(centers, dtype=torch.float32, device=tok_f32.device)
+    if centers.ndim != 2 or centers.shape[1] != tok_f32.shape[1]:
+        raise ValueError(
+            f"init centroids must be 2-D with {tok_f32.shape[1]} columns, got {tuple(centers.shape)}")
+    if centers.shape[0] > k:
+        raise ValueError(f"got {centers.shape[0]} init centroids for {k} clusters")
+    d2 = torch.cdist(tok_f32.double(), centers.double()).pow(2).min(dim=1).values
+    while centers.shape[0] < k:
+        i = int(torch.argmax(d2))
+        centers = torch.cat([centers, tok_f32[i:i + 1]], dim=0)
+        d2 = torch.minimum(d2, (tok_f32.double() - tok_f32[i].double()).pow(2).sum(dim=1))
+    return centers
+
+
+def run_lloyd(x, starts, max_iters):
+    """x [bh,n,d] bf16, starts [bh,c,d] f32 -> dict of raw svgear_kmeans outputs."""
+    bh, n, d = x.shape
+    c = starts.shape[1]
+    dev = x.device
+    out = dict(
+        assign=torch.empty((bh, n), dtype=torch.int32, device=dev),
+        perm=torch.empty((bh, n), dtype=torch.int32, device=dev),
+        sizes=torch.empty((bh, c), dtype=torch.int32, device=dev),
+        offsets=torch.empty((bh, c), dtype=torch.int32, device=dev),
+        centroids=torch.empty((bh, c, d), dtype=torch.float32, device=dev),
+        iters=torch.zeros((bh,), dtype=torch.int32, device=dev),
+        inertia=torch.zeros((bh,), dtype=torch.float64, device=dev),
+    )
+    shape = _lib.Shape(bh, n, n, d, c, c)
+    ws = workspace(_lib.workspace_bytes(shape), dev)
+    rc = _lib.lib().svgear_kmeans(
+        bh, n, d, c, x.data_ptr(), starts.data_ptr(), int(max_iters), out["assign"].data_ptr(),
+        out["perm"].data_ptr(), out["sizes"].data_ptr(), out["offsets"].data_ptr(),
+        out["centroids"].data_ptr(), out["iters"].data_ptr(), out["inertia"].data_ptr(),
+        ws.data_ptr(), ws.numel(), stream_ptr())
+    _lib.check("svgear_kmeans", rc)
+    return out
+
+
+def _flops(n, k, d, iters):
+    return 2 * n * k * d + iters * (2 * n * k * d + 2 * n * k + 2 * n * d)  # clustering.py:138-140
+
+
+def kmeans(tokens, num_clusters, *, max_iters=25, seed=0, restarts=1, init_centroids=None):
+    """Cluster token rows; best of `restarts` seeded runs (+ an optional warm start).
+
+    Mirrors clustering.kmeans (clustering.py:144-207) including its validation errors.  For a
+    batch [bh, n, d], instance b is seeded with `seed + b` and `init_centroids` may be [bh, c', d].
+    """
+    x, was_2d = _validated(tokens, num_clusters, restarts, max_iters)
+    bh, n, d = x.shape
+    k = int(num_clusters)
+    x_host = x.float().cpu().numpy().astype(np.float64)
+    pool = []  # list over starts of [bh,k,d] f32
+    for r in range(restarts):
+        pool.append(torch.from_numpy(np.stack(
+            [seeded_start(x_host[b], k, seed + b, r) for b in range(bh)])).to(x.device, torch.float32))
+    if init_centroids is not None:
+        ic = torch.as_tensor(np.asarray(init_centroids) if not isinstance(init_centroids, torch.Tensor)
+                             else init_centroids)
+        if ic.ndim == 2:
+            ic = ic.unsqueeze(0).expand(bh, -1, -1)
+        xf = x.float()
+        pool.append(torch.stack([_pad_centers(xf[b], ic[b], k) for b in range(bh)]))
+    # every start is one more batch instance: [S*bh, ...]
+    S = len(pool)
+    res = run_lloyd(x.repeat(S, 1, 1) if S > 1 else x, torch.cat(pool, dim=0).contiguous(), max_iters)
+    inertia = res["inertia"].view(S, bh)
+    best = torch.argmin(inertia, dim=0)  # ties -> earliest start, as the reference
+    pick = best * bh + torch.arange(bh, device=x.device)
+    iters = res["iters"].view(S, bh)
+    flops = int(sum(_flops(n, k, d, int(i)) for i in iters.flatten().tolist()))
+    fields = {key: res[key].index_select(0, pick) for key in ("assign", "perm", "sizes", "offsets", "centroids")}
+    sq = (lambda t: t[0]) if was_2d else (lambda t: t)
+    it = iters.gather(0, best.unsqueeze(0))[0]
+    return ClusterModel(
+        num_clusters=k, assignments=sq(fields["assign"]), centroids=sq(fields["centroids"]),
+        sizes=sq(fields["sizes"]), permutation=sq(fields["perm"]), offsets=sq(fields["offsets"]),
+        flops=flops, iters=int(it[0]) if was_2d else it,
+        inertia=float(inertia.min(dim=0).values[0]) if was_2d else inertia.min(dim=0).values)
+
+
+def _validated(tokens, num_clusters, restarts, max_iters):
+    if isinstance(tokens, torch.Tensor):
+        nd, n = tokens.ndim, (tokens.shape[-2] if tokens.ndim >= 2 else 0)
+    else:
+        arr = np.asarray(tokens)
+        nd, n = arr.ndim, (arr.shape[-2] if arr.ndim >= 2 else 0)
+    if nd not in (2, 3):
+        raise ShapeError(f"token matrix must be 2-D, got shape {tuple(np.shape(tokens))}")
+    if num_clusters < 1:
+        raise ValueError(f"num_clusters must be >= 1, got {num_clusters}")
+    if num_clusters > n:
+        raise ValueError(f"num_clusters ({num_clusters}) exceeds token count ({n})")
+    if restarts < 1:
+        raise ValueError(f"restarts must be >= 1, got {restarts}")
+    if max_iters < 1:
+        raise ValueError(f"max_iters must be >= 1, got {max_iters}")
+    return as_tokens(tokens)
+
+
+def permute_rows(tokens, model: ClusterModel):
+    """Reorder raw-order rows into cluster-contiguous order (clustering.py:210-212)."""
+    x, was_2d = as_tokens(tokens, check_finite=False)
+    bh, n, d = x.shape
+    perm = model.permutation.view(bh, n).contiguous()
+    out = torch.empty_like(x)
+    rc = _lib.lib().svgear_permute_rows(bh, n, d, x.data_ptr(), perm.data_ptr(), out.data_ptr(), stream_ptr())
+    _lib.check("svgear_permute_rows", rc)
+    return out[0] if was_2d else out
+
+
+def inverse_permute_rows(rows, model: ClusterModel):
+    """Undo permute_rows (clustering.py:215-219): out[perm[i]] = rows[i]."""
+    perm = model.permutation.long()
+    out = torch.empty_like(rows)
+    if perm.ndim == 1:
+        out[perm] = rows
+    else:
+        out.scatter_(1, perm.unsqueeze(-1).expand_as(rows) if rows.ndim == 3 else perm, rows)
+    return out
+
+
+def segment_means(tokens_permuted, model: ClusterModel):
+    """Per-cluster means of a cluster-contiguous matrix (clustering.py:247-257), float32."""
+    x, was_2d = as_tokens(tokens_permuted, check_finite=False)
+    bh, n, d = x.shape
+    c = model.num_clusters
+    sizes = model.sizes.view(bh, c).contiguous()
+    offsets = model.offsets.view(bh, c).contiguous()
+    out = torch.empty((bh, c, d), dtype=torch.float32, device=x.device)
+    rc = _lib.lib().svgear_segment_means(bh, n, d, c, x.data_ptr(), sizes.data_ptr(), offsets.data_ptr(),
+                                         out.data_ptr(), stream_ptr())
+    _lib.check("svgear_segment_means", rc)
+    return out[0] if was_2d else out
+
+
+def cluster_means(model: ClusterModel, tokens):
+    """Per-cluster means of raw-order `tokens` under the model (clustering.py:222-240)."""
+    n = model.assignments.shape[-1]
+    if tokens.shape[-2] != n:
+        raise ValueError(f"token count {tokens.shape[-2]} does not match model ({n} assignments)")
+    return segment_means(permute_rows(tokens, model), model)

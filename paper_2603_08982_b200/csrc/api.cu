@@ -1,0 +1,291 @@
+// extern "C" entry points of libsvgear.so (declared in include/svgear.h).
+#include <math.h>
+#include <string.h>
+
+#include "common.cuh"
+
+using namespace svg;
+
+namespace svg {
+long long g_launches = 0;
+}
+
+namespace {
+
+bool shape_ok(const SvgEarShape* s) {
+  if (!s) return false;
+  if (s->bh < 1 || s->n_q < 1 || s->n_k < 1) return false;
+  if (s->d != 64 && s->d != 128) return false;
+  if (s->c_q < 1 || s->c_q > s->n_q || s->c_q > kMaxClusters) return false;
+  if (s->c_k < 1 || s->c_k > s->n_k || s->c_k > kMaxClusters) return false;
+  return true;
+}
+
+// Everything svgear_forward keeps in the workspace.  The same routine sizes (base == nullptr) and
+// carves it, so the two can never disagree.
+struct ForwardPlan {
+  KmeansScratch km;  // shared by both sides (sized for the larger)
+  AttendScratch at;
+  int32_t *q_assign, *k_assign, *q_perm, *k_perm, *q_sizes, *k_sizes, *q_offsets, *k_offsets;
+  int32_t *q_iters, *k_iters;
+  float *q_cent, *k_cent, *v_cent, *sbar, *stab, *lse_tmp;
+  double* err;
+  int64_t* entries;
+  bf16 *qp, *kp, *vp;
+};
+
+bool plan_forward(const SvgEarShape& s, Carver& cv, ForwardPlan& p) {
+  const int nmax = s.n_q > s.n_k ? s.n_q : s.n_k;
+  const int cmax = s.c_q > s.c_k ? s.c_q : s.c_k;
+  p.km.carve(cv, s.bh, nmax, cmax);
+  p.at.carve(cv, s);
+  p.q_assign = cv.take<int32_t>((size_t)s.bh * s.n_q);
+  p.k_assign = cv.take<int32_t>((size_t)s.bh * s.n_k);
+  p.q_perm = cv.take<int32_t>((size_t)s.bh * s.n_q);
+  p.k_perm = cv.take<int32_t>((size_t)s.bh * s.n_k);
+  p.q_sizes = cv.take<int32_t>((size_t)s.bh * s.c_q);
+  p.k_sizes = cv.take<int32_t>((size_t)s.bh * s.c_k);
+  p.q_offsets = cv.take<int32_t>((size_t)s.bh * s.c_q);
+  p.k_offsets = cv.take<int32_t>((size_t)s.bh * s.c_k);
+  p.q_iters = cv.take<int32_t>(s.bh);
+  p.k_iters = cv.take<int32_t>(s.bh);
+  p.q_cent = cv.take<float>((size_t)s.bh * s.c_q * s.d);
+  p.k_cent = cv.take<float>((size_t)s.bh * s.c_k * s.d);
+  p.v_cent = cv.take<float>((size_t)s.bh * s.c_k * s.d);
+  p.sbar = cv.take<float>((size_t)s.bh * s.c_q * s.c_k);
+  p.stab = cv.take<float>((size_t)s.bh * s.c_q);
+  p.lse_tmp = cv.take<float>((size_t)s.bh * s.n_q);
+  p.err = cv.take<double>((size_t)s.bh * s.c_q * s.c_k);
+  p.entries = cv.take<int64_t>(s.bh);
+  p.qp = cv.take<bf16>((size_t)s.bh * s.n_q * s.d);
+  p.kp = cv.take<bf16>((size_t)s.bh * s.n_k * s.d);
+  p.vp = cv.take<bf16>((size_t)s.bh * s.n_k * s.d);
+  return cv.ok;
+}
+
+size_t forward_bytes(const SvgEarShape& s) {
+  Carver cv(nullptr, (size_t)-1);
+  ForwardPlan p;
+  plan_forward(s, cv, p);
+  return cv.off + 256;
+}
+
+bool device_present() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return n > 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* svgear_strerror(int status) {
+  switch (status) {
+    case SVGEAR_OK: return "ok";
+    case SVGEAR_EINVAL: return "invalid argument";
+    case SVGEAR_ESHAPE: return "unsupported or inconsistent shape";
+    case SVGEAR_ECUDA: return "CUDA error (or no CUDA device)";
+    case SVGEAR_EWORKSPACE: return "workspace too small";
+    case SVGEAR_EUNSUPPORTED: return "not supported on this path";
+    default: return "unknown status";
+  }
+}
+
+int svgear_version(void) { return SVGEAR_VERSION; }
+
+int64_t svgear_launch_count(void) { return (int64_t)svg::g_launches; }
+
+int svgear_workspace_bytes(const SvgEarShape* shape, size_t* bytes) {
+  if (!shape || !bytes) return SVGEAR_EINVAL;
+  if (!shape_ok(shape)) return SVGEAR_ESHAPE;
+  *bytes = forward_bytes(*shape);
+  return SVGEAR_OK;
+}
+
+int svgear_kmeans(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
+                  const float* init_centroids, int32_t max_iters, int32_t* assign, int32_t* perm,
+                  int32_t* sizes, int32_t* offsets, float* centroids, int32_t* iters,
+                  double* inertia, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!x || !init_centroids || !assign || !perm || !sizes || !offsets || !centroids || !workspace)
+    return SVGEAR_EINVAL;
+  if (max_iters < 1) return SVGEAR_EINVAL;
+  if (bh < 1 || n < 1 || (d != 64 && d != 128) || c < 1 || c > n || c > kMaxClusters)
+    return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  Carver cv(workspace, workspace_bytes);
+  KmeansScratch sc;
+  if (!sc.carve(cv, bh, n, c)) return SVGEAR_EWORKSPACE;
+  return launch_kmeans(bh, n, d, c, (const bf16*)x, init_centroids, max_iters, assign, perm, sizes,
+                       offsets, centroids, iters, inertia, sc, (cudaStream_t)stream);
+}
+
+int svgear_permute_rows(int32_t bh, int32_t n, int32_t d, const void* x, const int32_t* perm,
+                        void* out, void* stream) {
+  if (!x || !perm || !out) return SVGEAR_EINVAL;
+  if (bh < 1 || n < 1 || (d != 64 && d != 128)) return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  return launch_gather_rows(bh, n, d, (const bf16*)x, perm, (bf16*)out, (cudaStream_t)stream);
+}
+
+int svgear_segment_means(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x_permuted,
+                         const int32_t* sizes, const int32_t* offsets, float* means, void* stream) {
+  if (!x_permuted || !sizes || !offsets || !means) return SVGEAR_EINVAL;
+  if (bh < 1 || n < 1 || (d != 64 && d != 128) || c < 1 || c > n) return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  return launch_segment_means(bh, n, d, c, (const bf16*)x_permuted, sizes, offsets, means, nullptr,
+                              (cudaStream_t)stream);
+}
+
+int svgear_error_table(const SvgEarShape* shape, int32_t mode, const float* q_centroids,
+                       const float* k_centroids, const float* v_centroids, const void* k_permuted,
+                       const void* v_permuted, const int32_t* q_sizes, const int32_t* k_sizes,
+                       const int32_t* k_offsets, double* error_table, float* stabilizers,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape || !q_centroids || !k_centroids || !k_permuted || !q_sizes || !k_sizes || !k_offsets ||
+      !error_table || !stabilizers || !workspace)
+    return SVGEAR_EINVAL;
+  if (mode != SVGEAR_EST_VALUE_AWARE && mode != SVGEAR_EST_PLAIN) return SVGEAR_EINVAL;
+  if (mode == SVGEAR_EST_VALUE_AWARE && (!v_centroids || !v_permuted)) return SVGEAR_EINVAL;
+  if (!shape_ok(shape)) return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  Carver cv(workspace, workspace_bytes);
+  float* sbar = cv.take<float>((size_t)shape->bh * shape->c_q * shape->c_k);
+  if (!cv.ok) return SVGEAR_EWORKSPACE;
+  return launch_error_table(*shape, mode, q_centroids, k_centroids, v_centroids,
+                            (const bf16*)k_permuted, (const bf16*)v_permuted, q_sizes, k_sizes,
+                            k_offsets, error_table, stabilizers, sbar, (cudaStream_t)stream);
+}
+
+int svgear_route_error_aware(int32_t bh, int32_t c_q, int32_t c_k, const double* error_table,
+                             const int32_t* q_sizes, const int32_t* k_sizes,
+                             int64_t capacity_entries, int32_t overshoot,
+                             int32_t single_item_fallback, uint8_t* mask, int64_t* entries,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  if (!error_table || !q_sizes || !k_sizes || !mask) return SVGEAR_EINVAL;
+  if (capacity_entries < 0) return SVGEAR_EINVAL;
+  if (overshoot != SVGEAR_FILL_REMAINDER && overshoot != SVGEAR_STOP_AT_FIRST_OVERFLOW)
+    return SVGEAR_EINVAL;
+  if (bh < 1 || c_q < 1 || c_k < 1 || c_k > kMaxClusters) return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  return launch_route(bh, c_q, c_k, error_table, q_sizes, k_sizes, capacity_entries, overshoot,
+                      single_item_fallback ? 1 : 0, 0, mask, entries, (cudaStream_t)stream);
+}
+
+int svgear_route_score(const SvgEarShape* shape, const float* q_centroids,
+                       const float* k_centroids, const int32_t* q_sizes, const int32_t* k_sizes,
+                       int64_t capacity_entries, int32_t overshoot, uint8_t* mask,
+                       int64_t* entries, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape || !q_centroids || !k_centroids || !q_sizes || !k_sizes || !mask || !workspace)
+    return SVGEAR_EINVAL;
+  if (capacity_entries < 0) return SVGEAR_EINVAL;
+  if (overshoot != SVGEAR_FILL_REMAINDER && overshoot != SVGEAR_STOP_AT_FIRST_OVERFLOW)
+    return SVGEAR_EINVAL;
+  if (!shape_ok(shape)) return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  Carver cv(workspace, workspace_bytes);
+  double* mass = cv.take<double>((size_t)shape->bh * shape->c_q * shape->c_k);
+  if (!cv.ok) return SVGEAR_EWORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = launch_score_mass(*shape, q_centroids, k_centroids, k_sizes, mass, st);
+  if (rc != SVGEAR_OK) return rc;
+  return launch_route(shape->bh, shape->c_q, shape->c_k, mass, q_sizes, k_sizes, capacity_entries,
+                      overshoot, 0, 1, mask, entries, st);
+}
+
+int svgear_sparse_attend(const SvgEarShape* shape, int32_t exec_mode, const void* q_permuted,
+                         const void* k_permuted, const void* v_permuted, const int32_t* q_perm,
+                         const int32_t* q_sizes, const int32_t* q_offsets, const int32_t* k_sizes,
+                         const int32_t* k_offsets, const float* k_centroids,
+                         const float* v_centroids, const uint8_t* mask, void* out, float* lse,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape || !q_permuted || !k_permuted || !v_permuted || !q_sizes || !q_offsets || !k_sizes ||
+      !k_offsets || !k_centroids || !v_centroids || !mask || !out || !workspace)
+    return SVGEAR_EINVAL;
+  if (exec_mode != SVGEAR_EXEC_BF16_TENSOR && exec_mode != SVGEAR_EXEC_FP32_CHECK)
+    return SVGEAR_EINVAL;
+  if (!shape_ok(shape)) return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  Carver cv(workspace, workspace_bytes);
+  AttendScratch sc;
+  if (!sc.carve(cv, *shape)) return SVGEAR_EWORKSPACE;
+  return launch_attend(*shape, exec_mode, (const bf16*)q_permuted, (const bf16*)k_permuted,
+                       (const bf16*)v_permuted, q_perm, q_sizes, q_offsets, k_sizes, k_offsets,
+                       k_centroids, v_centroids, mask, out, lse, sc, (cudaStream_t)stream);
+}
+
+int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const void* v,
+                   const float* q_init, const float* k_init, int32_t kmeans_iters,
+                   int32_t estimator_mode, int64_t capacity_entries, int32_t overshoot,
+                   int32_t single_item_fallback, int32_t exec_mode, void* out, uint8_t* mask,
+                   const SvgEarAux* aux, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape || !q || !k || !v || !q_init || !k_init || !out || !mask || !workspace)
+    return SVGEAR_EINVAL;
+  if (kmeans_iters < 1 || capacity_entries < 0) return SVGEAR_EINVAL;
+  if (estimator_mode != SVGEAR_EST_VALUE_AWARE && estimator_mode != SVGEAR_EST_PLAIN)
+    return SVGEAR_EINVAL;
+  if (overshoot != SVGEAR_FILL_REMAINDER && overshoot != SVGEAR_STOP_AT_FIRST_OVERFLOW)
+    return SVGEAR_EINVAL;
+  if (exec_mode != SVGEAR_EXEC_BF16_TENSOR && exec_mode != SVGEAR_EXEC_FP32_CHECK)
+    return SVGEAR_EINVAL;
+  if (!shape_ok(shape)) return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  const SvgEarShape& s = *shape;
+  Carver cv(workspace, workspace_bytes);
+  ForwardPlan p;
+  if (!plan_forward(s, cv, p)) return SVGEAR_EWORKSPACE;
+  SvgEarAux a;
+  memset(&a, 0, sizeof(a));
+  if (aux) a = *aux;
+  // aux outputs, when requested, are written in place instead of the workspace copies
+  int32_t* q_assign = a.q_assign ? a.q_assign : p.q_assign;
+  int32_t* k_assign = a.k_assign ? a.k_assign : p.k_assign;
+  int32_t* q_perm = a.q_perm ? a.q_perm : p.q_perm;
+  int32_t* k_perm = a.k_perm ? a.k_perm : p.k_perm;
+  int32_t* q_sizes = a.q_sizes ? a.q_sizes : p.q_sizes;
+  int32_t* k_sizes = a.k_sizes ? a.k_sizes : p.k_sizes;
+  int32_t* q_offsets = a.q_offsets ? a.q_offsets : p.q_offsets;
+  int32_t* k_offsets = a.k_offsets ? a.k_offsets : p.k_offsets;
+  float* q_cent = a.q_centroids ? a.q_centroids : p.q_cent;
+  float* k_cent = a.k_centroids ? a.k_centroids : p.k_cent;
+  float* v_cent = a.v_centroids ? a.v_centroids : p.v_cent;
+  int32_t* q_iters = a.q_iters ? a.q_iters : p.q_iters;
+  int32_t* k_iters = a.k_iters ? a.k_iters : p.k_iters;
+  double* err = a.error_table ? a.error_table : p.err;
+  float* stab = a.stabilizers ? a.stabilizers : p.stab;
+  int64_t* entries = a.mask_entries ? a.mask_entries : p.entries;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  // (1) cluster Q and K independently; V follows K (analysis.py:228-238)
+  rc = launch_kmeans(s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign, q_perm,
+                     q_sizes, q_offsets, q_cent, q_iters, nullptr, p.km, st);
+  if (rc) return rc;
+  rc = launch_kmeans(s.bh, s.n_k, s.d, s.c_k, (const bf16*)k, k_init, kmeans_iters, k_assign, k_perm,
+                     k_sizes, k_offsets, k_cent, k_iters, nullptr, p.km, st);
+  if (rc) return rc;
+  rc = launch_gather_rows(s.bh, s.n_q, s.d, (const bf16*)q, q_perm, p.qp, st);
+  if (rc) return rc;
+  rc = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)k, k_perm, p.kp, st);
+  if (rc) return rc;
+  rc = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)v, k_perm, p.vp, st);
+  if (rc) return rc;
+  rc = launch_segment_means(s.bh, s.n_k, s.d, s.c_k, p.vp, k_sizes, k_offsets, v_cent, nullptr, st);
+  if (rc) return rc;
+  // (2) error table + routing
+  rc = launch_error_table(s, estimator_mode, q_cent, k_cent, v_cent, p.kp, p.vp, q_sizes, k_sizes,
+                          k_offsets, err, stab, p.sbar, st);
+  if (rc) return rc;
+  rc = launch_route(s.bh, s.c_q, s.c_k, err, q_sizes, k_sizes, capacity_entries, overshoot,
+                    single_item_fallback ? 1 : 0, 0, mask, entries, st);
+  if (rc) return rc;
+  // (3) fused executor, output scattered to original token order
+  return launch_attend(s, exec_mode, p.qp, p.kp, p.vp, q_perm, q_sizes, q_offsets, k_sizes, k_offsets,
+                       k_cent, v_cent, mask, out, a.lse, p.at, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,149 @@
+// Shared device/host helpers for libsvgear (sm_100a only).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/svgear.h"
+
+#define SVG_CUDA_OK(call)                       \
+  do {                                          \
+    cudaError_t e__ = (call);                   \
+    if (e__ != cudaSuccess) return SVGEAR_ECUDA; \
+  } while (0)
+
+#define SVG_LAUNCH_OK()                                      \
+  do {                                                       \
+    ++svg::g_launches;                                       \
+    if (cudaPeekAtLastError() != cudaSuccess) {              \
+      (void)cudaGetLastError();                              \
+      return SVGEAR_ECUDA;                                   \
+    }                                                        \
+  } while (0)
+
+namespace svg {
+
+extern long long g_launches;  // diagnostic: kernels launched by this library in this process
+
+typedef __nv_bfloat16 bf16;
+
+constexpr int kMaxClusters = 4096;
+constexpr int kSortChunk = 1024;  // tokens per counting-sort chunk
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Bump allocator over the caller-provided workspace.
+struct Carver {
+  char* base;
+  size_t off;
+  size_t cap;
+  bool ok;
+  __host__ Carver(void* p, size_t bytes) : base((char*)p), off(0), cap(bytes), ok(true) {}
+  template <typename T>
+  __host__ T* take(size_t count) {
+    off = align_up(off, 256);
+    T* r = (T*)(base + off);
+    off += count * sizeof(T);
+    if (off > cap) ok = false;
+    return r;
+  }
+};
+
+__device__ __forceinline__ float bf16_bits_to_float(uint16_t b) {
+  return __uint_as_float(((uint32_t)b) << 16);
+}
+
+// 8 bf16 (one 16-byte chunk) -> 8 floats
+__device__ __forceinline__ void unpack8(const uint4& u, float* f) {
+  f[0] = __uint_as_float(u.x << 16);
+  f[1] = __uint_as_float(u.x & 0xffff0000u);
+  f[2] = __uint_as_float(u.y << 16);
+  f[3] = __uint_as_float(u.y & 0xffff0000u);
+  f[4] = __uint_as_float(u.z << 16);
+  f[5] = __uint_as_float(u.z & 0xffff0000u);
+  f[6] = __uint_as_float(u.w << 16);
+  f[7] = __uint_as_float(u.w & 0xffff0000u);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- stage launchers (defined in the per-stage .cu files) -------------------------------------
+
+struct KmeansScratch {
+  int32_t* prev_assign;   // [bh][n]
+  float* own_d2;          // [bh][n]
+  float* cnorm;           // [bh][c]
+  int32_t* chunk_counts;  // [bh][nchunks][c]
+  double* chunk_inertia;  // [bh][nchunks]
+  int32_t* done;          // [bh]
+  int32_t* changed;       // [bh]
+  static size_t bytes(int bh, int n, int c);
+  bool carve(Carver& cv, int bh, int n, int c);
+};
+
+int launch_kmeans(int bh, int n, int d, int c, const bf16* x, const float* init, int max_iters,
+                  int32_t* assign, int32_t* perm, int32_t* sizes, int32_t* offsets,
+                  float* centroids, int32_t* iters, double* inertia, KmeansScratch& sc,
+                  cudaStream_t st);
+int launch_gather_rows(int bh, int n, int d, const bf16* x, const int32_t* perm, bf16* out,
+                       cudaStream_t st);
+int launch_segment_means(int bh, int n, int d, int c, const bf16* xp, const int32_t* sizes,
+                         const int32_t* offsets, float* means, float* norms, cudaStream_t st);
+
+int launch_error_table(const SvgEarShape& s, int mode, const float* qc, const float* kc,
+                       const float* vc, const bf16* kp, const bf16* vp, const int32_t* q_sizes,
+                       const int32_t* k_sizes, const int32_t* k_offsets, double* err,
+                       float* stabilizers, float* sbar, cudaStream_t st);
+
+struct RouteScratch {
+  int32_t* state;  // per-head scratch ints
+  static size_t bytes(int bh) { return align_up((size_t)bh * 64 * sizeof(int32_t), 256); }
+};
+int launch_route(int bh, int c_q, int c_k, const double* val, const int32_t* q_sizes,
+                 const int32_t* k_sizes, int64_t capacity, int overshoot, int fallback,
+                 int ratio_mode, uint8_t* mask, int64_t* entries, cudaStream_t st);
+int launch_score_mass(const SvgEarShape& s, const float* qc, const float* kc,
+                      const int32_t* k_sizes, double* mass, cudaStream_t st);
+
+struct AttendScratch {
+  int32_t* tile_list;   // [bh][max_tiles][4]  (q-cluster, first row, rows, pad)
+  int32_t* tile_count;  // [bh]
+  bf16* kbar_bf16;      // [bh][ckpad][d]
+  bf16* vbar_bf16;      // [bh][ckpad][d]
+  float* lnw;           // [bh][c_k]
+  static int max_tiles(int n_q, int c_q, int rows) { return ceil_div(n_q, rows) + c_q; }
+  static size_t bytes(const SvgEarShape& s);
+  bool carve(Carver& cv, const SvgEarShape& s);
+};
+int launch_attend(const SvgEarShape& s, int exec_mode, const bf16* qp, const bf16* kp,
+                  const bf16* vp, const int32_t* q_perm, const int32_t* q_sizes,
+                  const int32_t* q_offsets, const int32_t* k_sizes, const int32_t* k_offsets,
+                  const float* kc, const float* vc, const uint8_t* mask, void* out, float* lse,
+                  AttendScratch& sc, cudaStream_t st);
+// tcgen05 path (attend_tc.cu)
+int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const bf16* vp,
+                     const int32_t* q_perm, const int32_t* k_sizes, const int32_t* k_offsets,
+                     const uint8_t* mask, bf16* out, float* lse, AttendScratch& sc,
+                     cudaStream_t st);
+
+}  // namespace svg

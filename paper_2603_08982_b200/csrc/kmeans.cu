@@ -1,0 +1,507 @@
+// Batched Lloyd k-means + stable cluster-contiguous permutation (subsystem 1).
+//
+// Reference semantics: /root/reference/pkg/src/routedattn/clustering.py
+//   _sq_dists  :55-62   d2 = max(|x|^2 - 2 x.c + |c|^2, 0)
+//   _lloyd     :104-141 argmin (ties -> lowest index), bincount, empty-cluster repair,
+//                       convergence test BEFORE the centroid update, member-mean update
+//   kmeans     :193-198 final centroids = member means, permutation = stable argsort, offsets
+//
+// One launch sequence per Lloyd iteration, all `bh` instances batched in grid.y; instances that
+// have converged set done[h] and every later kernel returns immediately for them.  No
+// floating-point atomics anywhere: counts use integer atomics, means/inertia use fixed-order
+// reductions, so results are deterministic run to run.
+#include "common.cuh"
+
+namespace svg {
+
+// ------------------------------------------------------------------------------------------------
+// centroid squared norms
+// ------------------------------------------------------------------------------------------------
+__global__ void centroid_norm_kernel(const float* __restrict__ cent, int d, int total,
+                                     float* __restrict__ cnorm) {
+  int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  int lane = threadIdx.x & 31;
+  if (row >= total) return;
+  const float* p = cent + (size_t)row * d;
+  float s = 0.f;
+  for (int k = lane; k < d; k += 32) s = fmaf(p[k], p[k], s);
+  s = warp_sum(s);
+  if (lane == 0) cnorm[row] = s;
+}
+
+// ------------------------------------------------------------------------------------------------
+// assignment, fp32 CUDA-core version: one thread per token, token row in registers, centroid tiles
+// broadcast from shared memory.  (The tcgen05 version lives in kmeans_tc.cu.)
+// ------------------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(128)
+    assign_fp32_kernel(const bf16* __restrict__ x, const float* __restrict__ cent,
+                       const float* __restrict__ cnorm, int n, int c, int32_t* __restrict__ assign,
+                       float* __restrict__ own_d2, int32_t* __restrict__ sizes,
+                       int32_t* __restrict__ changed, const int32_t* __restrict__ done) {
+  const int h = blockIdx.y;
+  if (done[h]) return;
+  constexpr int TC = 32;
+  __shared__ float4 sc[TC][D / 4];
+  __shared__ float scn[TC];
+  const int tid = threadIdx.x;
+  const int t = blockIdx.x * 128 + tid;
+  const int tt = min(t, n - 1);
+
+  if (blockIdx.x == 0) {  // reset the per-iteration counters of this instance
+    for (int j = tid; j < c; j += 128) sizes[(size_t)h * c + j] = 0;
+    if (tid == 0) changed[h] = 0;
+  }
+
+  float xr[D];
+  {
+    const uint4* xp = reinterpret_cast<const uint4*>(x + ((size_t)h * n + tt) * D);
+#pragma unroll
+    for (int i = 0; i < D / 8; ++i) {
+      uint4 u = __ldg(xp + i);
+      unpack8(u, xr + 8 * i);
+    }
+  }
+  float xn = 0.f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) xn = fmaf(xr[k], xr[k], xn);
+
+  float best = INFINITY;
+  int bi = 0;
+  const float* ch = cent + (size_t)h * c * D;
+  for (int c0 = 0; c0 < c; c0 += TC) {
+    __syncthreads();
+    for (int i = tid; i < TC * (D / 4); i += 128) {
+      int r = i / (D / 4), q = i % (D / 4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c0 + r < c) v = __ldg(reinterpret_cast<const float4*>(ch + (size_t)(c0 + r) * D) + q);
+      sc[r][q] = v;
+    }
+    if (tid < TC) scn[tid] = (c0 + tid < c) ? cnorm[(size_t)h * c + c0 + tid] : 0.f;
+    __syncthreads();
+    const int lim = min(TC, c - c0);
+    for (int r = 0; r < lim; r += 4) {
+      float d0 = 0.f, d1 = 0.f, d2 = 0.f, d3 = 0.f;
+#pragma unroll
+      for (int q = 0; q < D / 4; ++q) {
+        float4 a0 = sc[r][q], a1 = sc[r + 1][q], a2 = sc[r + 2][q], a3 = sc[r + 3][q];
+        d0 = fmaf(xr[4 * q], a0.x, d0); d0 = fmaf(xr[4 * q + 1], a0.y, d0);
+        d0 = fmaf(xr[4 * q + 2], a0.z, d0); d0 = fmaf(xr[4 * q + 3], a0.w, d0);
+        d1 = fmaf(xr[4 * q], a1.x, d1); d1 = fmaf(xr[4 * q + 1], a1.y, d1);
+        d1 = fmaf(xr[4 * q + 2], a1.z, d1); d1 = fmaf(xr[4 * q + 3], a1.w, d1);
+        d2 = fmaf(xr[4 * q], a2.x, d2); d2 = fmaf(xr[4 * q + 1], a2.y, d2);
+        d2 = fmaf(xr[4 * q + 2], a2.z, d2); d2 = fmaf(xr[4 * q + 3], a2.w, d2);
+        d3 = fmaf(xr[4 * q], a3.x, d3); d3 = fmaf(xr[4 * q + 1], a3.y, d3);
+        d3 = fmaf(xr[4 * q + 2], a3.z, d3); d3 = fmaf(xr[4 * q + 3], a3.w, d3);
+      }
+      float dd[4] = {d0, d1, d2, d3};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (r + u < lim) {
+          // same association as the reference: (|x|^2 - 2 x.c) + |c|^2, clipped at zero
+          float v = fmaxf((xn - 2.0f * dd[u]) + scn[r + u], 0.f);
+          if (v < best) {  // strict: ties keep the lowest cluster index
+            best = v;
+            bi = c0 + r + u;
+          }
+        }
+      }
+    }
+  }
+  if (t < n) {
+    assign[(size_t)h * n + t] = bi;
+    own_d2[(size_t)h * n + t] = best;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// cluster sizes (integer atomics -> deterministic)
+// ------------------------------------------------------------------------------------------------
+__global__ void sizes_hist_kernel(const int32_t* __restrict__ assign, int n, int c,
+                                  int32_t* __restrict__ sizes, const int32_t* __restrict__ done) {
+  const int h = blockIdx.y;
+  if (done[h]) return;
+  extern __shared__ int32_t hist[];
+  for (int j = threadIdx.x; j < c; j += blockDim.x) hist[j] = 0;
+  __syncthreads();
+  const int per_block = ceil_div(n, gridDim.x);
+  const int lo = blockIdx.x * per_block, hi = min(n, lo + per_block);
+  for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) atomicAdd(&hist[assign[(size_t)h * n + t]], 1);
+  __syncthreads();
+  for (int j = threadIdx.x; j < c; j += blockDim.x)
+    if (hist[j]) atomicAdd(&sizes[(size_t)h * c + j], hist[j]);
+}
+
+// ------------------------------------------------------------------------------------------------
+// empty-cluster repair (clustering.py:116-124): for each empty cluster in ascending order move the
+// token with the largest own distance (first maximum) among clusters of size >= 2.
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024)
+    repair_kernel(int n, int c, int32_t* __restrict__ assign_all, float* __restrict__ own_all,
+                  int32_t* __restrict__ sizes_all, const int32_t* __restrict__ done) {
+  const int h = blockIdx.x;
+  if (done[h]) return;
+  int32_t* assign = assign_all + (size_t)h * n;
+  float* own = own_all + (size_t)h * n;
+  int32_t* sizes = sizes_all + (size_t)h * c;
+  __shared__ float s_val[32];
+  __shared__ int s_idx[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  int local = 0;
+  for (int j = tid; j < c; j += blockDim.x) local |= (sizes[j] == 0);
+  if (!__syncthreads_or(local)) return;
+
+  for (int e = 0; e < c; ++e) {
+    __syncthreads();
+    if (sizes[e] != 0) continue;  // block-uniform
+    float bv = -1.f;
+    int bx = 0x7fffffff;
+    for (int t = tid; t < n; t += blockDim.x) {
+      if (sizes[assign[t]] >= 2) {
+        float v = own[t];
+        if (v > bv) { bv = v; bx = t; }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int ox = __shfl_xor_sync(0xffffffffu, bx, o);
+      if (ov > bv || (ov == bv && ox < bx)) { bv = ov; bx = ox; }
+    }
+    if (lane == 0) { s_val[warp] = bv; s_idx[warp] = bx; }
+    __syncthreads();
+    if (warp == 0) {
+      int nw = blockDim.x >> 5;
+      bv = lane < nw ? s_val[lane] : -1.f;
+      bx = lane < nw ? s_idx[lane] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        int ox = __shfl_xor_sync(0xffffffffu, bx, o);
+        if (ov > bv || (ov == bv && ox < bx)) { bv = ov; bx = ox; }
+      }
+      if (lane == 0 && bx != 0x7fffffff) {
+        sizes[assign[bx]] -= 1;
+        sizes[e] += 1;
+        assign[bx] = e;
+        own[bx] = 0.f;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// per-chunk histogram + convergence compare + inertia partials
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    chunk_hist_kernel(const int32_t* __restrict__ assign, int32_t* __restrict__ prev,
+                      const float* __restrict__ own, int n, int c, int nchunks, int iter,
+                      int32_t* __restrict__ chunk_counts, double* __restrict__ chunk_inertia,
+                      int32_t* __restrict__ changed, const int32_t* __restrict__ done) {
+  const int h = blockIdx.y;
+  if (done[h]) return;
+  extern __shared__ int32_t hist[];
+  __shared__ double s_part[8];
+  const int tid = threadIdx.x;
+  for (int j = tid; j < c; j += 256) hist[j] = 0;
+  __syncthreads();
+  const int lo = blockIdx.x * kSortChunk, hi = min(n, lo + kSortChunk);
+  int diff = 0;
+  double dsum = 0.0;
+  for (int t = lo + tid; t < hi; t += 256) {
+    size_t g = (size_t)h * n + t;
+    int a = assign[g];
+    atomicAdd(&hist[a], 1);
+    if (iter > 0) diff |= (prev[g] != a);
+    prev[g] = a;
+    dsum += (double)own[g];
+  }
+  diff = __syncthreads_or(diff);
+  if (tid == 0 && diff) atomicOr(&changed[h], 1);
+  int32_t* out = chunk_counts + ((size_t)h * nchunks + blockIdx.x) * c;
+  for (int j = tid; j < c; j += 256) out[j] = hist[j];
+  dsum = warp_sum(dsum);
+  if ((tid & 31) == 0) s_part[tid >> 5] = dsum;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += s_part[w];
+    chunk_inertia[(size_t)h * nchunks + blockIdx.x] = s;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// offsets (exclusive scan of sizes), per-chunk scatter bases, inertia, convergence decision
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024)
+    scan_kernel(int n, int c, int nchunks, int iter, const int32_t* __restrict__ sizes_all,
+                int32_t* __restrict__ offsets_all, int32_t* __restrict__ chunk_counts,
+                const double* __restrict__ chunk_inertia, double* __restrict__ inertia,
+                int32_t* __restrict__ iters, const int32_t* __restrict__ changed,
+                int32_t* __restrict__ done) {
+  const int h = blockIdx.x;
+  if (done[h]) return;
+  const int32_t* sizes = sizes_all + (size_t)h * c;
+  int32_t* offsets = offsets_all + (size_t)h * c;
+  __shared__ int s_warp[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int PER = kMaxClusters / 1024;  // 4 consecutive clusters per thread
+  int v[PER], tot = 0;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    int j = tid * PER + u;
+    v[u] = j < c ? sizes[j] : 0;
+    tot += v[u];
+  }
+  int inc = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int w = s_warp[lane], wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    s_warp[lane] = wi - w;  // exclusive warp base
+  }
+  __syncthreads();
+  int run = s_warp[warp] + inc - tot;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    int j = tid * PER + u;
+    if (j < c) {
+      offsets[j] = run;
+      int base = run;
+      int32_t* col = chunk_counts + (size_t)h * nchunks * c + j;
+      for (int chn = 0; chn < nchunks; ++chn) {
+        int cnt = col[(size_t)chn * c];
+        col[(size_t)chn * c] = base;
+        base += cnt;
+      }
+    }
+    run += v[u];
+  }
+  if (tid == 0) {
+    double s = 0.0;
+    for (int chn = 0; chn < nchunks; ++chn) s += chunk_inertia[(size_t)h * nchunks + chn];
+    if (inertia) inertia[h] = s;
+    if (iters) iters[h] = iter + 1;
+    if (iter > 0 && !changed[h]) done[h] = 1;  // assignments unchanged -> converged
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// stable scatter: perm[base[cluster] + rank among earlier same-cluster tokens] = token
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    scatter_perm_kernel(const int32_t* __restrict__ assign, int n, int c, int nchunks,
+                        const int32_t* __restrict__ chunk_base, int32_t* __restrict__ perm,
+                        const int32_t* __restrict__ done) {
+  const int h = blockIdx.y;
+  if (done[h]) return;
+  extern __shared__ int32_t cnt[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t* base_in = chunk_base + ((size_t)h * nchunks + blockIdx.x) * c;
+  for (int j = tid; j < c; j += 256) cnt[j] = base_in[j];
+  __syncthreads();
+  for (int r = 0; r < kSortChunk / 256; ++r) {
+    const int t = blockIdx.x * kSortChunk + r * 256 + tid;
+    const bool valid = t < n;
+    const int a = valid ? assign[(size_t)h * n + t] : (0x7fffff00 | lane);
+    const unsigned m = __match_any_sync(0xffffffffu, a);
+    const int leader = __ffs(m) - 1;
+    const int rank = __popc(m & ((1u << lane) - 1u));
+    int base = 0;
+    for (int w = 0; w < 8; ++w) {
+      if (warp == w && valid && lane == leader) {
+        base = cnt[a];
+        cnt[a] = base + __popc(m);
+      }
+      __syncthreads();
+    }
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (valid) perm[(size_t)h * n + base + rank] = t;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// member means in ascending row order, float64 accumulation, one rounding to f32.
+// perm == nullptr means `x` is already cluster-contiguous (segment_means).
+// ------------------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(128)
+    cluster_mean_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ perm, int n, int c,
+                        const int32_t* __restrict__ sizes, const int32_t* __restrict__ offsets,
+                        float* __restrict__ means, float* __restrict__ norms,
+                        const int32_t* __restrict__ done) {
+  const int h = blockIdx.y;
+  if (done && done[h]) return;
+  const int j = blockIdx.x;
+  constexpr int EPL = D / 32;
+  __shared__ double part[4][D];
+  __shared__ float s_c[D];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nj = sizes[(size_t)h * c + j], o = offsets[(size_t)h * c + j];
+  double acc[EPL];
+#pragma unroll
+  for (int u = 0; u < EPL; ++u) acc[u] = 0.0;
+  for (int r = warp; r < nj; r += 4) {
+    const int row = perm ? perm[(size_t)h * n + o + r] : (o + r);
+    const bf16* p = x + ((size_t)h * n + row) * D + lane * EPL;
+    if (EPL == 4) {
+      uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+      acc[0] += (double)__uint_as_float(u.x << 16);
+      acc[1] += (double)__uint_as_float(u.x & 0xffff0000u);
+      acc[2] += (double)__uint_as_float(u.y << 16);
+      acc[3] += (double)__uint_as_float(u.y & 0xffff0000u);
+    } else {
+      uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(p));
+      acc[0] += (double)__uint_as_float(u << 16);
+      acc[1] += (double)__uint_as_float(u & 0xffff0000u);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < EPL; ++u) part[warp][lane * EPL + u] = acc[u];
+  __syncthreads();
+  if (tid < D) {
+    float* out = means + ((size_t)h * c + j) * D;
+    float m;
+    if (nj > 0) {
+      double s = (part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]);
+      m = (float)(s / (double)nj);
+      out[tid] = m;
+    } else {
+      m = out[tid];
+    }
+    s_c[tid] = m;
+  }
+  __syncthreads();
+  if (norms && warp == 0) {
+    float s = 0.f;
+    for (int k = lane; k < D; k += 32) s = fmaf(s_c[k], s_c[k], s);
+    s = warp_sum(s);
+    if (lane == 0) norms[(size_t)h * c + j] = s;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// row gather (permute_rows): 16-byte chunks
+// ------------------------------------------------------------------------------------------------
+__global__ void gather_rows_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ perm,
+                                   int n, int chunks_per_row, uint4* __restrict__ out) {
+  const int h = blockIdx.y;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)n * chunks_per_row) return;
+  const int row = (int)(idx / chunks_per_row), ch = (int)(idx % chunks_per_row);
+  const int src = perm[(size_t)h * n + row];
+  out[((size_t)h * n + row) * chunks_per_row + ch] =
+      __ldg(x + ((size_t)h * n + src) * chunks_per_row + ch);
+}
+
+// ------------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------------
+size_t KmeansScratch::bytes(int bh, int n, int c) {
+  const int nchunks = ceil_div(n, kSortChunk);
+  size_t b = 0;
+  b += align_up((size_t)bh * n * 4, 256) * 2;           // prev_assign, own_d2
+  b += align_up((size_t)bh * c * 4, 256);               // cnorm
+  b += align_up((size_t)bh * nchunks * c * 4, 256);     // chunk_counts
+  b += align_up((size_t)bh * nchunks * 8, 256);         // chunk_inertia
+  b += align_up((size_t)bh * 4, 256) * 2;               // done, changed
+  return b + 2048;
+}
+
+bool KmeansScratch::carve(Carver& cv, int bh, int n, int c) {
+  const int nchunks = ceil_div(n, kSortChunk);
+  prev_assign = cv.take<int32_t>((size_t)bh * n);
+  own_d2 = cv.take<float>((size_t)bh * n);
+  cnorm = cv.take<float>((size_t)bh * c);
+  chunk_counts = cv.take<int32_t>((size_t)bh * nchunks * c);
+  chunk_inertia = cv.take<double>((size_t)bh * nchunks);
+  done = cv.take<int32_t>(bh);
+  changed = cv.take<int32_t>(bh);
+  return cv.ok;
+}
+
+int launch_kmeans_assign_tc(int bh, int n, int d, int c, const bf16* x, const float* cent,
+                            const float* cnorm, int32_t* assign, float* own_d2, int32_t* sizes,
+                            int32_t* changed, const int32_t* done, cudaStream_t st);
+
+int launch_kmeans(int bh, int n, int d, int c, const bf16* x, const float* init, int max_iters,
+                  int32_t* assign, int32_t* perm, int32_t* sizes, int32_t* offsets,
+                  float* centroids, int32_t* iters, double* inertia, KmeansScratch& sc,
+                  cudaStream_t st) {
+  const int nchunks = ceil_div(n, kSortChunk);
+  SVG_CUDA_OK(cudaMemcpyAsync(centroids, init, (size_t)bh * c * d * sizeof(float),
+                              cudaMemcpyDeviceToDevice, st));
+  SVG_CUDA_OK(cudaMemsetAsync(sc.done, 0, (size_t)bh * 4, st));
+  SVG_CUDA_OK(cudaMemsetAsync(sc.changed, 0, (size_t)bh * 4, st));
+  centroid_norm_kernel<<<ceil_div(bh * c, 8), 256, 0, st>>>(centroids, d, bh * c, sc.cnorm);
+  SVG_LAUNCH_OK();
+  const size_t hist_smem = (size_t)c * sizeof(int32_t);
+  const int hist_blocks = max(1, min(64, ceil_div(n, 4096)));
+  for (int it = 0; it < max_iters; ++it) {
+    dim3 ga(ceil_div(n, 128), bh);
+    if (d == 128)
+      assign_fp32_kernel<128><<<ga, 128, 0, st>>>(x, centroids, sc.cnorm, n, c, assign, sc.own_d2,
+                                                  sizes, sc.changed, sc.done);
+    else
+      assign_fp32_kernel<64><<<ga, 128, 0, st>>>(x, centroids, sc.cnorm, n, c, assign, sc.own_d2,
+                                                 sizes, sc.changed, sc.done);
+    SVG_LAUNCH_OK();
+    sizes_hist_kernel<<<dim3(hist_blocks, bh), 256, hist_smem, st>>>(assign, n, c, sizes, sc.done);
+    SVG_LAUNCH_OK();
+    repair_kernel<<<bh, 1024, 0, st>>>(n, c, assign, sc.own_d2, sizes, sc.done);
+    SVG_LAUNCH_OK();
+    chunk_hist_kernel<<<dim3(nchunks, bh), 256, hist_smem, st>>>(
+        assign, sc.prev_assign, sc.own_d2, n, c, nchunks, it, sc.chunk_counts, sc.chunk_inertia,
+        sc.changed, sc.done);
+    SVG_LAUNCH_OK();
+    scan_kernel<<<bh, 1024, 0, st>>>(n, c, nchunks, it, sizes, offsets, sc.chunk_counts,
+                                     sc.chunk_inertia, inertia, iters, sc.changed, sc.done);
+    SVG_LAUNCH_OK();
+    scatter_perm_kernel<<<dim3(nchunks, bh), 256, hist_smem, st>>>(assign, n, c, nchunks,
+                                                                   sc.chunk_counts, perm, sc.done);
+    SVG_LAUNCH_OK();
+    if (d == 128)
+      cluster_mean_kernel<128><<<dim3(c, bh), 128, 0, st>>>(x, perm, n, c, sizes, offsets,
+                                                           centroids, sc.cnorm, sc.done);
+    else
+      cluster_mean_kernel<64><<<dim3(c, bh), 128, 0, st>>>(x, perm, n, c, sizes, offsets,
+                                                          centroids, sc.cnorm, sc.done);
+    SVG_LAUNCH_OK();
+  }
+  return SVGEAR_OK;
+}
+
+int launch_gather_rows(int bh, int n, int d, const bf16* x, const int32_t* perm, bf16* out,
+                       cudaStream_t st) {
+  const int cpr = d / 8;
+  const long long total = (long long)n * cpr;
+  gather_rows_kernel<<<dim3((unsigned)((total + 255) / 256), bh), 256, 0, st>>>(
+      reinterpret_cast<const uint4*>(x), perm, n, cpr, reinterpret_cast<uint4*>(out));
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
+int launch_segment_means(int bh, int n, int d, int c, const bf16* xp, const int32_t* sizes,
+                         const int32_t* offsets, float* means, float* norms, cudaStream_t st) {
+  if (d == 128)
+    cluster_mean_kernel<128><<<dim3(c, bh), 128, 0, st>>>(xp, nullptr, n, c, sizes, offsets, means,
+                                                         norms, nullptr);
+  else
+    cluster_mean_kernel<64><<<dim3(c, bh), 128, 0, st>>>(xp, nullptr, n, c, sizes, offsets, means,
+                                                        norms, nullptr);
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
+}  // namespace svg

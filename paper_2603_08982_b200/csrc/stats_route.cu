@@ -1,0 +1,518 @@
+// Block statistics, the value-aware error table and budgeted routing (subsystem 2).
+//
+// Reference semantics:
+//   estimator.estimate_errors_streaming  estimator.py:187-253   (value-aware, Eq.8)
+//   estimator.estimate_errors            estimator.py:120-148   (plain, Eq.5)
+//   estimator.to_ratios                  estimator.py:83-96     order (-ratio,-error,qc,kc)
+//   router._greedy_fill                  router.py:100-110
+//   router._apply_single_item_fallback   router.py:113-121
+//   router.route_score                   router.py:253-280
+//
+// Error table arithmetic.  With g_it = (q̄_i.(k_t - k̄_j))/sqrt(d) for key t of cluster j,
+//   || w̄_ij v̄_j - e_it v_t ||^2 = w̄_ij^2 || (v̄_j - v_t) - expm1(g_it) v_t ||^2
+//                                = w̄_ij^2 ( A_t - 2 x B_t + x^2 C_t ),   x = expm1(g_it)
+// with per-key scalars A_t = |v̄_j - v_t|^2, B_t = (v̄_j - v_t).v_t, C_t = |v_t|^2 that do not
+// depend on the query cluster.  This is the reference's quantity exactly (w̄ = exp(s̄_ij - m_ref),
+// e = exp(logit - m_ref) = w̄ exp(g)), but evaluated from DIFFERENCES so that fp32 keeps the
+// small residuals of tight clusters; a running maximum M of g (the reference's m_loc - s̄_ij)
+// keeps every exponential <= 1, and the final rescale exp(2(s̄_ij - m_ref + M)) is applied in
+// float64, the type of the reference's table.
+#include "common.cuh"
+
+namespace svg {
+
+// ------------------------------------------------------------------------------------------------
+// centroid logits s̄ = q̄ k̄^T / sqrt(d) and their row maxima (estimator.py:216-217)
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    centroid_logits_kernel(const float* __restrict__ qc, const float* __restrict__ kc, int d,
+                           int c_q, int c_k, float scale, float* __restrict__ sbar,
+                           float* __restrict__ mref) {
+  const int h = blockIdx.y, i = blockIdx.x;
+  __shared__ float sq[128];
+  __shared__ float smax[8];
+  const int tid = threadIdx.x;
+  if (tid < d) sq[tid] = qc[((size_t)h * c_q + i) * d + tid];
+  __syncthreads();
+  float mx = -INFINITY;
+  for (int j = tid; j < c_k; j += 256) {
+    const float4* kp = reinterpret_cast<const float4*>(kc + ((size_t)h * c_k + j) * d);
+    float s = 0.f;
+    for (int q = 0; q < d / 4; ++q) {
+      float4 kv = __ldg(kp + q);
+      s = fmaf(sq[4 * q], kv.x, s);
+      s = fmaf(sq[4 * q + 1], kv.y, s);
+      s = fmaf(sq[4 * q + 2], kv.z, s);
+      s = fmaf(sq[4 * q + 3], kv.w, s);
+    }
+    s *= scale;
+    sbar[((size_t)h * c_q + i) * c_k + j] = s;
+    mx = fmaxf(mx, s);
+  }
+  mx = warp_max(mx);
+  if ((tid & 31) == 0) smax[tid >> 5] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < 8; ++w) mx = fmaxf(mx, smax[w]);
+    mref[(size_t)h * c_q + i] = mx;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// error table: one block per key cluster; thread <-> query cluster (q̄_i in registers); key tiles
+// of 32 rows staged in shared memory as fp32 differences k_t - k̄_j.
+// ------------------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    error_table_kernel(int mode, const float* __restrict__ qc, const float* __restrict__ kc,
+                       const float* __restrict__ vc, const bf16* __restrict__ kp,
+                       const bf16* __restrict__ vp, const int32_t* __restrict__ q_sizes,
+                       const int32_t* __restrict__ k_sizes, const int32_t* __restrict__ k_offsets,
+                       const float* __restrict__ sbar, const float* __restrict__ mref, int n_k,
+                       int c_q, int c_k, float scale, double* __restrict__ err) {
+  constexpr int TK = 32;
+  const int h = blockIdx.y, j = blockIdx.x;
+  __shared__ float4 skd[TK][D / 4];  // k_t - k̄_j
+  __shared__ float sA[TK], sB[TK], sC[TK];
+  __shared__ float skb[D], svb[D];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nj = k_sizes[(size_t)h * c_k + j], o = k_offsets[(size_t)h * c_k + j];
+  if (tid < D) {
+    skb[tid] = kc[((size_t)h * c_k + j) * D + tid];
+    svb[tid] = (mode == SVGEAR_EST_VALUE_AWARE) ? vc[((size_t)h * c_k + j) * D + tid] : 0.f;
+  }
+  __syncthreads();
+
+  const int nthr = blockDim.x, nwarp = blockDim.x >> 5;
+  for (int ibase = 0; ibase < c_q; ibase += nthr) {
+    const int i = ibase + tid;
+    const bool act = i < c_q;
+    float qr[D];
+    {
+      const float4* qp = reinterpret_cast<const float4*>(qc + ((size_t)h * c_q + (act ? i : 0)) * D);
+#pragma unroll
+      for (int q = 0; q < D / 4; ++q) {
+        float4 v = __ldg(qp + q);
+        qr[4 * q] = v.x; qr[4 * q + 1] = v.y; qr[4 * q + 2] = v.z; qr[4 * q + 3] = v.w;
+      }
+    }
+    float M = 0.f;    // running max(0, g)
+    float acc = 0.f;  // sum at scale exp(-2M)
+    for (int t0 = 0; t0 < nj; t0 += TK) {
+      const int nt = min(TK, nj - t0);
+      __syncthreads();
+      // stage the tile: each warp takes rows warp, warp+8, ...; lanes split the row
+      for (int r = warp; r < TK; r += nwarp) {
+        float a = 0.f, b = 0.f, cc = 0.f;
+        if (r < nt) {
+          const size_t row = (size_t)h * n_k + o + t0 + r;
+          constexpr int EPL = D / 32;
+          float kf[EPL], vf[EPL];
+          if (EPL == 4) {
+            uint2 ku = __ldg(reinterpret_cast<const uint2*>(kp + row * D + lane * 4));
+            kf[0] = __uint_as_float(ku.x << 16); kf[1] = __uint_as_float(ku.x & 0xffff0000u);
+            kf[2] = __uint_as_float(ku.y << 16); kf[3] = __uint_as_float(ku.y & 0xffff0000u);
+            if (mode == SVGEAR_EST_VALUE_AWARE) {
+              uint2 vu = __ldg(reinterpret_cast<const uint2*>(vp + row * D + lane * 4));
+              vf[0] = __uint_as_float(vu.x << 16); vf[1] = __uint_as_float(vu.x & 0xffff0000u);
+              vf[2] = __uint_as_float(vu.y << 16); vf[3] = __uint_as_float(vu.y & 0xffff0000u);
+            }
+          } else {
+            uint32_t ku = __ldg(reinterpret_cast<const uint32_t*>(kp + row * D + lane * 2));
+            kf[0] = __uint_as_float(ku << 16); kf[1] = __uint_as_float(ku & 0xffff0000u);
+            if (mode == SVGEAR_EST_VALUE_AWARE) {
+              uint32_t vu = __ldg(reinterpret_cast<const uint32_t*>(vp + row * D + lane * 2));
+              vf[0] = __uint_as_float(vu << 16); vf[1] = __uint_as_float(vu & 0xffff0000u);
+            }
+          }
+          float* dst = reinterpret_cast<float*>(&skd[r][0]) + lane * EPL;
+#pragma unroll
+          for (int u = 0; u < EPL; ++u) {
+            dst[u] = kf[u] - skb[lane * EPL + u];
+            if (mode == SVGEAR_EST_VALUE_AWARE) {
+              float dv = svb[lane * EPL + u] - vf[u];
+              a = fmaf(dv, dv, a);
+              b = fmaf(dv, vf[u], b);
+              cc = fmaf(vf[u], vf[u], cc);
+            }
+          }
+          a = warp_sum(a); b = warp_sum(b); cc = warp_sum(cc);
+          if (mode != SVGEAR_EST_VALUE_AWARE) { a = 0.f; b = 0.f; cc = 1.f; }
+        } else {
+          float* dst = reinterpret_cast<float*>(&skd[r][0]) + lane * (D / 32);
+#pragma unroll
+          for (int u = 0; u < D / 32; ++u) dst[u] = 0.f;
+        }
+        if (lane == 0) { sA[r] = a; sB[r] = b; sC[r] = cc; }
+      }
+      __syncthreads();
+      if (act) {
+        for (int t = 0; t < nt; ++t) {
+          float g0 = 0.f, g1 = 0.f;
+#pragma unroll
+          for (int q = 0; q < D / 4; q += 2) {
+            float4 k0 = skd[t][q], k1 = skd[t][q + 1];
+            g0 = fmaf(qr[4 * q], k0.x, g0); g0 = fmaf(qr[4 * q + 1], k0.y, g0);
+            g0 = fmaf(qr[4 * q + 2], k0.z, g0); g0 = fmaf(qr[4 * q + 3], k0.w, g0);
+            g1 = fmaf(qr[4 * q + 4], k1.x, g1); g1 = fmaf(qr[4 * q + 5], k1.y, g1);
+            g1 = fmaf(qr[4 * q + 6], k1.z, g1); g1 = fmaf(qr[4 * q + 7], k1.w, g1);
+          }
+          const float g = (g0 + g1) * scale;
+          if (g > M) {
+            const float r = expf(M - g);
+            acc *= r * r;
+            M = g;
+          }
+          const float em = expf(-M);          // 1 when M == 0
+          const float xs = (g < 20.f) ? expm1f(g) * em : (expf(g - M) - em);
+          acc += (sA[t] * em) * em - 2.f * (em * xs) * sB[t] + (xs * xs) * sC[t];
+        }
+      }
+    }
+    if (act) {
+      const size_t e = ((size_t)h * c_q + i) * c_k + j;
+      const double lift = 2.0 * ((double)sbar[e] - (double)mref[(size_t)h * c_q + i] + (double)M);
+      double v = (double)fmaxf(acc, 0.f) * exp(lift);
+      err[e] = (double)q_sizes[(size_t)h * c_q + i] * v;
+    }
+  }
+}
+
+int launch_error_table(const SvgEarShape& s, int mode, const float* qc, const float* kc,
+                       const float* vc, const bf16* kp, const bf16* vp, const int32_t* q_sizes,
+                       const int32_t* k_sizes, const int32_t* k_offsets, double* err,
+                       float* stabilizers, float* sbar, cudaStream_t st) {
+  const float scale = 1.0f / sqrtf((float)s.d);
+  centroid_logits_kernel<<<dim3(s.c_q, s.bh), 256, 0, st>>>(qc, kc, s.d, s.c_q, s.c_k, scale, sbar,
+                                                           stabilizers);
+  SVG_LAUNCH_OK();
+  const int passes = ceil_div(s.c_q, 256);
+  const int thr = min(256, max(128, ceil_div(ceil_div(s.c_q, passes), 32) * 32));
+  if (s.d == 128)
+    error_table_kernel<128><<<dim3(s.c_k, s.bh), thr, 0, st>>>(
+        mode, qc, kc, vc, kp, vp, q_sizes, k_sizes, k_offsets, sbar, stabilizers, s.n_k, s.c_q,
+        s.c_k, scale, err);
+  else
+    error_table_kernel<64><<<dim3(s.c_k, s.bh), thr, 0, st>>>(
+        mode, qc, kc, vc, kp, vp, q_sizes, k_sizes, k_offsets, sbar, stabilizers, s.n_k, s.c_q,
+        s.c_k, scale, err);
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// cluster mass for score routing: row softmax of s̄ + ln|k_c| in float64 (router.py:193-206,267)
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+    score_mass_kernel(const float* __restrict__ qc, const float* __restrict__ kc,
+                      const int32_t* __restrict__ k_sizes, int d, int c_q, int c_k, double scale,
+                      double* __restrict__ mass) {
+  const int h = blockIdx.y, i = blockIdx.x;
+  __shared__ double sq[128];
+  __shared__ double sred[8];
+  __shared__ double s_bcast;
+  const int tid = threadIdx.x;
+  if (tid < d) sq[tid] = (double)qc[((size_t)h * c_q + i) * d + tid];
+  __syncthreads();
+  double* row = mass + ((size_t)h * c_q + i) * c_k;
+  double mx = -INFINITY;
+  for (int j = tid; j < c_k; j += 256) {
+    const float* kp = kc + ((size_t)h * c_k + j) * d;
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) s = fma(sq[k], (double)__ldg(kp + k), s);
+    s = s * scale + log((double)k_sizes[(size_t)h * c_k + j]);
+    row[j] = s;
+    mx = fmax(mx, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((tid & 31) == 0) sred[tid >> 5] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, sred[w]);
+    s_bcast = mx;
+  }
+  __syncthreads();
+  mx = s_bcast;
+  double sum = 0.0;
+  for (int j = tid; j < c_k; j += 256) {
+    double w = exp(row[j] - mx);
+    row[j] = w;
+    sum += w;
+  }
+  sum = warp_sum(sum);
+  __syncthreads();
+  if ((tid & 31) == 0) sred[tid >> 5] = sum;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += sred[w];
+    s_bcast = s;
+  }
+  __syncthreads();
+  sum = s_bcast;
+  for (int j = tid; j < c_k; j += 256) row[j] = row[j] / sum;
+}
+
+int launch_score_mass(const SvgEarShape& s, const float* qc, const float* kc,
+                      const int32_t* k_sizes, double* mass, cudaStream_t st) {
+  score_mass_kernel<<<dim3(s.c_q, s.bh), 256, 0, st>>>(qc, kc, k_sizes, s.d, s.c_q, s.c_k,
+                                                      1.0 / sqrt((double)s.d), mass);
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// routing: exact greedy walk without a sort.
+//
+// Walk order = descending priority P(b) = (ord(primary_b), ord(value_b), ~b) compared
+// lexicographically, where primary = value/(|q||k|) for error-aware routing (ratio_mode 0) or
+// primary = value for mass routing (ratio_mode 1), and ord() is the order-preserving map of a
+// float64 onto uint64.  Because the index is part of the key the order is total, exactly the
+// reference's sort key (-ratio, -error, qc, kc).
+//   phase 1  MSD radix select on P with weighted (block-size) histograms finds the first block
+//            that does not fit = end of the "take while it fits" prefix;
+//   phase 2  fillRemainder: repeatedly take the highest-priority block after the cursor whose
+//            weight still fits (block-wide lexicographic arg-max), until none fits;
+//   phase 3  best-single-fitting-block fallback.
+// One CTA per instance; integer atomics only.
+// ------------------------------------------------------------------------------------------------
+struct Prio {
+  unsigned long long a, b;
+  unsigned int c;
+};
+__device__ __forceinline__ bool prio_gt(const Prio& x, const Prio& y) {
+  if (x.a != y.a) return x.a > y.a;
+  if (x.b != y.b) return x.b > y.b;
+  return x.c > y.c;
+}
+__device__ __forceinline__ unsigned long long ord64(double v) {
+  unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ unsigned int prio_digit(const Prio& p, int pass) {
+  // 20 digits of 8 bits, most significant first: a[7..0], b[7..0], c[3..0]
+  if (pass < 8) return (unsigned int)(p.a >> (56 - 8 * pass)) & 0xffu;
+  if (pass < 16) return (unsigned int)(p.b >> (56 - 8 * (pass - 8))) & 0xffu;
+  return (p.c >> (24 - 8 * (pass - 16))) & 0xffu;
+}
+__device__ __forceinline__ bool prio_prefix_eq(const Prio& p, const Prio& q, int pass) {
+  // do the first `pass` digits of p and q agree?
+  if (pass <= 0) return true;
+  if (pass < 8) return (p.a >> (64 - 8 * pass)) == (q.a >> (64 - 8 * pass));
+  if (p.a != q.a) return false;
+  if (pass == 8) return true;
+  if (pass < 16) return (p.b >> (64 - 8 * (pass - 8))) == (q.b >> (64 - 8 * (pass - 8)));
+  if (p.b != q.b) return false;
+  if (pass == 16) return true;
+  return (p.c >> (32 - 8 * (pass - 16))) == (q.c >> (32 - 8 * (pass - 16)));
+}
+
+__global__ void __launch_bounds__(1024)
+    route_kernel(int c_q, int c_k, const double* __restrict__ val_all,
+                 const int32_t* __restrict__ q_sizes_all, const int32_t* __restrict__ k_sizes_all,
+                 long long capacity, int overshoot, int fallback, int ratio_mode,
+                 uint8_t* __restrict__ mask_all, long long* __restrict__ entries_all) {
+  const int h = blockIdx.x;
+  const int nb = c_q * c_k;
+  const double* val = val_all + (size_t)h * nb;
+  const int32_t* qs = q_sizes_all + (size_t)h * c_q;
+  uint8_t* mask = mask_all + (size_t)h * nb;
+  extern __shared__ int32_t s_ks[];  // [c_k]
+  __shared__ unsigned long long s_hw[256];
+  __shared__ unsigned int s_hc[256];
+  __shared__ Prio s_prefix;  // digits chosen so far (others zero)
+  __shared__ Prio s_red[32];
+  __shared__ long long s_redw[32];
+  __shared__ double s_redd[32];
+  __shared__ long long s_base;
+  __shared__ int s_flag;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int j = tid; j < c_k; j += blockDim.x) s_ks[j] = k_sizes_all[(size_t)h * c_k + j];
+  if (tid == 0) { s_prefix.a = 0; s_prefix.b = 0; s_prefix.c = 0; s_base = 0; s_flag = 0; }
+  __syncthreads();
+
+  auto weight = [&](int b) -> long long { return (long long)qs[b / c_k] * (long long)s_ks[b % c_k]; };
+  auto prio = [&](int b, long long w) -> Prio {
+    Prio p;
+    const double v = val[b];
+    p.a = ord64(ratio_mode == 0 ? v / (double)w : v);
+    p.b = ord64(v);
+    p.c = ~(unsigned int)b;
+    return p;
+  };
+
+  // ---- phase 1: first block that does not fit ---------------------------------------------------
+  bool all_fit = false;
+  int npass = 0;
+  for (int pass = 0; pass < 20; ++pass) {
+    for (int k = tid; k < 256; k += blockDim.x) { s_hw[k] = 0ull; s_hc[k] = 0u; }
+    __syncthreads();
+    const Prio pre = s_prefix;
+    for (int b = tid; b < nb; b += blockDim.x) {
+      const long long w = weight(b);
+      const Prio p = prio(b, w);
+      if (prio_prefix_eq(p, pre, pass)) {
+        const unsigned int dg = prio_digit(p, pass);
+        atomicAdd(&s_hw[dg], (unsigned long long)w);
+        atomicAdd(&s_hc[dg], 1u);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      long long run = s_base;
+      int found = -1;
+      for (int dg = 255; dg >= 0; --dg) {
+        if (s_hc[dg] == 0) continue;
+        if (run + (long long)s_hw[dg] > capacity) { found = dg; break; }
+        run += (long long)s_hw[dg];
+      }
+      s_base = run;
+      if (found < 0) {
+        s_flag = 1;  // every candidate fits (only possible on pass 0: everything is selected)
+      } else {
+        if (pass < 8) s_prefix.a |= (unsigned long long)found << (56 - 8 * pass);
+        else if (pass < 16) s_prefix.b |= (unsigned long long)found << (56 - 8 * (pass - 8));
+        else s_prefix.c |= (unsigned int)found << (24 - 8 * (pass - 16));
+        s_flag = (s_hc[found] == 1) ? 2 : 0;  // unique candidate -> it is the boundary block
+      }
+    }
+    __syncthreads();
+    npass = pass + 1;
+    if (s_flag == 1) { all_fit = true; break; }
+    if (s_flag == 2) break;
+  }
+  // locate the boundary block (unique element matching the chosen digits)
+  Prio bound;
+  bound.a = 0; bound.b = 0; bound.c = 0;
+  long long remaining = capacity - s_base;
+  __syncthreads();
+  if (!all_fit) {
+    if (tid == 0) s_red[0] = bound;
+    __syncthreads();
+    const Prio pre = s_prefix;
+    for (int b = tid; b < nb; b += blockDim.x) {
+      const long long w = weight(b);
+      const Prio p = prio(b, w);
+      if (prio_prefix_eq(p, pre, npass)) s_red[0] = p;  // exactly one writer
+    }
+    __syncthreads();
+    bound = s_red[0];
+  }
+  __syncthreads();
+  // ---- mask of the prefix -------------------------------------------------------------------------
+  for (int b = tid; b < nb; b += blockDim.x) {
+    const long long w = weight(b);
+    mask[b] = all_fit ? 1 : (prio_gt(prio(b, w), bound) ? 1 : 0);
+  }
+  // ---- phase 2: fillRemainder tail ------------------------------------------------------------------
+  if (!all_fit && overshoot == SVGEAR_FILL_REMAINDER) {
+    Prio cur = bound;
+    while (true) {
+      Prio best;
+      best.a = 0; best.b = 0; best.c = 0;
+      long long bw = 0;
+      bool have = false;
+      for (int b = tid; b < nb; b += blockDim.x) {
+        const long long w = weight(b);
+        if (w > remaining) continue;
+        const Prio p = prio(b, w);
+        if (prio_gt(cur, p) && (!have || prio_gt(p, best))) { best = p; bw = w; have = true; }
+      }
+      // block arg-max (an all-zero Prio is below every real key because ord64 sets the top bit
+      // for non-negative values and c = ~b is never 0 for b < 2^32-1)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        Prio q;
+        q.a = __shfl_xor_sync(0xffffffffu, best.a, o);
+        q.b = __shfl_xor_sync(0xffffffffu, best.b, o);
+        q.c = __shfl_xor_sync(0xffffffffu, best.c, o);
+        long long qw = __shfl_xor_sync(0xffffffffu, bw, o);
+        if (prio_gt(q, best)) { best = q; bw = qw; }
+      }
+      __syncthreads();
+      if (lane == 0) { s_red[warp] = best; s_redw[warp] = bw; }
+      __syncthreads();
+      if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        Prio q = s_red[lane < nw ? lane : 0];
+        long long qw = s_redw[lane < nw ? lane : 0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          Prio r;
+          r.a = __shfl_xor_sync(0xffffffffu, q.a, o);
+          r.b = __shfl_xor_sync(0xffffffffu, q.b, o);
+          r.c = __shfl_xor_sync(0xffffffffu, q.c, o);
+          long long rw = __shfl_xor_sync(0xffffffffu, qw, o);
+          if (prio_gt(r, q)) { q = r; qw = rw; }
+        }
+        if (lane == 0) { s_red[0] = q; s_redw[0] = qw; }
+      }
+      __syncthreads();
+      best = s_red[0];
+      bw = s_redw[0];
+      if (best.a == 0 && best.b == 0 && best.c == 0) break;  // nothing fits any more
+      if (tid == 0) mask[~best.c] = 1;
+      remaining -= bw;
+      cur = best;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  // ---- phase 3: single-item fallback + entry count ----------------------------------------------
+  double sum_sel = 0.0;
+  long long ent = 0;
+  double bestv = -INFINITY;
+  int besti = 0x7fffffff;
+  for (int b = tid; b < nb; b += blockDim.x) {
+    const long long w = weight(b);
+    const double v = val[b];
+    if (mask[b]) { sum_sel += v; ent += w; }
+    if (w <= capacity && v > bestv) { bestv = v; besti = b; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sum_sel += __shfl_xor_sync(0xffffffffu, sum_sel, o);
+    ent += __shfl_xor_sync(0xffffffffu, ent, o);
+    double ov = __shfl_xor_sync(0xffffffffu, bestv, o);
+    int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+    if (ov > bestv || (ov == bestv && oi < besti)) { bestv = ov; besti = oi; }
+  }
+  if (lane == 0) { s_redd[warp] = sum_sel; s_redw[warp] = ent; s_red[warp].a = (unsigned long long)__double_as_longlong(bestv); s_red[warp].c = (unsigned int)besti; }
+  __syncthreads();
+  if (tid == 0) {
+    const int nw = blockDim.x >> 5;
+    double s = 0.0;
+    long long e = 0;
+    double bv = -INFINITY;
+    int bx = 0x7fffffff;
+    for (int w = 0; w < nw; ++w) {
+      s += s_redd[w];
+      e += s_redw[w];
+      double ov = __longlong_as_double((long long)s_red[w].a);
+      int oi = (int)s_red[w].c;
+      if (ov > bv || (ov == bv && oi < bx)) { bv = ov; bx = oi; }
+    }
+    int swap = (fallback && bx != 0x7fffffff && bv > s) ? 1 : 0;
+    s_flag = swap;
+    s_base = swap ? (long long)bx : -1;
+    if (entries_all) entries_all[h] = swap ? weight(bx) : e;
+  }
+  __syncthreads();
+  if (s_flag) {
+    const int keep = (int)s_base;
+    for (int b = tid; b < nb; b += blockDim.x) mask[b] = (b == keep) ? 1 : 0;
+  }
+}
+
+int launch_route(int bh, int c_q, int c_k, const double* val, const int32_t* q_sizes,
+                 const int32_t* k_sizes, int64_t capacity, int overshoot, int fallback,
+                 int ratio_mode, uint8_t* mask, int64_t* entries, cudaStream_t st) {
+  route_kernel<<<bh, 1024, (size_t)c_k * sizeof(int32_t), st>>>(
+      c_q, c_k, val, q_sizes, k_sizes, (long long)capacity, overshoot, fallback, ratio_mode, mask,
+      reinterpret_cast<long long*>(entries));
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
+}  // namespace svg

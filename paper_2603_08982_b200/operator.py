@@ -1,0 +1,146 @@
+"""The drop-in operator: svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget).
+
+Per (batch, head) instance this is exactly the reference's four-call composition
+    prepare -> build_error_table -> route_error_aware(global density) -> sparse_attend
+(README.md:94-98, cli.py:119-134) followed by inverse_permute_rows, executed by ONE C-ABI call
+(svgear_forward) on the current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._tensors import ShapeError, require_cuda, stream_ptr, workspace
+from .analysis import side_seeds
+from .clustering import seeded_start, strided_start
+from .router import _OVERSHOOT, entry_capacity
+
+_EST = {"valueAware": _lib.EST_VALUE_AWARE, "plain": _lib.EST_PLAIN}
+
+
+def reference_init(q, k, n_q_clusters, n_k_clusters, seed):
+    """k-means++ start centres the reference would draw for `prepare(seed=...)`, for every
+    instance of a [.., S, d] batch (instance index b uses seed + b).  Host-side numpy; meant for
+    parity runs — it is O(C*S*d) per instance on the CPU."""
+    qf = q.reshape(-1, q.shape[-2], q.shape[-1]).float().cpu().numpy().astype(np.float64)
+    kf = k.reshape(-1, k.shape[-2], k.shape[-1]).float().cpu().numpy().astype(np.float64)
+    qi, ki = [], []
+    for b in range(qf.shape[0]):
+        qs, ks = side_seeds(seed + b)
+        qi.append(seeded_start(qf[b], n_q_clusters, qs))
+        ki.append(seeded_start(kf[b], n_k_clusters, ks))
+    return (torch.from_numpy(np.stack(qi)).float(), torch.from_numpy(np.stack(ki)).float())
+
+
+def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_init=None,
+                      k_init=None, init="reference", kmeans_iters=25, estimator="valueAware",
+                      overshoot="fillRemainder", single_item_fallback=True, check_fp32=False,
+                      return_aux=False, workspace_buffer=None):
+    """SVG-EAR attention.
+
+    q, k, v : bf16 CUDA tensors [B, H, S, d] (or [H, S, d] / [S, d]); d in {64, 128}.
+    n_q_clusters, n_k_clusters : cluster counts C_q, C_k.
+    budget : exact-compute budget = global density rho in [0, 1]
+             (router.DensityBudget.global_density, router.py:59-61).
+    init   : "reference" -> k-means++ centres drawn with the reference's RNG recipe from `seed`
+             (host side, slow at scale); "strided" -> evenly strided tokens (device side);
+             ignored for a side whose q_init / k_init ([.., C, d] float32 centres) is given.
+    check_fp32 : run the executor in fp32 on CUDA cores and return a float32 output.
+    Returns (out, mask) — out [.., S, d] in ORIGINAL token order, mask [.., C_q, C_k] bool
+    (True = block computed exactly) — plus a dict of intermediates when return_aux=True.
+    """
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a torch.Tensor")
+        if t.ndim not in (2, 3, 4):
+            raise ShapeError(f"{name} must be [B,H,S,d], [H,S,d] or [S,d], got shape {tuple(t.shape)}")
+    if k.shape != v.shape:
+        raise ValueError(f"key/value row counts differ: {tuple(k.shape)} vs {tuple(v.shape)}")
+    if q.shape[:-2] != k.shape[:-2] or q.shape[-1] != k.shape[-1]:
+        raise ShapeError(f"q {tuple(q.shape)} and k {tuple(k.shape)} disagree on batch/head/d")
+    n_q, n_k, d = q.shape[-2], k.shape[-2], q.shape[-1]
+    if d not in (64, 128):
+        raise ShapeError(f"head dimension must be 64 or 128 on the B200 path, got {d}")
+    for name, c, n in (("n_q_clusters", n_q_clusters, n_q), ("n_k_clusters", n_k_clusters, n_k)):
+        if c < 1:
+            raise ValueError(f"num_clusters must be >= 1, got {c} ({name})")
+        if c > n:
+            raise ValueError(f"num_clusters ({c}) exceeds token count ({n}) ({name})")
+    if budget is None or not (0.0 <= float(budget) <= 1.0):
+        raise ValueError(f"globalDensity budget needs rho in [0, 1], got {budget}")
+    if kmeans_iters < 1:
+        raise ValueError(f"max_iters must be >= 1, got {kmeans_iters}")
+    if estimator not in _EST:
+        raise ValueError(f"unknown estimator mode {estimator!r}")
+    if overshoot not in _OVERSHOOT:
+        raise ValueError(f"unknown overshoot policy {overshoot!r}")
+    if init not in ("reference", "strided"):
+        raise ValueError(f"unknown init {init!r}")
+    dev = require_cuda()
+    lead = tuple(q.shape[:-2])
+    bh = int(np.prod(lead)) if lead else 1
+    qb = q.to(dev, torch.bfloat16).reshape(bh, n_q, d).contiguous()
+    kb = k.to(dev, torch.bfloat16).reshape(bh, n_k, d).contiguous()
+    vb = v.to(dev, torch.bfloat16).reshape(bh, n_k, d).contiguous()
+    c_q, c_k = int(n_q_clusters), int(n_k_clusters)
+
+    if q_init is None or k_init is None:
+        if init == "reference":
+            rq, rk = reference_init(qb, kb, c_q, c_k, seed)
+        else:
+            rq, rk = strided_start(qb, c_q), strided_start(kb, c_k)
+        q_init = rq if q_init is None else q_init
+        k_init = rk if k_init is None else k_init
+    q_init = q_init.to(dev, torch.float32).reshape(bh, c_q, d).contiguous()
+    k_init = k_init.to(dev, torch.float32).reshape(bh, c_k, d).contiguous()
+
+    shape = _lib.Shape(bh, n_q, n_k, d, c_q, c_k)
+    need = _lib.workspace_bytes(shape)
+    ws = workspace_buffer if workspace_buffer is not None else workspace(need, dev)
+    if ws.numel() * ws.element_size() < need:
+        raise ValueError(f"workspace_buffer too small: need {need} bytes")
+    out = torch.empty((bh, n_q, d), dtype=torch.float32 if check_fp32 else torch.bfloat16, device=dev)
+    mask = torch.empty((bh, c_q, c_k), dtype=torch.uint8, device=dev)
+    aux_t, aux_c = {}, None
+    if return_aux:
+        i32, f32 = torch.int32, torch.float32
+        aux_t = dict(
+            q_assign=torch.empty((bh, n_q), dtype=i32, device=dev),
+            k_assign=torch.empty((bh, n_k), dtype=i32, device=dev),
+            q_perm=torch.empty((bh, n_q), dtype=i32, device=dev),
+            k_perm=torch.empty((bh, n_k), dtype=i32, device=dev),
+            q_sizes=torch.empty((bh, c_q), dtype=i32, device=dev),
+            k_sizes=torch.empty((bh, c_k), dtype=i32, device=dev),
+            q_offsets=torch.empty((bh, c_q), dtype=i32, device=dev),
+            k_offsets=torch.empty((bh, c_k), dtype=i32, device=dev),
+            q_centroids=torch.empty((bh, c_q, d), dtype=f32, device=dev),
+            k_centroids=torch.empty((bh, c_k, d), dtype=f32, device=dev),
+            v_centroids=torch.empty((bh, c_k, d), dtype=f32, device=dev),
+            q_iters=torch.zeros((bh,), dtype=i32, device=dev),
+            k_iters=torch.zeros((bh,), dtype=i32, device=dev),
+            error_table=torch.empty((bh, c_q, c_k), dtype=torch.float64, device=dev),
+            stabilizers=torch.empty((bh, c_q), dtype=f32, device=dev),
+            mask_entries=torch.zeros((bh,), dtype=torch.int64, device=dev),
+            lse=torch.empty((bh, n_q), dtype=f32, device=dev),
+        )
+        aux_c = _lib.Aux(**{name: aux_t[name].data_ptr() for name in _lib.Aux.FIELDS})
+    rc = _lib.lib().svgear_forward(
+        C.byref(shape), qb.data_ptr(), kb.data_ptr(), vb.data_ptr(), q_init.data_ptr(),
+        k_init.data_ptr(), int(kmeans_iters), _EST[estimator],
+        entry_capacity(float(budget), n_q * n_k), _OVERSHOOT[overshoot],
+        1 if single_item_fallback else 0,
+        _lib.EXEC_FP32_CHECK if check_fp32 else _lib.EXEC_BF16_TENSOR, out.data_ptr(),
+        mask.data_ptr(), C.byref(aux_c) if aux_c is not None else None, ws.data_ptr(),
+        ws.numel() * ws.element_size(), stream_ptr())
+    _lib.check("svgear_forward", rc)
+    out = out.reshape(*lead, n_q, d)
+    mask_b = mask.bool().reshape(*lead, c_q, c_k)
+    if not return_aux:
+        return out, mask_b
+    aux = {name: t.reshape(*lead, *t.shape[1:]) for name, t in aux_t.items()}
+    aux["q_init"], aux["k_init"] = q_init.reshape(*lead, c_q, d), k_init.reshape(*lead, c_k, d)
+    return out, mask_b, aux
