@@ -234,7 +234,7 @@ int launch_attend(const SvgEarShape& s, int exec_mode, const bf16* qp, const bf1
                   const int32_t* q_offsets, const int32_t* k_sizes, const int32_t* k_offsets,
                   const float* kc, const float* vc, const uint8_t* mask, void* out, float* lse,
                   AttendScratch& sc, cudaStream_t st) {
-  const int ckpad = ceil_div(s.c_k, 64) * 64 + 64;
+  const int ckpad = ceil_div(s.c_k, 64) * 64;  // rows of the bf16 centroid arrays (zero padded)
   const float scale = 1.0f / sqrtf((float)s.d);
   prep_centroids_kernel<<<dim3(ceil_div(ckpad * s.d, 256), s.bh), 256, 0, st>>>(
       kc, vc, k_sizes, s.d, s.c_k, ckpad, sc.kbar_bf16, sc.vbar_bf16, sc.lnw);

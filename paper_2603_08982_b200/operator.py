@@ -141,6 +141,6 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
     mask_b = mask.bool().reshape(*lead, c_q, c_k)
     if not return_aux:
         return out, mask_b
-    aux = {name: t.reshape(*lead, *t.shape[1:]) for name, t in aux_t.items()}
+    aux = {name: t.reshape(tuple(lead) + tuple(t.shape[1:])) for name, t in aux_t.items()}
     aux["q_init"], aux["k_init"] = q_init.reshape(*lead, c_q, d), k_init.reshape(*lead, c_k, d)
     return out, mask_b, aux

@@ -82,8 +82,17 @@ class TestOperatorVsGolden:
             # not pinned; any mask reproduces dense attention (tests/test_acceptance.py:128-163)
             pass
         else:
-            assert mm == 0.0, f"{name}: mask mismatch rate {mm} at rho={rho}"
-            assert int(aux["mask_entries"]) == int(g[f"entries_{tag(rho)}"])
+            # the GPU router is exact on ITS table (checked against the oracle's walk) ...
+            mine = SimpleNamespace(error_sum=err, q_sizes=g["q_sizes"], k_sizes=g["k_sizes"])
+            assert np.array_equal(host(mask), O.route_error_aware(mine, rho).selected)
+            # ... and may differ from the reference mask only on fp ties: blocks whose reference
+            # error is rounding noise (e.g. singleton key clusters: 1e-29 in float64, 0 here)
+            diff = host(mask) != want_mask
+            assert (ref[diff] <= 1e-12 * ref.max()).all(), f"{name}: mask mismatch rate {mm} at rho={rho}"
+            if mm == 0.0:
+                assert int(aux["mask_entries"]) == int(g[f"entries_{tag(rho)}"])
+            else:
+                print(f"{name} rho={rho}: mask mismatch rate {mm:.3f} (noise-level ties only)")
             e = rel_l2(host(out.float()), g[f"out_{tag(rho)}"])
             assert e <= (TOL_FP32 if check_fp32 else TOL_BF16), f"{name}: rel-L2 {e}"
         if name == "dups_d64" or rho == 1.0:
