@@ -99,11 +99,13 @@ int svgear_workspace_bytes(const SvgEarShape* shape, size_t* bytes);
  * Semantics kept: distance = max(|x|^2 - 2x.c + |c|^2, 0); ties -> lowest cluster index; empty
  * clusters repaired in ascending order from the farthest token of a cluster with >=2 members;
  * convergence is tested before the centroid update; final centroids are the member means;
- * permutation = stable sort by cluster.  Distances are evaluated in fp32 (reference: float64).
+ * permutation = stable sort by cluster.  Distances are evaluated in fp32 (reference: float64):
+ * exec_mode SVGEAR_EXEC_BF16_TENSOR forms x.c on the tensor cores (tcgen05) from a 3-way bf16
+ * split of the fp32 centroids with fp32 accumulation; SVGEAR_EXEC_FP32_CHECK uses fp32 FMAs.
  *   x            [bh][n][d] bf16          init_centroids [bh][c][d] f32
  *   assign,perm  [bh][n] i32              sizes,offsets  [bh][c] i32
  *   centroids    [bh][c][d] f32           iters [bh] i32, inertia [bh] f64 (either may be NULL) */
-int svgear_kmeans(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
+int svgear_kmeans(int32_t exec_mode, int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
                   const float* init_centroids, int32_t max_iters, int32_t* assign, int32_t* perm,
                   int32_t* sizes, int32_t* offsets, float* centroids, int32_t* iters,
                   double* inertia, void* workspace, size_t workspace_bytes, void* stream);

@@ -84,7 +84,7 @@ def _pad_centers(tok_f32, centers, k):
     return centers
 
 
-def run_lloyd(x, starts, max_iters):
+def run_lloyd(x, starts, max_iters, fp32_check=False):
     """x [bh,n,d] bf16, starts [bh,c,d] f32 -> dict of raw svgear_kmeans outputs."""
     bh, n, d = x.shape
     c = starts.shape[1]
@@ -101,7 +101,7 @@ def run_lloyd(x, starts, max_iters):
     shape = _lib.Shape(bh, n, n, d, c, c)
     ws = workspace(_lib.workspace_bytes(shape), dev)
     rc = _lib.lib().svgear_kmeans(
-        bh, n, d, c, x.data_ptr(), starts.data_ptr(), int(max_iters), out["assign"].data_ptr(),
+        _lib.EXEC_FP32_CHECK if fp32_check else _lib.EXEC_BF16_TENSOR, bh, n, d, c, x.data_ptr(), starts.data_ptr(), int(max_iters), out["assign"].data_ptr(),
         out["perm"].data_ptr(), out["sizes"].data_ptr(), out["offsets"].data_ptr(),
         out["centroids"].data_ptr(), out["iters"].data_ptr(), out["inertia"].data_ptr(),
         ws.data_ptr(), ws.numel(), stream_ptr())
@@ -113,7 +113,8 @@ def _flops(n, k, d, iters):
     return 2 * n * k * d + iters * (2 * n * k * d + 2 * n * k + 2 * n * d)  # clustering.py:138-140
 
 
-def kmeans(tokens, num_clusters, *, max_iters=25, seed=0, restarts=1, init_centroids=None):
+def kmeans(tokens, num_clusters, *, max_iters=25, seed=0, restarts=1, init_centroids=None,
+           fp32_check=False):
     """Cluster token rows; best of `restarts` seeded runs (+ an optional warm start).
 
     Mirrors clustering.kmeans (clustering.py:144-207) including its validation errors.  For a
@@ -136,7 +137,8 @@ def kmeans(tokens, num_clusters, *, max_iters=25, seed=0, restarts=1, init_centr
         pool.append(torch.stack([_pad_centers(xf[b], ic[b], k) for b in range(bh)]))
     # every start is one more batch instance: [S*bh, ...]
     S = len(pool)
-    res = run_lloyd(x.repeat(S, 1, 1) if S > 1 else x, torch.cat(pool, dim=0).contiguous(), max_iters)
+    res = run_lloyd(x.repeat(S, 1, 1) if S > 1 else x, torch.cat(pool, dim=0).contiguous(), max_iters,
+                    fp32_check=fp32_check)
     inertia = res["inertia"].view(S, bh)
     best = torch.argmin(inertia, dim=0)  # ties -> earliest start, as the reference
     pick = best * bh + torch.arange(bh, device=x.device)

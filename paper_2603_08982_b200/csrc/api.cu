@@ -37,7 +37,7 @@ struct ForwardPlan {
 bool plan_forward(const SvgEarShape& s, Carver& cv, ForwardPlan& p) {
   const int nmax = s.n_q > s.n_k ? s.n_q : s.n_k;
   const int cmax = s.c_q > s.c_k ? s.c_q : s.c_k;
-  p.km.carve(cv, s.bh, nmax, cmax);
+  p.km.carve(cv, s.bh, nmax, cmax, s.d);
   p.at.carve(cv, s);
   p.q_assign = cv.take<int32_t>((size_t)s.bh * s.n_q);
   p.k_assign = cv.take<int32_t>((size_t)s.bh * s.n_k);
@@ -106,20 +106,21 @@ int svgear_workspace_bytes(const SvgEarShape* shape, size_t* bytes) {
   return SVGEAR_OK;
 }
 
-int svgear_kmeans(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
+int svgear_kmeans(int32_t exec_mode, int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
                   const float* init_centroids, int32_t max_iters, int32_t* assign, int32_t* perm,
                   int32_t* sizes, int32_t* offsets, float* centroids, int32_t* iters,
                   double* inertia, void* workspace, size_t workspace_bytes, void* stream) {
   if (!x || !init_centroids || !assign || !perm || !sizes || !offsets || !centroids || !workspace)
     return SVGEAR_EINVAL;
   if (max_iters < 1) return SVGEAR_EINVAL;
+  if (exec_mode != SVGEAR_EXEC_BF16_TENSOR && exec_mode != SVGEAR_EXEC_FP32_CHECK) return SVGEAR_EINVAL;
   if (bh < 1 || n < 1 || (d != 64 && d != 128) || c < 1 || c > n || c > kMaxClusters)
     return SVGEAR_ESHAPE;
   if (!device_present()) return SVGEAR_ECUDA;
   Carver cv(workspace, workspace_bytes);
   KmeansScratch sc;
-  if (!sc.carve(cv, bh, n, c)) return SVGEAR_EWORKSPACE;
-  return launch_kmeans(bh, n, d, c, (const bf16*)x, init_centroids, max_iters, assign, perm, sizes,
+  if (!sc.carve(cv, bh, n, c, d)) return SVGEAR_EWORKSPACE;
+  return launch_kmeans(exec_mode, bh, n, d, c, (const bf16*)x, init_centroids, max_iters, assign, perm, sizes,
                        offsets, centroids, iters, inertia, sc, (cudaStream_t)stream);
 }
 
@@ -262,10 +263,10 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
   // (1) cluster Q and K independently; V follows K (analysis.py:228-238)
-  rc = launch_kmeans(s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign, q_perm,
+  rc = launch_kmeans(exec_mode, s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign, q_perm,
                      q_sizes, q_offsets, q_cent, q_iters, nullptr, p.km, st);
   if (rc) return rc;
-  rc = launch_kmeans(s.bh, s.n_k, s.d, s.c_k, (const bf16*)k, k_init, kmeans_iters, k_assign, k_perm,
+  rc = launch_kmeans(exec_mode, s.bh, s.n_k, s.d, s.c_k, (const bf16*)k, k_init, kmeans_iters, k_assign, k_perm,
                      k_sizes, k_offsets, k_cent, k_iters, nullptr, p.km, st);
   if (rc) return rc;
   rc = launch_gather_rows(s.bh, s.n_q, s.d, (const bf16*)q, q_perm, p.qp, st);

@@ -97,12 +97,14 @@ struct KmeansScratch {
   double* chunk_inertia;  // [bh][nchunks]
   int32_t* done;          // [bh]
   int32_t* changed;       // [bh]
-  static size_t bytes(int bh, int n, int c);
-  bool carve(Carver& cv, int bh, int n, int c);
+  bf16* pieces;           // [bh][pieces][cpad][d]  split-bf16 centroids (tensor-core assignment)
+  float* cnorm_pad;       // [bh][cpad]
+  float* xnorm;           // [bh][n]
+  bool carve(Carver& cv, int bh, int n, int c, int d);
 };
 
-int launch_kmeans(int bh, int n, int d, int c, const bf16* x, const float* init, int max_iters,
-                  int32_t* assign, int32_t* perm, int32_t* sizes, int32_t* offsets,
+int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, const float* init,
+                  int max_iters, int32_t* assign, int32_t* perm, int32_t* sizes, int32_t* offsets,
                   float* centroids, int32_t* iters, double* inertia, KmeansScratch& sc,
                   cudaStream_t st);
 int launch_gather_rows(int bh, int n, int d, const bf16* x, const int32_t* perm, bf16* out,

@@ -408,18 +408,14 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ x, const int32_t* _
 // ------------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------------
-size_t KmeansScratch::bytes(int bh, int n, int c) {
-  const int nchunks = ceil_div(n, kSortChunk);
-  size_t b = 0;
-  b += align_up((size_t)bh * n * 4, 256) * 2;           // prev_assign, own_d2
-  b += align_up((size_t)bh * c * 4, 256);               // cnorm
-  b += align_up((size_t)bh * nchunks * c * 4, 256);     // chunk_counts
-  b += align_up((size_t)bh * nchunks * 8, 256);         // chunk_inertia
-  b += align_up((size_t)bh * 4, 256) * 2;               // done, changed
-  return b + 2048;
-}
+size_t kmeans_tc_scratch_bytes(int bh, int n, int c, int d);
+int launch_token_norms(int bh, int n, int d, const bf16* x, float* xnorm, cudaStream_t st);
+int launch_kmeans_assign_tc(int bh, int n, int d, int c, const bf16* x, const float* cent,
+                            const float* cnorm, bf16* pieces, float* cnorm_pad, const float* xnorm,
+                            int32_t* assign, float* own_d2, int32_t* sizes, int32_t* changed,
+                            const int32_t* done, cudaStream_t st);
 
-bool KmeansScratch::carve(Carver& cv, int bh, int n, int c) {
+bool KmeansScratch::carve(Carver& cv, int bh, int n, int c, int d) {
   const int nchunks = ceil_div(n, kSortChunk);
   prev_assign = cv.take<int32_t>((size_t)bh * n);
   own_d2 = cv.take<float>((size_t)bh * n);
@@ -428,15 +424,15 @@ bool KmeansScratch::carve(Carver& cv, int bh, int n, int c) {
   chunk_inertia = cv.take<double>((size_t)bh * nchunks);
   done = cv.take<int32_t>(bh);
   changed = cv.take<int32_t>(bh);
+  const int cpad = ceil_div(c, 128) * 128;
+  pieces = cv.take<bf16>((size_t)bh * 3 * cpad * d);
+  cnorm_pad = cv.take<float>((size_t)bh * cpad);
+  xnorm = cv.take<float>((size_t)bh * n);
   return cv.ok;
 }
 
-int launch_kmeans_assign_tc(int bh, int n, int d, int c, const bf16* x, const float* cent,
-                            const float* cnorm, int32_t* assign, float* own_d2, int32_t* sizes,
-                            int32_t* changed, const int32_t* done, cudaStream_t st);
-
-int launch_kmeans(int bh, int n, int d, int c, const bf16* x, const float* init, int max_iters,
-                  int32_t* assign, int32_t* perm, int32_t* sizes, int32_t* offsets,
+int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, const float* init,
+                  int max_iters, int32_t* assign, int32_t* perm, int32_t* sizes, int32_t* offsets,
                   float* centroids, int32_t* iters, double* inertia, KmeansScratch& sc,
                   cudaStream_t st) {
   const int nchunks = ceil_div(n, kSortChunk);
@@ -446,11 +442,20 @@ int launch_kmeans(int bh, int n, int d, int c, const bf16* x, const float* init,
   SVG_CUDA_OK(cudaMemsetAsync(sc.changed, 0, (size_t)bh * 4, st));
   centroid_norm_kernel<<<ceil_div(bh * c, 8), 256, 0, st>>>(centroids, d, bh * c, sc.cnorm);
   SVG_LAUNCH_OK();
+  const bool use_tc = exec_mode == SVGEAR_EXEC_BF16_TENSOR;
+  if (use_tc) {
+    int rc = launch_token_norms(bh, n, d, x, sc.xnorm, st);
+    if (rc) return rc;
+  }
   const size_t hist_smem = (size_t)c * sizeof(int32_t);
   const int hist_blocks = max(1, min(64, ceil_div(n, 4096)));
   for (int it = 0; it < max_iters; ++it) {
     dim3 ga(ceil_div(n, 128), bh);
-    if (d == 128)
+    if (use_tc) {
+      int rc = launch_kmeans_assign_tc(bh, n, d, c, x, centroids, sc.cnorm, sc.pieces, sc.cnorm_pad,
+                                       sc.xnorm, assign, sc.own_d2, sizes, sc.changed, sc.done, st);
+      if (rc) return rc;
+    } else if (d == 128)
       assign_fp32_kernel<128><<<ga, 128, 0, st>>>(x, centroids, sc.cnorm, n, c, assign, sc.own_d2,
                                                   sizes, sc.changed, sc.done);
     else

@@ -1,0 +1,276 @@
+// k-means assignment on the tensor cores (tcgen05 + TMEM), sm_100a.
+//
+// Reference step: clustering._sq_dists + argmin (clustering.py:55-62, 113):
+//     d2[t,c] = max(|x_t|^2 - 2 x_t.c_c + |c_c|^2, 0),  assign[t] = first argmin_c d2[t,c].
+// The x.c^T contraction is ~99.5 % of a Lloyd iteration.  Tokens are bf16 (exact); each fp32
+// centroid is split into kPieces bf16 pieces c = c0 + c1 (+ c2) so that sum_p x.c_p reproduces
+// the fp32 product to ~2^-24 with fp32 accumulation in TMEM — the pieces simply extend the K
+// dimension of one GEMM.  The epilogue (one thread per token) turns accumulator columns into
+// distances and keeps the running (min, first index), so the [n x C] distance matrix never
+// exists in memory.
+//
+// CTA = 256 tokens (two M=128 tiles) x all centroids, N tiles of 128.  Centroid-piece tiles
+// (32 KB at d=128) stream through a 4-stage cp.async pipeline; each piece tile is reused by both
+// M tiles, which keeps L2 traffic at 32 B/cycle/SM.  TMEM: 2 buffers x (2 M tiles x 128 columns)
+// = 512 columns, so the epilogue of N tile n overlaps the MMAs of N tile n+1.
+//   warps 0-7 : epilogue (warp w -> M tile w/4, TMEM lanes 32*(w%4)..)
+//   warp  8   : producer (A token tiles once, then the centroid-piece tiles)
+//   warp  9   : TMEM allocator + single-thread MMA issuer
+#include "tc_common.cuh"
+
+namespace svg {
+
+using namespace tc;
+
+namespace {
+constexpr int kPieces = 3;
+constexpr int KM = 256;     // tokens per CTA
+constexpr int KN = 128;     // centroids per N tile
+constexpr int KSTAGES = 4;  // centroid-piece pipeline depth
+constexpr int KTHREADS = 320;
+
+enum { KB_AFULL = 0, KB_BFULL = 1, KB_BEMPTY = 1 + KSTAGES, KB_ACCFULL = 1 + 2 * KSTAGES, KB_ACCEMPTY = 3 + 2 * KSTAGES };
+
+template <int D>
+struct KSmem {
+  static constexpr int kABytes = KM * D * 2;
+  static constexpr int kBBytes = KN * D * 2;
+  static constexpr int kA = 0;
+  static constexpr int kB = kA + kABytes;
+  static constexpr int kBars = kB + KSTAGES * kBBytes;
+  static constexpr size_t bytes() { return 1024 + kBars + 256; }
+};
+}  // namespace
+
+// fp32 centroids -> kPieces bf16 pieces [bh][piece][cpad][d] + padded norms (inf beyond c)
+__global__ void split_centroids_kernel(const float* __restrict__ cent, const float* __restrict__ cnorm,
+                                       int d, int c, int cpad, bf16* __restrict__ pieces,
+                                       float* __restrict__ cnorm_pad, const int32_t* __restrict__ done) {
+  const int h = blockIdx.y;
+  if (done[h]) return;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= cpad * d) return;
+  const int j = idx / d;
+  float v = j < c ? cent[(size_t)h * c * d + idx] : 0.f;
+#pragma unroll
+  for (int p = 0; p < kPieces; ++p) {
+    const bf16 b = __float2bfloat16_rn(v);
+    pieces[((size_t)h * kPieces + p) * cpad * d + idx] = b;
+    v -= __bfloat162float(b);
+  }
+  if (idx % d == 0) cnorm_pad[(size_t)h * cpad + j] = j < c ? cnorm[(size_t)h * c + j] : INFINITY;
+}
+
+__global__ void token_norm_kernel(const bf16* __restrict__ x, int d, long long total, float* __restrict__ xn) {
+  const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= total) return;
+  // sequential-in-k accumulation per lane chunk is not needed for parity: |x|^2 is a per-token
+  // constant of the argmin; it only enters own_d2.  Lanes split the row, fixed shuffle tree.
+  const bf16* p = x + row * d;
+  float s = 0.f;
+  for (int k = lane; k < d; k += 32) {
+    const float f = __bfloat162float(p[k]);
+    s = fmaf(f, f, s);
+  }
+  s = warp_sum(s);
+  if (lane == 0) xn[row] = s;
+}
+
+template <int D>
+__global__ void __launch_bounds__(KTHREADS, 1)
+    assign_tc_kernel(const bf16* __restrict__ x, const bf16* __restrict__ pieces,
+                     const float* __restrict__ cnorm_pad, const float* __restrict__ xnorm, int n, int c,
+                     int cpad, int32_t* __restrict__ assign, float* __restrict__ own_d2,
+                     int32_t* __restrict__ sizes, int32_t* __restrict__ changed,
+                     const int32_t* __restrict__ done) {
+  using L = KSmem<D>;
+  const int h = blockIdx.y;
+  if (done[h]) return;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sA = sbase + L::kA, sB = sbase + L::kB, bars = sbase + L::kBars;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kBars + 192);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto bar = [&](int i) -> uint32_t { return bars + 8u * (uint32_t)i; };
+
+  if (blockIdx.x == 0) {  // reset the per-iteration counters of this instance
+    for (int j = tid; j < c; j += KTHREADS) sizes[(size_t)h * c + j] = 0;
+    if (tid == 0) changed[h] = 0;
+  }
+  if (tid == 0) {
+    mbar_init(bar(KB_AFULL), 1);
+    for (int s = 0; s < KSTAGES; ++s) {
+      mbar_init(bar(KB_BFULL + s), 1);
+      mbar_init(bar(KB_BEMPTY + s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(KB_ACCFULL + b), 1);
+      mbar_init(bar(KB_ACCEMPTY + b), 256);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int NT = cpad / KN;        // N tiles
+  const int U = NT * kPieces;      // pipeline units
+  const int tok0 = blockIdx.x * KM;
+
+  if (warp == 8) {
+    // =========================== producer ========================================================
+    constexpr int CPR = D / 8, RPI = 32 / CPR;
+    const int sub = lane / CPR, chunk = lane % CPR;
+    const bf16* xsrc = x + (size_t)h * n * D;
+    for (int r0 = 0; r0 < KM; r0 += RPI) {
+      const int r = r0 + sub;                 // row within the CTA: M tile r/128, row r%128
+      const int row = min(tok0 + r, n - 1);
+      const int mt = r >> 7, rr = r & 127;
+      cp_async16(sA + (uint32_t)(mt * (128 * D * 2) + (chunk >> 3) * (128 * 128)) + swz(rr, chunk & 7),
+                 xsrc + (size_t)row * D + chunk * 8);
+    }
+    cp_async_commit();  // group 0 = A
+    for (int u = 0; u < U; ++u) {
+      const int st = u % KSTAGES;
+      if (u >= KSTAGES) mbar_wait(bar(KB_BEMPTY + st), ((u / KSTAGES) - 1) & 1);
+      const int nt = u / kPieces, p = u % kPieces;
+      const bf16* bsrc = pieces + (((size_t)h * kPieces + p) * cpad + (size_t)nt * KN) * D;
+      const uint32_t dst = sB + (uint32_t)st * L::kBBytes;
+#pragma unroll 4
+      for (int r0 = 0; r0 < KN; r0 += RPI) {
+        const int r = r0 + sub;
+        cp_async16(dst + (uint32_t)((chunk >> 3) * (KN * 128)) + swz(r, chunk & 7),
+                   bsrc + (size_t)r * D + chunk * 8);
+      }
+      cp_async_commit();  // group u+1
+      // keep KSTAGES-2 groups in flight; group u-1 has landed after this wait
+      asm volatile("cp.async.wait_group %0;" ::"n"(KSTAGES - 2) : "memory");
+      if (u >= 1) {
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(u == 1 ? bar(KB_AFULL) : bar(KB_BFULL + (u - 2) % KSTAGES));
+      }
+    }
+    cp_async_wait_all();
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      if (U == 1) mbar_arrive(bar(KB_AFULL));
+      for (int u = max(U - 2, 0); u < U; ++u) mbar_arrive(bar(KB_BFULL + u % KSTAGES));
+    }
+  } else if (warp == 9) {
+    // =========================== MMA issuer ======================================================
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(128, KN, 0);
+      mbar_wait(bar(KB_AFULL), 0);
+      for (int nt = 0; nt < NT; ++nt) {
+        const int buf = nt & 1;
+        if (nt >= 2) mbar_wait(bar(KB_ACCEMPTY + buf), ((nt >> 1) - 1) & 1);
+        for (int p = 0; p < kPieces; ++p) {
+          const int u = nt * kPieces + p, st = u % KSTAGES;
+          mbar_wait(bar(KB_BFULL + st), (u / KSTAGES) & 1);
+          tc_fence_after();
+          const uint32_t bb = sB + (uint32_t)st * L::kBBytes;
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint64_t ad = make_desc(
+                  sA + (uint32_t)(m * (128 * D * 2) + (kk >> 2) * (128 * 128) + (kk & 3) * 32), 16, 1024);
+              const uint64_t bd = make_desc(bb + (uint32_t)((kk >> 2) * (KN * 128) + (kk & 3) * 32), 16, 1024);
+              umma_ss(tmem + (uint32_t)(buf * 256 + m * 128), ad, bd, idesc, (p > 0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(bar(KB_BEMPTY + st));
+        }
+        umma_commit(bar(KB_ACCFULL + buf));
+      }
+    }
+    __syncwarp();
+  } else {
+    // =========================== epilogue: distances + running arg-min ===========================
+    const int m = warp >> 2;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const int t = tok0 + m * 128 + (warp & 3) * 32 + lane;
+    const float xn = xnorm[(size_t)h * n + min(t, n - 1)];
+    const float* cn = cnorm_pad + (size_t)h * cpad;
+    float best = INFINITY;
+    int bi = 0;
+    for (int nt = 0; nt < NT; ++nt) {
+      const int buf = nt & 1;
+      mbar_wait(bar(KB_ACCFULL + buf), (nt >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tcol = tmem + lane_base + (uint32_t)(buf * 256 + m * 128);
+#pragma unroll
+      for (int c4 = 0; c4 < KN; c4 += 32) {
+        uint32_t a[32];
+        TMEM_LD32(tcol + c4, a);
+        tc_wait_ld();
+        const int cb = nt * KN + c4;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          // same association as the reference: (|x|^2 - 2 x.c) + |c|^2, clipped at zero
+          const float v = fmaxf((xn - 2.0f * __uint_as_float(a[j])) + __ldg(cn + cb + j), 0.f);
+          if (v < best) {  // strict: ties keep the lowest cluster index
+            best = v;
+            bi = cb + j;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(bar(KB_ACCEMPTY + buf));
+    }
+    if (t < n) {
+      assign[(size_t)h * n + t] = bi;
+      own_d2[(size_t)h * n + t] = best;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+size_t kmeans_tc_scratch_bytes(int bh, int n, int c, int d) {
+  const int cpad = ceil_div(c, KN) * KN;
+  return align_up((size_t)bh * kPieces * cpad * d * 2, 256) + align_up((size_t)bh * cpad * 4, 256) +
+         align_up((size_t)bh * n * 4, 256) + 1024;
+}
+
+int launch_token_norms(int bh, int n, int d, const bf16* x, float* xnorm, cudaStream_t st) {
+  const long long total = (long long)bh * n;
+  token_norm_kernel<<<(unsigned)((total + 7) / 8), 256, 0, st>>>(x, d, total, xnorm);
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
+int launch_kmeans_assign_tc(int bh, int n, int d, int c, const bf16* x, const float* cent,
+                            const float* cnorm, bf16* pieces, float* cnorm_pad, const float* xnorm,
+                            int32_t* assign, float* own_d2, int32_t* sizes, int32_t* changed,
+                            const int32_t* done, cudaStream_t st) {
+  const int cpad = ceil_div(c, KN) * KN;
+  split_centroids_kernel<<<dim3(ceil_div(cpad * d, 256), bh), 256, 0, st>>>(cent, cnorm, d, c, cpad, pieces,
+                                                                           cnorm_pad, done);
+  SVG_LAUNCH_OK();
+  dim3 grid(ceil_div(n, KM), bh);
+  if (d == 128) {
+    const size_t smem = KSmem<128>::bytes();
+    SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    assign_tc_kernel<128><<<grid, KTHREADS, smem, st>>>(x, pieces, cnorm_pad, xnorm, n, c, cpad, assign, own_d2,
+                                                        sizes, changed, done);
+  } else {
+    const size_t smem = KSmem<64>::bytes();
+    SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    assign_tc_kernel<64><<<grid, KTHREADS, smem, st>>>(x, pieces, cnorm_pad, xnorm, n, c, cpad, assign, own_d2,
+                                                       sizes, changed, done);
+  }
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
+}  // namespace svg

@@ -45,12 +45,12 @@ class TestCAbi:
     def test_argument_errors_precede_device_errors(self):
         lib = P.load_library()
         # null pointers -> EINVAL, bad iteration count -> EINVAL, bad d -> ESHAPE
-        assert lib.svgear_kmeans(1, 8, 64, 2, None, None, 5, None, None, None, None, None, None, None,
+        assert lib.svgear_kmeans(0, 1, 8, 64, 2, None, None, 5, None, None, None, None, None, None, None,
                                  None, 0, None) == _lib.EINVAL
         buf = (C.c_char * 4096)()
         p = C.addressof(buf)
-        assert lib.svgear_kmeans(1, 8, 64, 2, p, p, 0, p, p, p, p, p, None, None, p, 4096, None) == _lib.EINVAL
-        assert lib.svgear_kmeans(1, 8, 48, 2, p, p, 5, p, p, p, p, p, None, None, p, 4096, None) == _lib.ESHAPE
+        assert lib.svgear_kmeans(0, 1, 8, 64, 2, p, p, 0, p, p, p, p, p, None, None, p, 4096, None) == _lib.EINVAL
+        assert lib.svgear_kmeans(0, 1, 8, 48, 2, p, p, 5, p, p, p, p, p, None, None, p, 4096, None) == _lib.ESHAPE
         assert lib.svgear_route_error_aware(1, 1, 2, p, p, p, -1, 0, 1, p, None, None, 0, None) == _lib.EINVAL
 
     @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
@@ -58,7 +58,7 @@ class TestCAbi:
         lib = P.load_library()
         buf = (C.c_char * 4096)()
         p = C.addressof(buf)
-        assert lib.svgear_kmeans(1, 8, 64, 2, p, p, 5, p, p, p, p, p, None, None, p, 4096, None) == _lib.ECUDA
+        assert lib.svgear_kmeans(0, 1, 8, 64, 2, p, p, 5, p, p, p, p, p, None, None, p, 4096, None) == _lib.ECUDA
         with pytest.raises(RuntimeError, match="no CPU fallback"):
             P.svg_ear_attention(*(torch.zeros(8, 64, dtype=torch.bfloat16),) * 3, 2, 2, 0.25)
 
