@@ -124,7 +124,8 @@ int svgear_segment_means(int32_t bh, int32_t n, int32_t d, int32_t c, const void
  *   k_permuted, v_permuted [bh][n_k][d] bf16 cluster-contiguous (v may be NULL for PLAIN)
  *   error_table [bh][c_q][c_k] f64 (stabilised at `stabilizers`, multiplied by |q_c|)
  *   stabilizers [bh][c_q] f32 = row max of centroid logits                                      */
-int svgear_error_table(const SvgEarShape* shape, int32_t mode, const float* q_centroids,
+int svgear_error_table(const SvgEarShape* shape, int32_t exec_mode, int32_t mode,
+                       const float* q_centroids,
                        const float* k_centroids, const float* v_centroids, const void* k_permuted,
                        const void* v_permuted, const int32_t* q_sizes, const int32_t* k_sizes,
                        const int32_t* k_offsets, double* error_table, float* stabilizers,

@@ -15,7 +15,7 @@ import threading
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_PATH = os.path.join(PKG_DIR, "libsvgear.so")
-SOURCES = ("api.cu", "kmeans.cu", "kmeans_tc.cu", "stats_route.cu", "attend_ref.cu", "attend_tc.cu")
+SOURCES = ("api.cu", "kmeans.cu", "kmeans_tc.cu", "stats_route.cu", "errtab_tc.cu", "attend_ref.cu", "attend_tc.cu")
 NVCC_FLAGS = (
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-shared", "-Xcompiler", "-fPIC",
@@ -56,7 +56,7 @@ SIGNATURES = {
     "svgear_kmeans": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_permute_rows": ([_I32, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "svgear_segment_means": ([_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P], C.c_int),
-    "svgear_error_table": ([C.POINTER(Shape), _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "svgear_error_table": ([C.POINTER(Shape), _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_route_error_aware": ([_I32, _I32, _I32, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_route_score": ([C.POINTER(Shape), _P, _P, _P, _P, _I64, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_sparse_attend": ([C.POINTER(Shape), _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),

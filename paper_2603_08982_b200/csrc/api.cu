@@ -26,9 +26,10 @@ bool shape_ok(const SvgEarShape* s) {
 struct ForwardPlan {
   KmeansScratch km;  // shared by both sides (sized for the larger)
   AttendScratch at;
+  ErrScratch es;
   int32_t *q_assign, *k_assign, *q_perm, *k_perm, *q_sizes, *k_sizes, *q_offsets, *k_offsets;
   int32_t *q_iters, *k_iters;
-  float *q_cent, *k_cent, *v_cent, *sbar, *stab, *lse_tmp;
+  float *q_cent, *k_cent, *v_cent, *stab, *lse_tmp;
   double* err;
   int64_t* entries;
   bf16 *qp, *kp, *vp;
@@ -52,7 +53,7 @@ bool plan_forward(const SvgEarShape& s, Carver& cv, ForwardPlan& p) {
   p.q_cent = cv.take<float>((size_t)s.bh * s.c_q * s.d);
   p.k_cent = cv.take<float>((size_t)s.bh * s.c_k * s.d);
   p.v_cent = cv.take<float>((size_t)s.bh * s.c_k * s.d);
-  p.sbar = cv.take<float>((size_t)s.bh * s.c_q * s.c_k);
+  p.es.carve(cv, s);
   p.stab = cv.take<float>((size_t)s.bh * s.c_q);
   p.lse_tmp = cv.take<float>((size_t)s.bh * s.n_q);
   p.err = cv.take<double>((size_t)s.bh * s.c_q * s.c_k);
@@ -141,7 +142,7 @@ int svgear_segment_means(int32_t bh, int32_t n, int32_t d, int32_t c, const void
                               (cudaStream_t)stream);
 }
 
-int svgear_error_table(const SvgEarShape* shape, int32_t mode, const float* q_centroids,
+int svgear_error_table(const SvgEarShape* shape, int32_t exec_mode, int32_t mode, const float* q_centroids,
                        const float* k_centroids, const float* v_centroids, const void* k_permuted,
                        const void* v_permuted, const int32_t* q_sizes, const int32_t* k_sizes,
                        const int32_t* k_offsets, double* error_table, float* stabilizers,
@@ -154,11 +155,12 @@ int svgear_error_table(const SvgEarShape* shape, int32_t mode, const float* q_ce
   if (!shape_ok(shape)) return SVGEAR_ESHAPE;
   if (!device_present()) return SVGEAR_ECUDA;
   Carver cv(workspace, workspace_bytes);
-  float* sbar = cv.take<float>((size_t)shape->bh * shape->c_q * shape->c_k);
-  if (!cv.ok) return SVGEAR_EWORKSPACE;
-  return launch_error_table(*shape, mode, q_centroids, k_centroids, v_centroids,
+  ErrScratch es;
+  if (!es.carve(cv, *shape)) return SVGEAR_EWORKSPACE;
+  if (exec_mode != SVGEAR_EXEC_BF16_TENSOR && exec_mode != SVGEAR_EXEC_FP32_CHECK) return SVGEAR_EINVAL;
+  return launch_error_table(*shape, exec_mode, mode, q_centroids, k_centroids, v_centroids,
                             (const bf16*)k_permuted, (const bf16*)v_permuted, q_sizes, k_sizes,
-                            k_offsets, error_table, stabilizers, sbar, (cudaStream_t)stream);
+                            k_offsets, error_table, stabilizers, es, (cudaStream_t)stream);
 }
 
 int svgear_route_error_aware(int32_t bh, int32_t c_q, int32_t c_k, const double* error_table,
@@ -278,8 +280,8 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
   rc = launch_segment_means(s.bh, s.n_k, s.d, s.c_k, p.vp, k_sizes, k_offsets, v_cent, nullptr, st);
   if (rc) return rc;
   // (2) error table + routing
-  rc = launch_error_table(s, estimator_mode, q_cent, k_cent, v_cent, p.kp, p.vp, q_sizes, k_sizes,
-                          k_offsets, err, stab, p.sbar, st);
+  rc = launch_error_table(s, exec_mode, estimator_mode, q_cent, k_cent, v_cent, p.kp, p.vp, q_sizes,
+                          k_sizes, k_offsets, err, stab, p.es, st);
   if (rc) return rc;
   rc = launch_route(s.bh, s.c_q, s.c_k, err, q_sizes, k_sizes, capacity_entries, overshoot,
                     single_item_fallback ? 1 : 0, 0, mask, entries, st);

@@ -112,10 +112,18 @@ int launch_gather_rows(int bh, int n, int d, const bf16* x, const int32_t* perm,
 int launch_segment_means(int bh, int n, int d, int c, const bf16* xp, const int32_t* sizes,
                          const int32_t* offsets, float* means, float* norms, cudaStream_t st);
 
-int launch_error_table(const SvgEarShape& s, int mode, const float* qc, const float* kc,
+struct ErrScratch {
+  float* sbar;    // [bh][c_q][c_k] centroid logits
+  bf16* kd_hi;    // [bh][n_k][d]   k - k̄ split into bf16 hi / lo (tensor-core path)
+  bf16* kd_lo;
+  float4* kstat;  // [bh][n_k]      (A, 2B, C, -) per key
+  bf16* qsplit;   // [bh][2][cqpad][d]
+  bool carve(Carver& cv, const SvgEarShape& s);
+};
+int launch_error_table(const SvgEarShape& s, int exec_mode, int mode, const float* qc, const float* kc,
                        const float* vc, const bf16* kp, const bf16* vp, const int32_t* q_sizes,
                        const int32_t* k_sizes, const int32_t* k_offsets, double* err,
-                       float* stabilizers, float* sbar, cudaStream_t st);
+                       float* stabilizers, ErrScratch& sc, cudaStream_t st);
 
 struct RouteScratch {
   int32_t* state;  // per-head scratch ints

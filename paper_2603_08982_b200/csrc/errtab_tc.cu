@@ -1,0 +1,345 @@
+// Value-aware / plain block error table on the tensor cores (tcgen05 + TMEM), sm_100a.
+//
+// Same quantity and arithmetic as error_table_kernel in stats_route.cu (which documents the
+// algebra and cites the reference, estimator.py:187-253 / 120-148):
+//     E[i,j] = |q_i| * w̄_ij^2 * sum_{t in cluster j} ( A_t - 2 x B_t + x^2 C_t ),  x = expm1(g_it),
+//     g_it = q̄_i . (k_t - k̄_j) / sqrt(d)
+// but the C_q x N_k x d contraction g runs on the tensor cores:
+//   * key_stats_kernel writes, per key, kd = k_t - k̄_j split into bf16 (hi, lo) and the scalars
+//     (A_t, B_t, C_t);
+//   * q̄ is split into bf16 (hi, lo); g = qh.dh + qh.dl + ql.dh accumulates in fp32 in TMEM
+//     (the dropped ql.dl term is 2^-18 relative);
+//   * the epilogue owns one query cluster per thread (TMEM lane) and walks the key columns of a
+//     key cluster in order, so the per-block sum and its running-max rescale stay in registers and
+//     each E[i,j] is written exactly once — no atomics, deterministic.
+// CTA = (instance, 128 query clusters, a range of key clusters); key clusters stream through in
+// chunks of <= 128 keys (N = chunk rounded up to 16), two TMEM buffers, two epilogue warp groups.
+//   warps 0-3 / 4-7 : epilogue groups (even / odd key clusters of the range)
+//   warp 8 : producer      warp 9 : TMEM allocator + MMA issuer
+#include "tc_common.cuh"
+
+namespace svg {
+
+using namespace tc;
+
+namespace {
+constexpr int EM = 128;       // query clusters per CTA (M)
+constexpr int ECH = 128;      // max keys per chunk
+constexpr int ERANGE = 16;    // key clusters per CTA
+constexpr int ETHREADS = 320;
+enum { EB_AFULL = 0, EB_BFULL = 1, EB_BEMPTY = 3, EB_ACCFULL = 5, EB_ACCEMPTY = 7 };
+
+template <int D>
+struct ESmem {
+  static constexpr int kTile = EM * D * 2;        // one [128 x d] bf16 tile
+  static constexpr int kA = 0;                    // qh, ql
+  static constexpr int kB = kA + 2 * kTile;       // 2 stages x (dh, dl)
+  static constexpr int kBars = kB + 4 * kTile;
+  static constexpr size_t bytes() { return 1024 + kBars + 256; }
+};
+
+#define TMEM_LD16(taddr, r)                                                                       \
+  asm volatile(                                                                                   \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "                                                   \
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"           \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),       \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),   \
+        "=r"(r[14]), "=r"(r[15])                                                                  \
+      : "r"(taddr)                                                                                \
+      : "memory")
+
+__device__ __forceinline__ float expm1_fast(float g) {
+  // |g| < 0.25: degree-6 Taylor (relative error < 2e-8); otherwise 2^(g log2 e) - 1
+  const float poly = g * fmaf(g, fmaf(g, fmaf(g, fmaf(g, fmaf(g, 1.f / 720.f, 1.f / 120.f), 1.f / 24.f), 1.f / 6.f), 0.5f), 1.f);
+  const float big = ex2(g * 1.4426950408889634f) - 1.f;
+  return fabsf(g) < 0.25f ? poly : big;
+}
+}  // namespace
+
+// per key: kd = k - k̄_j as bf16 (hi, lo); (A, B, C) = (|v̄-v|^2, (v̄-v).v, |v|^2)  [plain: 0,0,1]
+template <int D>
+__global__ void __launch_bounds__(128)
+    key_stats_kernel(int mode, const float* __restrict__ kc, const float* __restrict__ vc,
+                     const bf16* __restrict__ kp, const bf16* __restrict__ vp,
+                     const int32_t* __restrict__ k_sizes, const int32_t* __restrict__ k_offsets, int n_k,
+                     int c_k, bf16* __restrict__ kd_hi, bf16* __restrict__ kd_lo, float4* __restrict__ kstat) {
+  const int h = blockIdx.y, j = blockIdx.x;
+  constexpr int EPL = D / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nj = k_sizes[(size_t)h * c_k + j], o = k_offsets[(size_t)h * c_k + j];
+  float kb[EPL], vb[EPL];
+#pragma unroll
+  for (int u = 0; u < EPL; ++u) {
+    kb[u] = kc[((size_t)h * c_k + j) * D + lane * EPL + u];
+    vb[u] = mode == SVGEAR_EST_VALUE_AWARE ? vc[((size_t)h * c_k + j) * D + lane * EPL + u] : 0.f;
+  }
+  for (int r = warp; r < nj; r += 4) {
+    const size_t row = (size_t)h * n_k + o + r;
+    float kf[EPL], vf[EPL];
+    if constexpr (EPL == 4) {
+      const uint2 ku = __ldg(reinterpret_cast<const uint2*>(kp + row * D + lane * 4));
+      kf[0] = __uint_as_float(ku.x << 16); kf[1] = __uint_as_float(ku.x & 0xffff0000u);
+      kf[2] = __uint_as_float(ku.y << 16); kf[3] = __uint_as_float(ku.y & 0xffff0000u);
+      if (mode == SVGEAR_EST_VALUE_AWARE) {
+        const uint2 vu = __ldg(reinterpret_cast<const uint2*>(vp + row * D + lane * 4));
+        vf[0] = __uint_as_float(vu.x << 16); vf[1] = __uint_as_float(vu.x & 0xffff0000u);
+        vf[2] = __uint_as_float(vu.y << 16); vf[3] = __uint_as_float(vu.y & 0xffff0000u);
+      }
+    } else {
+      const uint32_t ku = __ldg(reinterpret_cast<const uint32_t*>(kp + row * D + lane * 2));
+      kf[0] = __uint_as_float(ku << 16); kf[1] = __uint_as_float(ku & 0xffff0000u);
+      if (mode == SVGEAR_EST_VALUE_AWARE) {
+        const uint32_t vu = __ldg(reinterpret_cast<const uint32_t*>(vp + row * D + lane * 2));
+        vf[0] = __uint_as_float(vu << 16); vf[1] = __uint_as_float(vu & 0xffff0000u);
+      }
+    }
+    float a = 0.f, b = 0.f, cc = 0.f;
+    uint32_t hi[EPL / 2], lo[EPL / 2];
+#pragma unroll
+    for (int u = 0; u < EPL; u += 2) {
+      const float d0 = kf[u] - kb[u], d1 = kf[u + 1] - kb[u + 1];
+      const bf16 h0 = __float2bfloat16_rn(d0), h1 = __float2bfloat16_rn(d1);
+      hi[u / 2] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+      lo[u / 2] = pack_bf16x2(d0 - __bfloat162float(h0), d1 - __bfloat162float(h1));
+    }
+    if (mode == SVGEAR_EST_VALUE_AWARE) {
+#pragma unroll
+      for (int u = 0; u < EPL; ++u) {
+        const float dv = vb[u] - vf[u];
+        a = fmaf(dv, dv, a);
+        b = fmaf(dv, vf[u], b);
+        cc = fmaf(vf[u], vf[u], cc);
+      }
+      a = warp_sum(a); b = warp_sum(b); cc = warp_sum(cc);
+    } else {
+      cc = 1.f;
+    }
+    if constexpr (EPL == 4) {
+      *reinterpret_cast<uint2*>(kd_hi + row * D + lane * 4) = make_uint2(hi[0], hi[1]);
+      *reinterpret_cast<uint2*>(kd_lo + row * D + lane * 4) = make_uint2(lo[0], lo[1]);
+    } else {
+      *reinterpret_cast<uint32_t*>(kd_hi + row * D + lane * 2) = hi[0];
+      *reinterpret_cast<uint32_t*>(kd_lo + row * D + lane * 2) = lo[0];
+    }
+    if (lane == 0) kstat[row] = make_float4(a, 2.f * b, cc, 0.f);
+  }
+}
+
+// q̄ -> bf16 (hi, lo), zero padded to a multiple of 128 rows: [bh][2][cqpad][d]
+__global__ void split_q_kernel(const float* __restrict__ qc, int d, int c_q, int cqpad, bf16* __restrict__ qsplit) {
+  const int h = blockIdx.y;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= cqpad * d) return;
+  const float v = (idx / d) < c_q ? qc[(size_t)h * c_q * d + idx] : 0.f;
+  const bf16 hi = __float2bfloat16_rn(v);
+  qsplit[((size_t)h * 2 + 0) * cqpad * d + idx] = hi;
+  qsplit[((size_t)h * 2 + 1) * cqpad * d + idx] = __float2bfloat16_rn(v - __bfloat162float(hi));
+}
+
+template <int D>
+__global__ void __launch_bounds__(ETHREADS, 1)
+    error_table_tc_kernel(const bf16* __restrict__ qsplit, const bf16* __restrict__ kd_hi,
+                          const bf16* __restrict__ kd_lo, const float4* __restrict__ kstat,
+                          const int32_t* __restrict__ q_sizes, const int32_t* __restrict__ k_sizes,
+                          const int32_t* __restrict__ k_offsets, const float* __restrict__ sbar,
+                          const float* __restrict__ mref, int n_k, int c_q, int c_k, int cqpad, float scale,
+                          double* __restrict__ err) {
+  using L = ESmem<D>;
+  const int h = blockIdx.z, mt = blockIdx.y;
+  const int j_lo = blockIdx.x * ERANGE, j_hi = min(c_k, j_lo + ERANGE);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t sA = sbase + L::kA, sB = sbase + L::kB, bars = sbase + L::kBars;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kBars + 192);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto bar = [&](int i) -> uint32_t { return bars + 8u * (uint32_t)i; };
+
+  if (tid == 0) {
+    mbar_init(bar(EB_AFULL), 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(bar(EB_BFULL + s), 1);
+      mbar_init(bar(EB_BEMPTY + s), 1);
+      mbar_init(bar(EB_ACCFULL + s), 1);
+      mbar_init(bar(EB_ACCEMPTY + s), 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(smem_u32(tmem_slot), 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int32_t* ksz = k_sizes + (size_t)h * c_k;
+  const int32_t* kof = k_offsets + (size_t)h * c_k;
+
+  if (warp == 8) {
+    // =========================== producer ========================================================
+    constexpr int CPR = D / 8, RPI = 32 / CPR;
+    const int sub = lane / CPR, chunk = lane % CPR;
+    for (int p = 0; p < 2; ++p) {
+      const bf16* src = qsplit + (((size_t)h * 2 + p) * cqpad + (size_t)mt * EM) * D;
+      for (int r0 = 0; r0 < EM; r0 += RPI) {
+        const int r = r0 + sub;
+        cp_async16(sA + (uint32_t)(p * L::kTile + (chunk >> 3) * (EM * 128)) + swz(r, chunk & 7),
+                   src + (size_t)r * D + chunk * 8);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar(EB_AFULL));
+    int u = 0;
+    for (int j = j_lo; j < j_hi; ++j) {
+      const int nj = ksz[j], o = kof[j];
+      for (int s0 = 0; s0 < nj; s0 += ECH, ++u) {
+        const int st = u & 1;
+        if (u >= 2) mbar_wait(bar(EB_BEMPTY + st), ((u >> 1) + 1) & 1);
+        const int nn = ((min(ECH, nj - s0) + 15) >> 4) << 4;
+        for (int p = 0; p < 2; ++p) {
+          const bf16* src = (p == 0 ? kd_hi : kd_lo) + (size_t)h * n_k * D;
+          const uint32_t dst = sB + (uint32_t)((st * 2 + p) * L::kTile);
+          for (int r0 = 0; r0 < nn; r0 += RPI) {
+            const int r = r0 + sub;
+            const int row = min(o + s0 + r, n_k - 1);
+            cp_async16(dst + (uint32_t)((chunk >> 3) * (EM * 128)) + swz(r, chunk & 7),
+                       src + (size_t)row * D + chunk * 8);
+          }
+        }
+        cp_async_commit();
+        cp_async_wait_all();
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(EB_BFULL + st));
+      }
+    }
+  } else if (warp == 9) {
+    // =========================== MMA issuer ======================================================
+    if (lane == 0) {
+      mbar_wait(bar(EB_AFULL), 0);
+      int u = 0, uses[2] = {0, 0};
+      for (int j = j_lo; j < j_hi; ++j) {
+        const int nj = ksz[j];
+        const int g = (j - j_lo) & 1;  // TMEM buffer / epilogue group of this key cluster
+        for (int s0 = 0; s0 < nj; s0 += ECH, ++u) {
+          const int st = u & 1;
+          const int nn = ((min(ECH, nj - s0) + 15) >> 4) << 4;
+          const uint32_t idesc = make_idesc(EM, nn, 0);
+          if (uses[g] >= 1) mbar_wait(bar(EB_ACCEMPTY + g), (uses[g] - 1) & 1);
+          mbar_wait(bar(EB_BFULL + st), (u >> 1) & 1);
+          tc_fence_after();
+          // g = qh.dh + qh.dl + ql.dh
+#pragma unroll
+          for (int prod = 0; prod < 3; ++prod) {
+            const uint32_t at = sA + (uint32_t)((prod == 2 ? 1 : 0) * L::kTile);
+            const uint32_t bt = sB + (uint32_t)((st * 2 + (prod == 1 ? 1 : 0)) * L::kTile);
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint64_t ad = make_desc(at + (uint32_t)((kk >> 2) * (EM * 128) + (kk & 3) * 32), 16, 1024);
+              const uint64_t bd = make_desc(bt + (uint32_t)((kk >> 2) * (EM * 128) + (kk & 3) * 32), 16, 1024);
+              umma_ss(tmem + (uint32_t)(g * 128), ad, bd, idesc, (prod > 0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(bar(EB_BEMPTY + st));
+          umma_commit(bar(EB_ACCFULL + g));
+          ++uses[g];
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // =========================== epilogue groups =================================================
+    const int g = warp >> 2;
+    const int i = mt * EM + (warp & 3) * 32 + lane;  // query cluster of this thread
+    const bool live = i < c_q;
+    const uint32_t tcol = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(g * 128);
+    const float mr = live ? mref[(size_t)h * c_q + i] : 0.f;
+    const double nq = live ? (double)q_sizes[(size_t)h * c_q + i] : 0.0;
+    const float4* ks = kstat + (size_t)h * n_k;
+    int uses = 0;
+    for (int j = j_lo + g; j < j_hi; j += 2) {
+      const int nj = ksz[j], o = kof[j];
+      float M = 0.f, em = 1.f, em2 = 1.f, acc = 0.f;
+      for (int s0 = 0; s0 < nj; s0 += ECH, ++uses) {
+        const int valid = min(ECH, nj - s0);
+        mbar_wait(bar(EB_ACCFULL + g), uses & 1);
+        tc_fence_after();
+        for (int c0 = 0; c0 < valid; c0 += 16) {
+          uint32_t a[16];
+          TMEM_LD16(tcol + c0, a);
+          tc_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            if (c0 + q < valid) {
+              const float4 st4 = __ldg(ks + o + s0 + c0 + q);
+              const float gg = __uint_as_float(a[q]) * scale;
+              if (gg > M) {
+                const float r = __expf(M - gg);
+                acc *= r * r;
+                M = gg;
+                em = __expf(-M);
+                em2 = em * em;
+              }
+              const float xs = gg < 20.f ? expm1_fast(gg) * em : (__expf(gg - M) - em);
+              acc += st4.x * em2 - (em * xs) * st4.y + (xs * xs) * st4.z;
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(bar(EB_ACCEMPTY + g));
+      }
+      if (live) {
+        const size_t e = ((size_t)h * c_q + i) * c_k + j;
+        const double lift = 2.0 * ((double)sbar[e] - (double)mr + (double)M);
+        err[e] = nq * ((double)fmaxf(acc, 0.f) * exp(lift));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+size_t errtab_tc_scratch_bytes(const SvgEarShape& s) {
+  const int cqpad = ceil_div(s.c_q, EM) * EM;
+  return align_up((size_t)s.bh * s.n_k * s.d * 2, 256) * 2 + align_up((size_t)s.bh * s.n_k * 16, 256) +
+         align_up((size_t)s.bh * 2 * cqpad * s.d * 2, 256) + 1024;
+}
+
+int launch_error_table_tc(const SvgEarShape& s, int mode, const float* qc, const float* kc, const float* vc,
+                          const bf16* kp, const bf16* vp, const int32_t* q_sizes, const int32_t* k_sizes,
+                          const int32_t* k_offsets, const float* sbar, const float* mref, bf16* kd_hi,
+                          bf16* kd_lo, float4* kstat, bf16* qsplit, double* err, cudaStream_t st) {
+  const int cqpad = ceil_div(s.c_q, EM) * EM;
+  const float scale = 1.0f / sqrtf((float)s.d);
+  split_q_kernel<<<dim3(ceil_div(cqpad * s.d, 256), s.bh), 256, 0, st>>>(qc, s.d, s.c_q, cqpad, qsplit);
+  SVG_LAUNCH_OK();
+  dim3 grid(ceil_div(s.c_k, ERANGE), cqpad / EM, s.bh);
+  if (s.d == 128) {
+    key_stats_kernel<128><<<dim3(s.c_k, s.bh), 128, 0, st>>>(mode, kc, vc, kp, vp, k_sizes, k_offsets, s.n_k,
+                                                            s.c_k, kd_hi, kd_lo, kstat);
+    SVG_LAUNCH_OK();
+    const size_t smem = ESmem<128>::bytes();
+    SVG_CUDA_OK(cudaFuncSetAttribute(error_table_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    error_table_tc_kernel<128><<<grid, ETHREADS, smem, st>>>(qsplit, kd_hi, kd_lo, kstat, q_sizes, k_sizes,
+                                                             k_offsets, sbar, mref, s.n_k, s.c_q, s.c_k, cqpad,
+                                                             scale, err);
+  } else {
+    key_stats_kernel<64><<<dim3(s.c_k, s.bh), 128, 0, st>>>(mode, kc, vc, kp, vp, k_sizes, k_offsets, s.n_k,
+                                                           s.c_k, kd_hi, kd_lo, kstat);
+    SVG_LAUNCH_OK();
+    const size_t smem = ESmem<64>::bytes();
+    SVG_CUDA_OK(cudaFuncSetAttribute(error_table_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    error_table_tc_kernel<64><<<grid, ETHREADS, smem, st>>>(qsplit, kd_hi, kd_lo, kstat, q_sizes, k_sizes,
+                                                            k_offsets, sbar, mref, s.n_k, s.c_q, s.c_k, cqpad,
+                                                            scale, err);
+  }
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
+}  // namespace svg

@@ -144,50 +144,75 @@ __global__ void __launch_bounds__(1024)
   int32_t* assign = assign_all + (size_t)h * n;
   float* own = own_all + (size_t)h * n;
   int32_t* sizes = sizes_all + (size_t)h * c;
+  constexpr int kMaxList = 1024;
   __shared__ float s_val[32];
   __shared__ int s_idx[32];
+  __shared__ int s_wcount[32];
+  __shared__ int s_empty[kMaxList];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  int local = 0;
-  for (int j = tid; j < c; j += blockDim.x) local |= (sizes[j] == 0);
-  if (!__syncthreads_or(local)) return;
-
-  for (int e = 0; e < c; ++e) {
-    __syncthreads();
-    if (sizes[e] != 0) continue;  // block-uniform
-    float bv = -1.f;
-    int bx = 0x7fffffff;
-    for (int t = tid; t < n; t += blockDim.x) {
-      if (sizes[assign[t]] >= 2) {
-        float v = own[t];
-        if (v > bv) { bv = v; bx = t; }
+  while (true) {
+    // ascending list of the (first kMaxList) empty clusters; a repaired cluster never becomes
+    // empty again because donors only come from clusters with >= 2 members
+    int carry = 0;
+    for (int base = 0; base < c; base += 1024) {
+      const int j = base + tid;
+      const bool flag = j < c && sizes[j] == 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, flag);
+      __syncthreads();
+      if (lane == 0) s_wcount[warp] = __popc(bal);
+      __syncthreads();
+      int woff = 0, tot = 0;
+      for (int w = 0; w < 32; ++w) {
+        const int cw = s_wcount[w];
+        if (w < warp) woff += cw;
+        tot += cw;
       }
+      const int pos = carry + woff + __popc(bal & ((1u << lane) - 1u));
+      if (flag && pos < kMaxList) s_empty[pos] = j;
+      carry += tot;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      int ox = __shfl_xor_sync(0xffffffffu, bx, o);
-      if (ov > bv || (ov == bv && ox < bx)) { bv = ov; bx = ox; }
-    }
-    if (lane == 0) { s_val[warp] = bv; s_idx[warp] = bx; }
     __syncthreads();
-    if (warp == 0) {
-      int nw = blockDim.x >> 5;
-      bv = lane < nw ? s_val[lane] : -1.f;
-      bx = lane < nw ? s_idx[lane] : 0x7fffffff;
+    const int ne = min(carry, kMaxList);
+    if (ne == 0) return;
+    for (int ei = 0; ei < ne; ++ei) {
+      const int e = s_empty[ei];
+      __syncthreads();
+      float bv = -1.f;
+      int bx = 0x7fffffff;
+      for (int t = tid; t < n; t += blockDim.x) {
+        if (sizes[assign[t]] >= 2) {
+          float v = own[t];
+          if (v > bv) { bv = v; bx = t; }
+        }
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         float ov = __shfl_xor_sync(0xffffffffu, bv, o);
         int ox = __shfl_xor_sync(0xffffffffu, bx, o);
         if (ov > bv || (ov == bv && ox < bx)) { bv = ov; bx = ox; }
       }
-      if (lane == 0 && bx != 0x7fffffff) {
-        sizes[assign[bx]] -= 1;
-        sizes[e] += 1;
-        assign[bx] = e;
-        own[bx] = 0.f;
+      if (lane == 0) { s_val[warp] = bv; s_idx[warp] = bx; }
+      __syncthreads();
+      if (warp == 0) {
+        bv = s_val[lane];
+        bx = s_idx[lane];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          int ox = __shfl_xor_sync(0xffffffffu, bx, o);
+          if (ov > bv || (ov == bv && ox < bx)) { bv = ov; bx = ox; }
+        }
+        if (lane == 0 && bx != 0x7fffffff) {
+          sizes[assign[bx]] -= 1;
+          sizes[e] += 1;
+          assign[bx] = e;
+          own[bx] = 0.f;
+        }
       }
     }
+    __syncthreads();
+    if (carry <= kMaxList) return;
   }
 }
 
@@ -280,10 +305,15 @@ __global__ void __launch_bounds__(1024)
       offsets[j] = run;
       int base = run;
       int32_t* col = chunk_counts + (size_t)h * nchunks * c + j;
-      for (int chn = 0; chn < nchunks; ++chn) {
-        int cnt = col[(size_t)chn * c];
-        col[(size_t)chn * c] = base;
-        base += cnt;
+      for (int ch0 = 0; ch0 < nchunks; ch0 += 8) {
+        int cnt[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cnt[q] = ch0 + q < nchunks ? col[(size_t)(ch0 + q) * c] : 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (ch0 + q < nchunks) col[(size_t)(ch0 + q) * c] = base;
+          base += cnt[q];
+        }
       }
     }
     run += v[u];
@@ -352,19 +382,31 @@ __global__ void __launch_bounds__(128)
   double acc[EPL];
 #pragma unroll
   for (int u = 0; u < EPL; ++u) acc[u] = 0.0;
-  for (int r = warp; r < nj; r += 4) {
-    const int row = perm ? perm[(size_t)h * n + o + r] : (o + r);
-    const bf16* p = x + ((size_t)h * n + row) * D + lane * EPL;
-    if (EPL == 4) {
-      uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
-      acc[0] += (double)__uint_as_float(u.x << 16);
-      acc[1] += (double)__uint_as_float(u.x & 0xffff0000u);
-      acc[2] += (double)__uint_as_float(u.y << 16);
-      acc[3] += (double)__uint_as_float(u.y & 0xffff0000u);
-    } else {
-      uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(p));
-      acc[0] += (double)__uint_as_float(u << 16);
-      acc[1] += (double)__uint_as_float(u & 0xffff0000u);
+  // rows are taken 32 at a time: warp w owns rows 8w..8w+7 of each group and issues its 8 row
+  // loads back to back (independent), then accumulates them in ascending order
+  for (int base = 0; base < nj; base += 32) {
+    int pidx = 0;
+    if (base + lane < nj) pidx = perm ? perm[(size_t)h * n + o + base + lane] : (o + base + lane);
+    uint2 buf[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int r = warp * 8 + q;
+      const int row = __shfl_sync(0xffffffffu, pidx, r);
+      buf[q] = make_uint2(0u, 0u);
+      if (base + r < nj) {
+        const bf16* p = x + ((size_t)h * n + row) * D + lane * EPL;
+        if (EPL == 4) buf[q] = __ldg(reinterpret_cast<const uint2*>(p));
+        else buf[q].x = __ldg(reinterpret_cast<const uint32_t*>(p));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      acc[0] += (double)__uint_as_float(buf[q].x << 16);
+      acc[1] += (double)__uint_as_float(buf[q].x & 0xffff0000u);
+      if constexpr (EPL == 4) {
+        acc[2] += (double)__uint_as_float(buf[q].y << 16);
+        acc[3] += (double)__uint_as_float(buf[q].y & 0xffff0000u);
+      }
     }
   }
 #pragma unroll

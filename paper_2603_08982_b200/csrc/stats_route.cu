@@ -178,14 +178,33 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-int launch_error_table(const SvgEarShape& s, int mode, const float* qc, const float* kc,
+int launch_error_table_tc(const SvgEarShape& s, int mode, const float* qc, const float* kc, const float* vc,
+                          const bf16* kp, const bf16* vp, const int32_t* q_sizes, const int32_t* k_sizes,
+                          const int32_t* k_offsets, const float* sbar, const float* mref, bf16* kd_hi,
+                          bf16* kd_lo, float4* kstat, bf16* qsplit, double* err, cudaStream_t st);
+
+bool ErrScratch::carve(Carver& cv, const SvgEarShape& s) {
+  const int cqpad = ceil_div(s.c_q, 128) * 128;
+  sbar = cv.take<float>((size_t)s.bh * s.c_q * s.c_k);
+  kd_hi = cv.take<bf16>((size_t)s.bh * s.n_k * s.d);
+  kd_lo = cv.take<bf16>((size_t)s.bh * s.n_k * s.d);
+  kstat = cv.take<float4>((size_t)s.bh * s.n_k);
+  qsplit = cv.take<bf16>((size_t)s.bh * 2 * cqpad * s.d);
+  return cv.ok;
+}
+
+int launch_error_table(const SvgEarShape& s, int exec_mode, int mode, const float* qc, const float* kc,
                        const float* vc, const bf16* kp, const bf16* vp, const int32_t* q_sizes,
                        const int32_t* k_sizes, const int32_t* k_offsets, double* err,
-                       float* stabilizers, float* sbar, cudaStream_t st) {
+                       float* stabilizers, ErrScratch& sc, cudaStream_t st) {
   const float scale = 1.0f / sqrtf((float)s.d);
+  float* sbar = sc.sbar;
   centroid_logits_kernel<<<dim3(s.c_q, s.bh), 256, 0, st>>>(qc, kc, s.d, s.c_q, s.c_k, scale, sbar,
                                                            stabilizers);
   SVG_LAUNCH_OK();
+  if (exec_mode == SVGEAR_EXEC_BF16_TENSOR)
+    return launch_error_table_tc(s, mode, qc, kc, vc, kp, vp, q_sizes, k_sizes, k_offsets, sbar, stabilizers,
+                                 sc.kd_hi, sc.kd_lo, sc.kstat, sc.qsplit, err, st);
   const int passes = ceil_div(s.c_q, 256);
   const int thr = min(256, max(128, ceil_div(ceil_div(s.c_q, passes), 32) * 32));
   if (s.d == 128)
@@ -290,22 +309,35 @@ __device__ __forceinline__ unsigned long long ord64(double v) {
   unsigned long long u = (unsigned long long)__double_as_longlong(v);
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
-__device__ __forceinline__ unsigned int prio_digit(const Prio& p, int pass) {
-  // 20 digits of 8 bits, most significant first: a[7..0], b[7..0], c[3..0]
-  if (pass < 8) return (unsigned int)(p.a >> (56 - 8 * pass)) & 0xffu;
-  if (pass < 16) return (unsigned int)(p.b >> (56 - 8 * (pass - 8))) & 0xffu;
-  return (p.c >> (24 - 8 * (pass - 16))) & 0xffu;
+// Radix-select digit schedule over the 160-bit key (a:64 | b:64 | c:32), most significant first,
+// 11-bit digits: a -> 6 passes, b -> 6 passes, c -> 3 passes.
+constexpr int kRouteBins = 2048;
+constexpr int kRoutePasses = 15;
+__device__ __forceinline__ void pass_geom(int pass, int& field, int& shift, int& width) {
+  if (pass < 12) {
+    field = pass / 6;
+    const int q = pass % 6;
+    shift = q < 5 ? 53 - 11 * q : 0;
+    width = q < 5 ? 11 : 9;
+  } else {
+    field = 2;
+    const int q = pass - 12;
+    shift = q == 0 ? 21 : (q == 1 ? 10 : 0);
+    width = q == 2 ? 10 : 11;
+  }
 }
-__device__ __forceinline__ bool prio_prefix_eq(const Prio& p, const Prio& q, int pass) {
-  // do the first `pass` digits of p and q agree?
-  if (pass <= 0) return true;
-  if (pass < 8) return (p.a >> (64 - 8 * pass)) == (q.a >> (64 - 8 * pass));
+__device__ __forceinline__ unsigned int prio_digit(const Prio& p, int field, int shift, int width) {
+  const unsigned long long v = field == 0 ? p.a : (field == 1 ? p.b : (unsigned long long)p.c);
+  return (unsigned int)(v >> shift) & ((1u << width) - 1u);
+}
+// do all digits BEFORE this pass agree with the chosen prefix?
+__device__ __forceinline__ bool prio_prefix_eq(const Prio& p, const Prio& q, int field, int shift, int width) {
+  const int hs = shift + width;  // bits of the current field already fixed are those above hs
+  if (field == 0) return hs >= 64 ? true : (p.a >> hs) == (q.a >> hs);
   if (p.a != q.a) return false;
-  if (pass == 8) return true;
-  if (pass < 16) return (p.b >> (64 - 8 * (pass - 8))) == (q.b >> (64 - 8 * (pass - 8)));
+  if (field == 1) return hs >= 64 ? true : (p.b >> hs) == (q.b >> hs);
   if (p.b != q.b) return false;
-  if (pass == 16) return true;
-  return (p.c >> (32 - 8 * (pass - 16))) == (q.c >> (32 - 8 * (pass - 16)));
+  return hs >= 32 ? true : (p.c >> hs) == (q.c >> hs);
 }
 
 __global__ void __launch_bounds__(1024)
@@ -319,8 +351,8 @@ __global__ void __launch_bounds__(1024)
   const int32_t* qs = q_sizes_all + (size_t)h * c_q;
   uint8_t* mask = mask_all + (size_t)h * nb;
   extern __shared__ int32_t s_ks[];  // [c_k]
-  __shared__ unsigned long long s_hw[256];
-  __shared__ unsigned int s_hc[256];
+  __shared__ unsigned long long s_hw[kRouteBins];
+  __shared__ unsigned int s_hc[kRouteBins];
   __shared__ Prio s_prefix;  // digits chosen so far (others zero)
   __shared__ Prio s_red[32];
   __shared__ long long s_redw[32];
@@ -328,57 +360,104 @@ __global__ void __launch_bounds__(1024)
   __shared__ long long s_base;
   __shared__ int s_flag;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int j = tid; j < c_k; j += blockDim.x) s_ks[j] = k_sizes_all[(size_t)h * c_k + j];
+  const int nthr = blockDim.x;
+  for (int j = tid; j < c_k; j += nthr) s_ks[j] = k_sizes_all[(size_t)h * c_k + j];
   if (tid == 0) { s_prefix.a = 0; s_prefix.b = 0; s_prefix.c = 0; s_base = 0; s_flag = 0; }
   __syncthreads();
 
-  auto weight = [&](int b) -> long long { return (long long)qs[b / c_k] * (long long)s_ks[b % c_k]; };
-  auto prio = [&](int b, long long w) -> Prio {
+  auto prio = [&](int b, double v, long long w) -> Prio {
     Prio p;
-    const double v = val[b];
     p.a = ord64(ratio_mode == 0 ? v / (double)w : v);
     p.b = ord64(v);
     p.c = ~(unsigned int)b;
     return p;
   };
+  // iterate this thread's blocks b = tid, tid + nthr, ... keeping (row, col) incrementally
+#define FOR_BLOCKS(BODY)                                        \
+  {                                                             \
+    int qi_ = tid / c_k, kj_ = tid % c_k;                       \
+    const int dq_ = nthr / c_k, dk_ = nthr % c_k;               \
+    for (int b = tid; b < nb; b += nthr) {                      \
+      const long long w = (long long)qs[qi_] * (long long)s_ks[kj_]; \
+      BODY                                                      \
+      qi_ += dq_; kj_ += dk_;                                   \
+      if (kj_ >= c_k) { kj_ -= c_k; ++qi_; }                    \
+    }                                                           \
+  }
 
   // ---- phase 1: first block that does not fit ---------------------------------------------------
   bool all_fit = false;
-  int npass = 0;
-  for (int pass = 0; pass < 20; ++pass) {
-    for (int k = tid; k < 256; k += blockDim.x) { s_hw[k] = 0ull; s_hc[k] = 0u; }
+  int last_field = 0, last_shift = 64, last_width = 0;
+  for (int pass = 0; pass < kRoutePasses; ++pass) {
+    int field, shift, width;
+    pass_geom(pass, field, shift, width);
+    for (int k = tid; k < kRouteBins; k += nthr) { s_hw[k] = 0ull; s_hc[k] = 0u; }
     __syncthreads();
     const Prio pre = s_prefix;
-    for (int b = tid; b < nb; b += blockDim.x) {
-      const long long w = weight(b);
-      const Prio p = prio(b, w);
-      if (prio_prefix_eq(p, pre, pass)) {
-        const unsigned int dg = prio_digit(p, pass);
-        atomicAdd(&s_hw[dg], (unsigned long long)w);
-        atomicAdd(&s_hc[dg], 1u);
-      }
+    {
+      // run-length accumulation: consecutive candidates usually share the digit in the top passes
+      unsigned int rd = 0xffffffffu, rc = 0;
+      unsigned long long rw = 0;
+      FOR_BLOCKS({
+        const Prio p = prio(b, val[b], w);
+        if (prio_prefix_eq(p, pre, field, shift, width)) {
+          const unsigned int dg = prio_digit(p, field, shift, width);
+          if (dg != rd) {
+            if (rc) { atomicAdd(&s_hw[rd], rw); atomicAdd(&s_hc[rd], rc); }
+            rd = dg; rw = 0; rc = 0;
+          }
+          rw += (unsigned long long)w;
+          rc += 1;
+        }
+      })
+      if (rc) { atomicAdd(&s_hw[rd], rw); atomicAdd(&s_hc[rd], rc); }
     }
     __syncthreads();
-    if (tid == 0) {
-      long long run = s_base;
-      int found = -1;
-      for (int dg = 255; dg >= 0; --dg) {
-        if (s_hc[dg] == 0) continue;
-        if (run + (long long)s_hw[dg] > capacity) { found = dg; break; }
-        run += (long long)s_hw[dg];
+    if (warp == 0) {
+      // find the first bin (from the top) where the running weight exceeds the capacity:
+      // each lane owns 64 consecutive bins, lane 0 the highest
+      const int nbins = 1 << width;
+      const int per = kRouteBins / 32;
+      const int hi = nbins - 1 - lane * per;  // this lane scans hi, hi-1, ..., hi-per+1
+      unsigned long long mine = 0;
+      for (int q = 0; q < per; ++q) {
+        const int dg = hi - q;
+        if (dg >= 0) mine += s_hw[dg];
       }
-      s_base = run;
-      if (found < 0) {
-        s_flag = 1;  // every candidate fits (only possible on pass 0: everything is selected)
+      unsigned long long inc = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const long long base0 = s_base;
+      const bool crosses = base0 + (long long)inc > capacity;
+      const unsigned bal = __ballot_sync(0xffffffffu, crosses);
+      const unsigned long long group_total = __shfl_sync(0xffffffffu, inc, 31);
+      if (bal == 0) {
+        if (lane == 0) { s_flag = 1; s_base = base0 + (long long)group_total; }
       } else {
-        if (pass < 8) s_prefix.a |= (unsigned long long)found << (56 - 8 * pass);
-        else if (pass < 16) s_prefix.b |= (unsigned long long)found << (56 - 8 * (pass - 8));
-        else s_prefix.c |= (unsigned int)found << (24 - 8 * (pass - 16));
-        s_flag = (s_hc[found] == 1) ? 2 : 0;  // unique candidate -> it is the boundary block
+        const int owner = __ffs(bal) - 1;
+        if (lane == owner) {
+          long long run = base0 + (long long)(inc - mine);
+          int found = -1;
+          for (int q = 0; q < per; ++q) {
+            const int dg = hi - q;
+            if (dg < 0) break;
+            if (s_hc[dg] == 0) continue;
+            if (run + (long long)s_hw[dg] > capacity) { found = dg; break; }
+            run += (long long)s_hw[dg];
+          }
+          s_base = run;
+          if (field == 0) s_prefix.a |= (unsigned long long)found << shift;
+          else if (field == 1) s_prefix.b |= (unsigned long long)found << shift;
+          else s_prefix.c |= (unsigned int)found << shift;
+          s_flag = (s_hc[found] == 1) ? 2 : 0;  // unique candidate -> it is the boundary block
+        }
       }
     }
     __syncthreads();
-    npass = pass + 1;
+    last_field = field; last_shift = shift; last_width = width;
     if (s_flag == 1) { all_fit = true; break; }
     if (s_flag == 2) break;
   }
@@ -388,23 +467,18 @@ __global__ void __launch_bounds__(1024)
   long long remaining = capacity - s_base;
   __syncthreads();
   if (!all_fit) {
-    if (tid == 0) s_red[0] = bound;
-    __syncthreads();
     const Prio pre = s_prefix;
-    for (int b = tid; b < nb; b += blockDim.x) {
-      const long long w = weight(b);
-      const Prio p = prio(b, w);
-      if (prio_prefix_eq(p, pre, npass)) s_red[0] = p;  // exactly one writer
-    }
+    // "all digits up to and including the last pass agree" == prefix test of a virtual next pass
+    FOR_BLOCKS({
+      const Prio p = prio(b, val[b], w);
+      if (prio_prefix_eq(p, pre, last_field, last_shift, 0)) s_red[0] = p;  // exactly one writer
+    })
     __syncthreads();
     bound = s_red[0];
   }
   __syncthreads();
   // ---- mask of the prefix -------------------------------------------------------------------------
-  for (int b = tid; b < nb; b += blockDim.x) {
-    const long long w = weight(b);
-    mask[b] = all_fit ? 1 : (prio_gt(prio(b, w), bound) ? 1 : 0);
-  }
+  FOR_BLOCKS({ mask[b] = all_fit ? 1 : (prio_gt(prio(b, val[b], w), bound) ? 1 : 0); })
   // ---- phase 2: fillRemainder tail ------------------------------------------------------------------
   if (!all_fit && overshoot == SVGEAR_FILL_REMAINDER) {
     Prio cur = bound;
@@ -412,15 +486,14 @@ __global__ void __launch_bounds__(1024)
       Prio best;
       best.a = 0; best.b = 0; best.c = 0;
       long long bw = 0;
-      bool have = false;
-      for (int b = tid; b < nb; b += blockDim.x) {
-        const long long w = weight(b);
-        if (w > remaining) continue;
-        const Prio p = prio(b, w);
-        if (prio_gt(cur, p) && (!have || prio_gt(p, best))) { best = p; bw = w; have = true; }
-      }
-      // block arg-max (an all-zero Prio is below every real key because ord64 sets the top bit
-      // for non-negative values and c = ~b is never 0 for b < 2^32-1)
+      FOR_BLOCKS({
+        if (w <= remaining) {
+          const Prio p = prio(b, val[b], w);
+          if (prio_gt(cur, p) && prio_gt(p, best)) { best = p; bw = w; }
+        }
+      })
+      // block arg-max (an all-zero Prio is below every real key: ord64 sets the top bit for
+      // non-negative values)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         Prio q;
@@ -434,7 +507,7 @@ __global__ void __launch_bounds__(1024)
       if (lane == 0) { s_red[warp] = best; s_redw[warp] = bw; }
       __syncthreads();
       if (warp == 0) {
-        const int nw = blockDim.x >> 5;
+        const int nw = nthr >> 5;
         Prio q = s_red[lane < nw ? lane : 0];
         long long qw = s_redw[lane < nw ? lane : 0];
 #pragma unroll
@@ -464,12 +537,11 @@ __global__ void __launch_bounds__(1024)
   long long ent = 0;
   double bestv = -INFINITY;
   int besti = 0x7fffffff;
-  for (int b = tid; b < nb; b += blockDim.x) {
-    const long long w = weight(b);
+  FOR_BLOCKS({
     const double v = val[b];
     if (mask[b]) { sum_sel += v; ent += w; }
     if (w <= capacity && v > bestv) { bestv = v; besti = b; }
-  }
+  })
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     sum_sel += __shfl_xor_sync(0xffffffffu, sum_sel, o);
@@ -478,31 +550,38 @@ __global__ void __launch_bounds__(1024)
     int oi = __shfl_xor_sync(0xffffffffu, besti, o);
     if (ov > bestv || (ov == bestv && oi < besti)) { bestv = ov; besti = oi; }
   }
-  if (lane == 0) { s_redd[warp] = sum_sel; s_redw[warp] = ent; s_red[warp].a = (unsigned long long)__double_as_longlong(bestv); s_red[warp].c = (unsigned int)besti; }
+  if (lane == 0) {
+    s_redd[warp] = sum_sel;
+    s_redw[warp] = ent;
+    s_red[warp].a = (unsigned long long)__double_as_longlong(bestv);
+    s_red[warp].c = (unsigned int)besti;
+  }
   __syncthreads();
   if (tid == 0) {
-    const int nw = blockDim.x >> 5;
+    const int nw = nthr >> 5;
     double s = 0.0;
     long long e = 0;
     double bv = -INFINITY;
     int bx = 0x7fffffff;
-    for (int w = 0; w < nw; ++w) {
-      s += s_redd[w];
-      e += s_redw[w];
-      double ov = __longlong_as_double((long long)s_red[w].a);
-      int oi = (int)s_red[w].c;
+    for (int w2 = 0; w2 < nw; ++w2) {
+      s += s_redd[w2];
+      e += s_redw[w2];
+      double ov = __longlong_as_double((long long)s_red[w2].a);
+      int oi = (int)s_red[w2].c;
       if (ov > bv || (ov == bv && oi < bx)) { bv = ov; bx = oi; }
     }
     int swap = (fallback && bx != 0x7fffffff && bv > s) ? 1 : 0;
     s_flag = swap;
     s_base = swap ? (long long)bx : -1;
-    if (entries_all) entries_all[h] = swap ? weight(bx) : e;
+    if (entries_all)
+      entries_all[h] = swap ? (long long)qs[bx / c_k] * (long long)s_ks[bx % c_k] : e;
   }
   __syncthreads();
   if (s_flag) {
     const int keep = (int)s_base;
-    for (int b = tid; b < nb; b += blockDim.x) mask[b] = (b == keep) ? 1 : 0;
+    for (int b = tid; b < nb; b += nthr) mask[b] = (b == keep) ? 1 : 0;
   }
+#undef FOR_BLOCKS
 }
 
 int launch_route(int bh, int c_q, int c_k, const double* val, const int32_t* q_sizes,

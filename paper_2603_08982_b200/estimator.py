@@ -46,7 +46,7 @@ class BlockErrorTable:
         return self.error_sum * torch.exp(2.0 * self.stabilizers.double()).unsqueeze(-1)
 
 
-def _run(q_model: ClusterModel, k_model: ClusterModel, k, v, mode):
+def _run(q_model: ClusterModel, k_model: ClusterModel, k, v, mode, fp32_check=False):
     kp, was_2d = as_tokens(k, "k", check_finite=False)
     bh, n_k, d = kp.shape
     vp = None
@@ -69,7 +69,8 @@ def _run(q_model: ClusterModel, k_model: ClusterModel, k, v, mode):
     shape = _lib.Shape(bh, max(n_q, c_q), n_k, d, c_q, c_k)
     ws = workspace(_lib.workspace_bytes(shape), dev)
     rc = _lib.lib().svgear_error_table(
-        C.byref(shape), _lib.EST_VALUE_AWARE if mode == "valueAware" else _lib.EST_PLAIN,
+        C.byref(shape), _lib.EXEC_FP32_CHECK if fp32_check else _lib.EXEC_BF16_TENSOR,
+        _lib.EST_VALUE_AWARE if mode == "valueAware" else _lib.EST_PLAIN,
         qc.data_ptr(), kc.data_ptr(), vc.data_ptr() if vc is not None else None, kp.data_ptr(),
         vp.data_ptr() if vp is not None else None, qs.data_ptr(), ks.data_ptr(), ko.data_ptr(),
         err.data_ptr(), stab.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr())
@@ -80,12 +81,12 @@ def _run(q_model: ClusterModel, k_model: ClusterModel, k, v, mode):
                            mode=mode, flops=c_q * n_k * per_key)
 
 
-def estimate_errors_streaming(q_model, k_model, k, v, *, tile_size: int = 64):
+def estimate_errors_streaming(q_model, k_model, k, v, *, tile_size: int = 64, fp32_check=False):
     """Value-aware table (estimator.py:187-253).  `k`, `v` cluster-contiguous for k_model.  The
     result does not depend on the tile size (the kernel streams 32-key tiles)."""
     if tile_size < 1:
         raise ValueError(f"tile_size must be >= 1, got {tile_size}")
-    return _run(q_model, k_model, k, v, "valueAware")
+    return _run(q_model, k_model, k, v, "valueAware", fp32_check)
 
 
 def estimate_errors_value_aware(q_model, k_model, k, v):
