@@ -161,6 +161,9 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(B_QFULL));
     }
+    uint32_t xo[8 / RPI];  // ((chunk & 7) ^ (row & 7)) << 4 for the 8/RPI row phases of this lane
+#pragma unroll
+    for (int j = 0; j < 8 / RPI; ++j) xo[j] = (uint32_t)(((chunk & 7) ^ ((j * RPI + sub) & 7)) << 4);
     int cur0 = 0, cur1 = 0;  // cursors into the selection list for slots lane and lane+32
     const int last_key = max(total_keys - 1, 0);
     for (int t = 0; t < T; ++t) {
@@ -182,13 +185,14 @@ __global__ void __launch_bounds__(NTHREADS, 2)
         r_lo = (t - n_exact) * BN + lane;
         r_hi = r_lo + 32;
       }
-      const uint32_t dst = sbuf + (uint32_t)st * L::kTileBytes;
-#pragma unroll 4
+      // lane-constant parts of the swizzled destination: the XOR pattern repeats every 8 rows
+      const uint32_t dst = sbuf + (uint32_t)st * L::kTileBytes + (uint32_t)((chunk >> 3) * (BN * 128)) +
+                           (uint32_t)(sub * 128);
+      const char* src = reinterpret_cast<const char*>(base) + chunk * 16;
+#pragma unroll
       for (int r0 = 0; r0 < BN; r0 += RPI) {
-        const int r = r0 + sub;
-        const int srow = __shfl_sync(0xffffffffu, (r & 32) ? r_hi : r_lo, r & 31);
-        cp_async16(dst + (uint32_t)((chunk >> 3) * (BN * 128)) + swz(r, chunk & 7),
-                   base + (size_t)srow * D + chunk * 8);
+        const int srow = __shfl_sync(0xffffffffu, r0 < 32 ? r_lo : r_hi, (r0 & 31) + sub);
+        cp_async16(dst + (uint32_t)(r0 * 128) + xo[(r0 / RPI) % (8 / RPI)], src + (size_t)srow * (D * 2));
       }
       cp_async_commit();
       cp_async_wait_all();

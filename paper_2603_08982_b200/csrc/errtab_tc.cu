@@ -34,7 +34,8 @@ struct ESmem {
   static constexpr int kTile = EM * D * 2;        // one [128 x d] bf16 tile
   static constexpr int kA = 0;                    // qh, ql
   static constexpr int kB = kA + 2 * kTile;       // 2 stages x (dh, dl)
-  static constexpr int kBars = kB + 4 * kTile;
+  static constexpr int kStat = kB + 4 * kTile;     // 2 stages x 128 keys x float4
+  static constexpr int kBars = kStat + 2 * ECH * 16;
   static constexpr size_t bytes() { return 1024 + kBars + 256; }
 };
 
@@ -151,6 +152,8 @@ __global__ void __launch_bounds__(ETHREADS, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sA = sbase + L::kA, sB = sbase + L::kB, bars = sbase + L::kBars;
+  const uint32_t sStat = sbase + L::kStat;
+  const float4* stat_smem = reinterpret_cast<const float4*>(smem + L::kStat);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kBars + 192);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto bar = [&](int i) -> uint32_t { return bars + 8u * (uint32_t)i; };
@@ -190,9 +193,10 @@ __global__ void __launch_bounds__(ETHREADS, 1)
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) mbar_arrive(bar(EB_AFULL));
-    int u = 0;
+    int u = 0, guses[2] = {0, 0};
     for (int j = j_lo; j < j_hi; ++j) {
       const int nj = ksz[j], o = kof[j];
+      const int g = (j - j_lo) & 1;
       for (int s0 = 0; s0 < nj; s0 += ECH, ++u) {
         const int st = u & 1;
         if (u >= 2) mbar_wait(bar(EB_BEMPTY + st), ((u >> 1) + 1) & 1);
@@ -207,6 +211,12 @@ __global__ void __launch_bounds__(ETHREADS, 1)
                        src + (size_t)row * D + chunk * 8);
           }
         }
+        // per-key scalars of this chunk go to the stat buffer of epilogue group g, which must have
+        // finished its previous chunk (same barrier the MMA issuer waits on)
+        if (guses[g] >= 1) mbar_wait(bar(EB_ACCEMPTY + g), (guses[g] - 1) & 1);
+        ++guses[g];
+        for (int r = lane; r < nn; r += 32)
+          cp_async16(sStat + (uint32_t)((g * ECH + r) * 16), kstat + (size_t)h * n_k + min(o + s0 + r, n_k - 1));
         cp_async_commit();
         cp_async_wait_all();
         fence_proxy_async();
@@ -256,13 +266,19 @@ __global__ void __launch_bounds__(ETHREADS, 1)
     const uint32_t tcol = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(g * 128);
     const float mr = live ? mref[(size_t)h * c_q + i] : 0.f;
     const double nq = live ? (double)q_sizes[(size_t)h * c_q + i] : 0.0;
-    const float4* ks = kstat + (size_t)h * n_k;
-    int uses = 0;
-    for (int j = j_lo + g; j < j_hi; j += 2) {
-      const int nj = ksz[j], o = kof[j];
+    int uses = 0, u = 0;  // u = global chunk counter (selects the stage the producer used)
+    for (int j = j_lo; j < j_hi; ++j) {
+      const int nj = ksz[j];
+      if (((j - j_lo) & 1) != g) {  // the other group's cluster: just advance the chunk counter
+        u += (nj + ECH - 1) / ECH;
+        continue;
+      }
+      const size_t e = ((size_t)h * c_q + (live ? i : 0)) * c_k + j;
+      const float sb = sbar[e];  // issued early; consumed after the chunks
       float M = 0.f, em = 1.f, em2 = 1.f, acc = 0.f;
-      for (int s0 = 0; s0 < nj; s0 += ECH, ++uses) {
+      for (int s0 = 0; s0 < nj; s0 += ECH, ++uses, ++u) {
         const int valid = min(ECH, nj - s0);
+        const float4* ks = stat_smem + g * ECH;
         mbar_wait(bar(EB_ACCFULL + g), uses & 1);
         tc_fence_after();
         for (int c0 = 0; c0 < valid; c0 += 16) {
@@ -272,7 +288,7 @@ __global__ void __launch_bounds__(ETHREADS, 1)
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             if (c0 + q < valid) {
-              const float4 st4 = __ldg(ks + o + s0 + c0 + q);
+              const float4 st4 = ks[c0 + q];
               const float gg = __uint_as_float(a[q]) * scale;
               if (gg > M) {
                 const float r = __expf(M - gg);
@@ -290,8 +306,7 @@ __global__ void __launch_bounds__(ETHREADS, 1)
         mbar_arrive(bar(EB_ACCEMPTY + g));
       }
       if (live) {
-        const size_t e = ((size_t)h * c_q + i) * c_k + j;
-        const double lift = 2.0 * ((double)sbar[e] - (double)mr + (double)M);
+        const double lift = 2.0 * ((double)sb - (double)mr + (double)M);
         err[e] = nq * ((double)fmaxf(acc, 0.f) * exp(lift));
       }
     }

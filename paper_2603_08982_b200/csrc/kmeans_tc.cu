@@ -23,7 +23,7 @@ namespace svg {
 using namespace tc;
 
 namespace {
-constexpr int kPieces = 3;
+constexpr int kPieces = 2;
 constexpr int KM = 256;     // tokens per CTA
 constexpr int KN = 128;     // centroids per N tile
 constexpr int KSTAGES = 4;  // centroid-piece pipeline depth
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(KTHREADS, 1)
     if (tid == 0) changed[h] = 0;
   }
   if (tid == 0) {
-    mbar_init(bar(KB_AFULL), 1);
+    mbar_init(bar(KB_AFULL), 256);
     for (int s = 0; s < KSTAGES; ++s) {
       mbar_init(bar(KB_BFULL + s), 1);
       mbar_init(bar(KB_BEMPTY + s), 1);
@@ -124,15 +124,6 @@ __global__ void __launch_bounds__(KTHREADS, 1)
     // =========================== producer ========================================================
     constexpr int CPR = D / 8, RPI = 32 / CPR;
     const int sub = lane / CPR, chunk = lane % CPR;
-    const bf16* xsrc = x + (size_t)h * n * D;
-    for (int r0 = 0; r0 < KM; r0 += RPI) {
-      const int r = r0 + sub;                 // row within the CTA: M tile r/128, row r%128
-      const int row = min(tok0 + r, n - 1);
-      const int mt = r >> 7, rr = r & 127;
-      cp_async16(sA + (uint32_t)(mt * (128 * D * 2) + (chunk >> 3) * (128 * 128)) + swz(rr, chunk & 7),
-                 xsrc + (size_t)row * D + chunk * 8);
-    }
-    cp_async_commit();  // group 0 = A
     for (int u = 0; u < U; ++u) {
       const int st = u % KSTAGES;
       if (u >= KSTAGES) mbar_wait(bar(KB_BEMPTY + st), ((u / KSTAGES) - 1) & 1);
@@ -145,22 +136,20 @@ __global__ void __launch_bounds__(KTHREADS, 1)
         cp_async16(dst + (uint32_t)((chunk >> 3) * (KN * 128)) + swz(r, chunk & 7),
                    bsrc + (size_t)r * D + chunk * 8);
       }
-      cp_async_commit();  // group u+1
-      // keep KSTAGES-2 groups in flight; group u-1 has landed after this wait
+      cp_async_commit();  // group u
+      // keep KSTAGES-2 groups in flight; unit u-2 has landed after this wait
       asm volatile("cp.async.wait_group %0;" ::"n"(KSTAGES - 2) : "memory");
-      if (u >= 1) {
+      if (u >= 2) {
         fence_proxy_async();
         __syncwarp();
-        if (lane == 0) mbar_arrive(u == 1 ? bar(KB_AFULL) : bar(KB_BFULL + (u - 2) % KSTAGES));
+        if (lane == 0) mbar_arrive(bar(KB_BFULL + (u - 2) % KSTAGES));
       }
     }
     cp_async_wait_all();
     fence_proxy_async();
     __syncwarp();
-    if (lane == 0) {
-      if (U == 1) mbar_arrive(bar(KB_AFULL));
+    if (lane == 0)
       for (int u = max(U - 2, 0); u < U; ++u) mbar_arrive(bar(KB_BFULL + u % KSTAGES));
-    }
   } else if (warp == 9) {
     // =========================== MMA issuer ======================================================
     if (lane == 0) {
@@ -192,6 +181,24 @@ __global__ void __launch_bounds__(KTHREADS, 1)
     __syncwarp();
   } else {
     // =========================== epilogue: distances + running arg-min ===========================
+    {
+      // the 8 epilogue warps first stage the token tile (A operand): warp w loads rows 32w..32w+31
+      constexpr int CPR = D / 8, RPI = 32 / CPR;
+      const int sub = lane / CPR, chunk = lane % CPR;
+      const bf16* xsrc = x + (size_t)h * n * D;
+#pragma unroll 4
+      for (int r0 = 0; r0 < 32; r0 += RPI) {
+        const int r = warp * 32 + r0 + sub;   // row within the CTA: M tile r/128, row r%128
+        const int row = min(tok0 + r, n - 1);
+        const int mt = r >> 7, rr = r & 127;
+        cp_async16(sA + (uint32_t)(mt * (128 * D * 2) + (chunk >> 3) * (128 * 128)) + swz(rr, chunk & 7),
+                   xsrc + (size_t)row * D + chunk * 8);
+      }
+      cp_async_commit();
+      cp_async_wait_all();
+      fence_proxy_async();
+      mbar_arrive(bar(KB_AFULL));
+    }
     const int m = warp >> 2;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const int t = tok0 + m * 128 + (warp & 3) * 32 + lane;
