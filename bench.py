@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--sigma", type=float, default=0.1)
+    ap.add_argument("--init", default="device", choices=["device", "strided"])
     return ap.parse_args()
 
 
@@ -209,7 +210,7 @@ def run_ours(args):
     q, k, v = make_heads(torch, lo, hi, S, d, cq, ck, args.sigma, dev)
     shape = _lib.Shape(max(hl, 1), S, S, d, cq, ck)
     ws = torch.empty(_lib.workspace_bytes(shape), dtype=torch.uint8, device=dev)
-    kw = dict(init="strided", kmeans_iters=args.kmeans_iters, check_fp32=args.fp32_check,
+    kw = dict(init=args.init, kmeans_iters=args.kmeans_iters, check_fp32=args.fp32_check,
               workspace_buffer=ws)
 
     def layer(qq, kk, vv, aux=False):
@@ -308,7 +309,8 @@ def run_ours(args):
             "dtype": "f32" if args.fp32_check else "bf16", "data": "synthetic",
             "config": {"workload": args.workload, "heads": H, "seq_len": S, "head_dim": d, "c_q": cq,
                        "c_k": ck, "rho": args.rho, "kmeans_max_iters": args.kmeans_iters,
-                       "kmeans_iters_run": iters, "kmeans_init": "strided tokens (device)",
+                       "kmeans_iters_run": iters, "kmeans_init": {"device": "k-means++ on a strided 8x subsample, on device (svgear_kmeans_seed)",
+                                       "strided": "strided tokens"}[args.init],
                        "inputs": f"per-head blob mixture sigma={args.sigma}, generated on device",
                        "executor": "fp32-check" if args.fp32_check else "bf16-tcgen05",
                        "density_achieved": density, "parallelism": f"head-parallel x{world}",
@@ -331,7 +333,7 @@ def run_ours(args):
 def stage_times(torch, P, _lib, q, k, v, cq, ck, args, reps):
     """Run the layer through the STAGED C-ABI entry points (same kernels as svgear_forward) with
     CUDA events between stages.  Returns ({stage: ms}, attention algorithmic FLOPs, density, iters)."""
-    from paper_2603_08982_b200.clustering import ClusterModel, run_lloyd, strided_start
+    from paper_2603_08982_b200.clustering import ClusterModel, device_start, run_lloyd, strided_start
     from paper_2603_08982_b200 import router as R
 
     qb, kb, vb = q[0], k[0], v[0]
@@ -344,8 +346,13 @@ def stage_times(torch, P, _lib, q, k, v, cq, ck, args, reps):
         marks[0][1].record()
         def mark(name):
             e = ev(); e.record(); marks.append((name, e))
-        rq = run_lloyd(qb, strided_start(qb, cq), args.kmeans_iters); mark("kmeans_q")
-        rk = run_lloyd(kb, strided_start(kb, ck), args.kmeans_iters); mark("kmeans_k")
+        if args.init == "device":
+            qi, ki = device_start(qb, cq, 0), device_start(kb, ck, 0x9E37)
+        else:
+            qi, ki = strided_start(qb, cq), strided_start(kb, ck)
+        mark("kmeans_seed")
+        rq = run_lloyd(qb, qi, args.kmeans_iters); mark("kmeans_q")
+        rk = run_lloyd(kb, ki, args.kmeans_iters); mark("kmeans_k")
         qm = ClusterModel(cq, rq["assign"], rq["centroids"], rq["sizes"], rq["perm"], rq["offsets"])
         km = ClusterModel(ck, rk["assign"], rk["centroids"], rk["sizes"], rk["perm"], rk["offsets"])
         qp, kp, vp = P.permute_rows(qb, qm), P.permute_rows(kb, km), P.permute_rows(vb, km); mark("permute")

@@ -110,6 +110,15 @@ int svgear_kmeans(int32_t exec_mode, int32_t bh, int32_t n, int32_t d, int32_t c
                   int32_t* sizes, int32_t* offsets, float* centroids, int32_t* iters,
                   double* inertia, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Device-side start centres for svgear_kmeans when the caller has none: k-means++ D^2 sampling
+ * (the reference's seeding rule, clustering.py:65-84) over a strided subsample of
+ * min(n, oversample*c) tokens with a counter-based hash RNG keyed by (seed, instance).  This is
+ * NOT the reference's numpy draw (the Python shim reproduces that one on the host for parity);
+ * it is deterministic and costs O(c * oversample * c * d) per instance.
+ *   centroids [bh][c][d] f32 (out)                                                              */
+int svgear_kmeans_seed(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
+                       int32_t oversample, uint32_t seed, float* centroids, void* stream);
+
 /* out[b][i][:] = x[b][perm[b][i]][:]   — clustering.permute_rows (clustering.py:210-212). */
 int svgear_permute_rows(int32_t bh, int32_t n, int32_t d, const void* x, const int32_t* perm,
                         void* out, void* stream);

@@ -11,7 +11,7 @@ from ._tensors import ShapeError
 from .analysis import Prepared, build_error_table, prepare
 from .attention import (AttentionResult, FlopCounters, compensation_flops, exact_block_flops,
                         sparse_attend)
-from .clustering import (ClusterModel, cluster_means, inverse_permute_rows, kmeans, kmeans_pp_init,
+from .clustering import (ClusterModel, cluster_means, device_start, inverse_permute_rows, kmeans, kmeans_pp_init,
                          permute_rows, segment_means, strided_start)
 from .estimator import (BlockErrorTable, estimate_errors, estimate_errors_streaming,
                         estimate_errors_value_aware)

@@ -68,6 +68,18 @@ def strided_start(tokens, k):
     return tokens.index_select(-2, idx).float().contiguous()
 
 
+def device_start(tokens, k, seed=0, oversample=8):
+    """Device-side k-means++ start on a strided subsample (svgear_kmeans_seed).  Deterministic, but
+    NOT the reference's numpy draw — use `seeded_start` / init="reference" for parity runs."""
+    x = tokens if tokens.ndim == 3 else tokens.unsqueeze(0)
+    bh, n, d = x.shape
+    out = torch.empty((bh, k, d), dtype=torch.float32, device=x.device)
+    rc = _lib.lib().svgear_kmeans_seed(bh, n, d, k, x.data_ptr(), int(oversample), int(seed) & 0xFFFFFFFF,
+                                       out.data_ptr(), stream_ptr())
+    _lib.check("svgear_kmeans_seed", rc)
+    return out if tokens.ndim == 3 else out[0]
+
+
 def _pad_centers(tok_f32, centers, k):
     """Grow a centre set to k rows by farthest-token selection (clustering.py:87-101)."""
     centers = torch.as_tensor(centers, dtype=torch.float32, device=tok_f32.device)

@@ -125,6 +125,16 @@ int svgear_kmeans(int32_t exec_mode, int32_t bh, int32_t n, int32_t d, int32_t c
                        offsets, centroids, iters, inertia, sc, (cudaStream_t)stream);
 }
 
+int svgear_kmeans_seed(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
+                       int32_t oversample, uint32_t seed, float* centroids, void* stream) {
+  if (!x || !centroids) return SVGEAR_EINVAL;
+  if (oversample < 1) return SVGEAR_EINVAL;
+  if (bh < 1 || n < 1 || (d != 64 && d != 128) || c < 1 || c > n || c > kMaxClusters)
+    return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  return launch_seed_pp(bh, n, d, c, (const bf16*)x, oversample, seed, centroids, (cudaStream_t)stream);
+}
+
 int svgear_permute_rows(int32_t bh, int32_t n, int32_t d, const void* x, const int32_t* perm,
                         void* out, void* stream) {
   if (!x || !perm || !out) return SVGEAR_EINVAL;

@@ -107,6 +107,8 @@ int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, con
                   int max_iters, int32_t* assign, int32_t* perm, int32_t* sizes, int32_t* offsets,
                   float* centroids, int32_t* iters, double* inertia, KmeansScratch& sc,
                   cudaStream_t st);
+int launch_seed_pp(int bh, int n, int d, int c, const bf16* x, int oversample, uint32_t seed, float* cent,
+                   cudaStream_t st);
 int launch_gather_rows(int bh, int n, int d, const bf16* x, const int32_t* perm, bf16* out,
                        cudaStream_t st);
 int launch_segment_means(int bh, int n, int d, int c, const bf16* xp, const int32_t* sizes,

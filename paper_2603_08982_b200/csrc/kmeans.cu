@@ -10,6 +10,8 @@
 // have converged set done[h] and every later kernel returns immediately for them.  No
 // floating-point atomics anywhere: counts use integer atomics, means/inertia use fixed-order
 // reductions, so results are deterministic run to run.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace svg {
@@ -547,6 +549,144 @@ int launch_segment_means(int bh, int n, int d, int c, const bf16* xp, const int3
   else
     cluster_mean_kernel<64><<<dim3(c, bh), 128, 0, st>>>(xp, nullptr, n, c, sizes, offsets, means,
                                                         norms, nullptr);
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
+}  // namespace svg
+
+// ------------------------------------------------------------------------------------------------
+// Device-side seeding: k-means++ (D^2 sampling, clustering.py:65-84) run on a strided SUBSAMPLE of
+// m = min(n, oversample*c) tokens with a counter-based hash RNG.  It is NOT the reference's draw
+// (that needs numpy's generator over all n tokens, host side); it is the start used when the
+// caller supplies no centres and asks for a device-side start.  One CTA per instance; the
+// running min-distance array lives in shared memory; deterministic.
+// ------------------------------------------------------------------------------------------------
+namespace svg {
+
+__device__ __forceinline__ uint32_t hash_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t x = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u ^ (c + 0x165667B1u) * 0xC2B2AE3Du;
+  x ^= x >> 16; x *= 0x7FEB352Du; x ^= x >> 15; x *= 0x846CA68Bu; x ^= x >> 16;
+  return x;
+}
+
+// A thread-block CLUSTER of 8 CTAs serves one instance: every thread keeps ONE subsample token in
+// registers for the whole run; per step each CTA reloads the newest centre (256 B), updates its
+// min-distances, block-scans them, and the 8 partial sums are exchanged through distributed shared
+// memory (2 cluster barriers per step).
+constexpr int kSeedCtas = 8;
+constexpr int kSeedThreads = 512;  // one subsample token per thread, held in registers
+
+template <int D>
+__global__ void __cluster_dims__(kSeedCtas, 1, 1) __launch_bounds__(kSeedThreads)
+    seed_pp_kernel(const bf16* __restrict__ x, int n, int c, int m, uint32_t seed, float* __restrict__ cent) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int h = blockIdx.x / kSeedCtas;
+  __shared__ float s_c[D];          // newest centre
+  __shared__ double s_warp[32];  // (16 warps used)
+  __shared__ double s_part[kSeedCtas];  // partial sums of all CTAs (written through DSMEM)
+  __shared__ int s_pick;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bf16* xh = x + (size_t)h * n * D;
+  float* ch = cent + (size_t)h * c * D;
+  auto sample_row = [&](int s) -> size_t { return (size_t)(((long long)s * n) / m); };
+  const int per = (m + kSeedCtas - 1) / kSeedCtas;  // samples per CTA, <= kSeedThreads
+  const int s_mine = rank * per + tid;
+  const bool have = tid < per && s_mine < m;
+  uint32_t row[D / 2];
+  if (have) {
+    const uint4* src = reinterpret_cast<const uint4*>(xh + sample_row(s_mine) * D);
+#pragma unroll
+    for (int q = 0; q < D / 8; ++q) {
+      const uint4 u = __ldg(src + q);
+      row[4 * q] = u.x; row[4 * q + 1] = u.y; row[4 * q + 2] = u.z; row[4 * q + 3] = u.w;
+    }
+  }
+  float mind = INFINITY;
+  int pick = (int)(hash_u32(seed, (uint32_t)h, 0u) % (uint32_t)m);
+  for (int step = 0; step < c; ++step) {
+    if (tid < D) {
+      const float v = __bfloat162float(xh[sample_row(pick) * D + tid]);
+      s_c[tid] = v;
+      if (rank == 0) ch[(size_t)step * D + tid] = v;
+    }
+    __syncthreads();
+    if (step == c - 1) break;
+    double mine = 0.0;
+    if (have) {
+      float d2 = 0.f;
+#pragma unroll
+      for (int q = 0; q < D / 4; ++q) {
+        const float4 cc = *reinterpret_cast<const float4*>(&s_c[4 * q]);
+        const uint32_t u0 = row[2 * q], u1 = row[2 * q + 1];
+        float df = __uint_as_float(u0 << 16) - cc.x; d2 = fmaf(df, df, d2);
+        df = __uint_as_float(u0 & 0xffff0000u) - cc.y; d2 = fmaf(df, df, d2);
+        df = __uint_as_float(u1 << 16) - cc.z; d2 = fmaf(df, df, d2);
+        df = __uint_as_float(u1 & 0xffff0000u) - cc.w; d2 = fmaf(df, df, d2);
+      }
+      mind = fminf(mind, d2);
+      mine = (double)mind;
+    }
+    // block scan of the per-thread values (fixed order)
+    double inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      double w = lane < kSeedThreads / 32 ? s_warp[lane] : 0.0, wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      s_warp[lane] = wi - w;
+      const double tot = __shfl_sync(0xffffffffu, wi, 31);
+      if (lane < kSeedCtas) {  // lane r publishes this CTA's total into CTA r
+        double* remote = cluster.map_shared_rank(s_part, lane);
+        remote[rank] = tot;
+      }
+      if (lane == 0) s_pick = -1;
+    }
+    cluster.sync();
+    double total = 0.0, before = 0.0;
+#pragma unroll
+    for (int r = 0; r < kSeedCtas; ++r) {
+      if (r == rank) before = total;
+      total += s_part[r];
+    }
+    if (total > 0.0) {
+      const double u = ((double)hash_u32(seed, (uint32_t)h, (uint32_t)step + 1u) + 0.5) * (1.0 / 4294967296.0);
+      const double target = u * total;
+      const double lo = before + s_warp[warp] + inc - mine;
+      if (have && target >= lo && target < lo + mine) {  // at most one thread in the cluster
+#pragma unroll
+        for (int r = 0; r < kSeedCtas; ++r) *cluster.map_shared_rank(&s_pick, r) = s_mine;
+      }
+    }
+    cluster.sync();
+    pick = s_pick;
+    if (pick < 0) pick = (int)(hash_u32(seed, (uint32_t)h, (uint32_t)step + 77777u) % (uint32_t)m);
+  }
+  cluster.sync();  // no CTA may exit while peers can still write its shared memory
+}
+
+int launch_seed_pp(int bh, int n, int d, int c, const bf16* x, int oversample, uint32_t seed, float* cent,
+                   cudaStream_t st) {
+  long long mm = (long long)oversample * c;
+  if (mm > n) mm = n;
+  if (mm > kSeedThreads * kSeedCtas) mm = kSeedThreads * kSeedCtas;  // subsample capacity
+  const int m = (int)mm;
+  if (m < c) return SVGEAR_EUNSUPPORTED;  // more clusters than the subsample can hold
+  if (d == 128)
+    seed_pp_kernel<128><<<bh * kSeedCtas, kSeedThreads, 0, st>>>(x, n, c, m, seed, cent);
+  else
+    seed_pp_kernel<64><<<bh * kSeedCtas, kSeedThreads, 0, st>>>(x, n, c, m, seed, cent);
   SVG_LAUNCH_OK();
   return SVGEAR_OK;
 }

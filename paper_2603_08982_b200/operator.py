@@ -16,7 +16,7 @@ import torch
 from . import _lib
 from ._tensors import ShapeError, require_cuda, stream_ptr, workspace
 from .analysis import side_seeds
-from .clustering import seeded_start, strided_start
+from .clustering import device_start, seeded_start, strided_start
 from .router import _OVERSHOOT, entry_capacity
 
 _EST = {"valueAware": _lib.EST_VALUE_AWARE, "plain": _lib.EST_PLAIN}
@@ -47,7 +47,8 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
     budget : exact-compute budget = global density rho in [0, 1]
              (router.DensityBudget.global_density, router.py:59-61).
     init   : "reference" -> k-means++ centres drawn with the reference's RNG recipe from `seed`
-             (host side, slow at scale); "strided" -> evenly strided tokens (device side);
+             (host side, slow at scale); "device" -> k-means++ on a strided subsample, on the
+             device (svgear_kmeans_seed); "strided" -> evenly strided tokens;
              ignored for a side whose q_init / k_init ([.., C, d] float32 centres) is given.
     check_fp32 : run the executor in fp32 on CUDA cores and return a float32 output.
     Returns (out, mask) — out [.., S, d] in ORIGINAL token order, mask [.., C_q, C_k] bool
@@ -78,7 +79,7 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
         raise ValueError(f"unknown estimator mode {estimator!r}")
     if overshoot not in _OVERSHOOT:
         raise ValueError(f"unknown overshoot policy {overshoot!r}")
-    if init not in ("reference", "strided"):
+    if init not in ("reference", "strided", "device"):
         raise ValueError(f"unknown init {init!r}")
     dev = require_cuda()
     lead = tuple(q.shape[:-2])
@@ -91,6 +92,8 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
     if q_init is None or k_init is None:
         if init == "reference":
             rq, rk = reference_init(qb, kb, c_q, c_k, seed)
+        elif init == "device":
+            rq, rk = device_start(qb, c_q, seed), device_start(kb, c_k, seed + 0x9E37)
         else:
             rq, rk = strided_start(qb, c_q), strided_start(kb, c_k)
         q_init = rq if q_init is None else q_init

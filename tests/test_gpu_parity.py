@@ -424,3 +424,25 @@ class TestPropertiesAtScale:
             assert bool((aux["mask_entries"] <= cap).all())
             assert bool((aux["mask_entries"] >= 0.97 * cap).all())
             assert bool(torch.isfinite(out.float()).all())
+
+
+class TestDeviceSeeding:
+    def test_device_start_is_deterministic_and_picks_tokens(self):
+        rng = np.random.default_rng(3)
+        x = dev(O.round_to_bf16(rng.normal(size=(2, 3000, 64))))
+        a = P.device_start(x, 40, seed=5)
+        b = P.device_start(x, 40, seed=5)
+        assert torch.equal(a, b) and a.shape == (2, 40, 64)
+        # every centre is one of the tokens, and D^2 sampling does not repeat a token
+        for h in range(2):
+            d2 = torch.cdist(a[h].double(), x[h].double())
+            assert float(d2.min(dim=1).values.max()) == 0.0
+            assert len({int(i) for i in d2.argmin(dim=1)}) == 40
+        assert not torch.equal(a, P.device_start(x, 40, seed=6))
+
+    def test_device_start_converges_fast_on_blobs(self):
+        q, k, v = (O.round_to_bf16(t) for t in O.blob_instance(4096, 4096, 64, 32, 64, 0.1, 0))
+        out, mask, aux = P.svg_ear_attention(dev(q), dev(k), dev(v), 32, 64, 0.25, init="device",
+                                             return_aux=True)
+        assert int(aux["q_iters"]) <= 8 and int(aux["k_iters"]) <= 8
+        assert bool(torch.isfinite(out.float()).all())

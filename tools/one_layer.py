@@ -14,6 +14,6 @@ H, S, d, cq, ck = bench.WORKLOADS[a.workload]
 H = a.heads or H
 q, k, v = bench.make_heads(torch, 0, H, S, d, cq, ck, 0.1, torch.device("cuda", 0))
 for _ in range(a.calls):
-    out, mask = P.svg_ear_attention(q, k, v, cq, ck, 0.25, init="strided", kmeans_iters=a.kmeans_iters)
+    out, mask = P.svg_ear_attention(q, k, v, cq, ck, 0.25, init="device", kmeans_iters=a.kmeans_iters)
 torch.cuda.synchronize()
 print("ok", float(mask.float().mean()))
