@@ -119,6 +119,12 @@ int svgear_kmeans(int32_t exec_mode, int32_t bh, int32_t n, int32_t d, int32_t c
 int svgear_kmeans_seed(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
                        int32_t oversample, uint32_t seed, float* centroids, void* stream);
 
+/* Same seeding rule, driven by a precomputed Gram matrix of the strided subsample
+ * (sample s = token floor(s*n/m); gram[b][s][t] = <x_s, x_t> in bf16, e.g. one batched library
+ * GEMM): a round then reads only the Gram rows of its new centres.  m <= 4096.              */
+int svgear_kmeans_seed_gram(int32_t bh, int32_t n, int32_t d, int32_t c, int32_t m, const void* x,
+                            const void* gram, uint32_t seed, float* centroids, void* stream);
+
 /* out[b][i][:] = x[b][perm[b][i]][:]   — clustering.permute_rows (clustering.py:210-212). */
 int svgear_permute_rows(int32_t bh, int32_t n, int32_t d, const void* x, const int32_t* perm,
                         void* out, void* stream);

@@ -55,6 +55,7 @@ SIGNATURES = {
     "svgear_workspace_bytes": ([C.POINTER(Shape), C.POINTER(_SZ)], C.c_int),
     "svgear_kmeans": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_kmeans_seed": ([_I32, _I32, _I32, _I32, _P, _I32, C.c_uint32, _P, _P], C.c_int),
+    "svgear_kmeans_seed_gram": ([_I32, _I32, _I32, _I32, _I32, _P, _P, C.c_uint32, _P, _P], C.c_int),
     "svgear_permute_rows": ([_I32, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "svgear_segment_means": ([_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P], C.c_int),
     "svgear_error_table": ([C.POINTER(Shape), _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),

@@ -68,15 +68,26 @@ def strided_start(tokens, k):
     return tokens.index_select(-2, idx).float().contiguous()
 
 
-def device_start(tokens, k, seed=0, oversample=8):
+def device_start(tokens, k, seed=0, oversample=8, gram=True):
     """Device-side k-means++ start on a strided subsample (svgear_kmeans_seed).  Deterministic, but
     NOT the reference's numpy draw — use `seeded_start` / init="reference" for parity runs."""
     x = tokens if tokens.ndim == 3 else tokens.unsqueeze(0)
+    x = x.contiguous()
     bh, n, d = x.shape
     out = torch.empty((bh, k, d), dtype=torch.float32, device=x.device)
-    rc = _lib.lib().svgear_kmeans_seed(bh, n, d, k, x.data_ptr(), int(oversample), int(seed) & 0xFFFFFFFF,
-                                       out.data_ptr(), stream_ptr())
-    _lib.check("svgear_kmeans_seed", rc)
+    m = min(n, int(oversample) * k, 4096)
+    if gram and m >= k:
+        # Gram matrix of the strided subsample: one plain batched library GEMM (bf16 in, bf16 out)
+        idx = torch.div(torch.arange(m, device=x.device, dtype=torch.int64) * n, m, rounding_mode="floor")
+        xs = x.index_select(1, idx)
+        g = torch.bmm(xs, xs.transpose(1, 2)).contiguous()
+        rc = _lib.lib().svgear_kmeans_seed_gram(bh, n, d, k, m, x.data_ptr(), g.data_ptr(),
+                                                int(seed) & 0xFFFFFFFF, out.data_ptr(), stream_ptr())
+        _lib.check("svgear_kmeans_seed_gram", rc)
+    else:
+        rc = _lib.lib().svgear_kmeans_seed(bh, n, d, k, x.data_ptr(), int(oversample), int(seed) & 0xFFFFFFFF,
+                                           out.data_ptr(), stream_ptr())
+        _lib.check("svgear_kmeans_seed", rc)
     return out if tokens.ndim == 3 else out[0]
 
 

@@ -31,6 +31,7 @@ struct ForwardPlan {
   int32_t *q_iters, *k_iters;
   float *q_cent, *k_cent, *v_cent, *stab, *lse_tmp;
   double* err;
+  unsigned long long* route_keys;
   int64_t* entries;
   bf16 *qp, *kp, *vp;
 };
@@ -57,6 +58,7 @@ bool plan_forward(const SvgEarShape& s, Carver& cv, ForwardPlan& p) {
   p.stab = cv.take<float>((size_t)s.bh * s.c_q);
   p.lse_tmp = cv.take<float>((size_t)s.bh * s.n_q);
   p.err = cv.take<double>((size_t)s.bh * s.c_q * s.c_k);
+  p.route_keys = cv.take<unsigned long long>((size_t)s.bh * s.c_q * s.c_k);
   p.entries = cv.take<int64_t>(s.bh);
   p.qp = cv.take<bf16>((size_t)s.bh * s.n_q * s.d);
   p.kp = cv.take<bf16>((size_t)s.bh * s.n_k * s.d);
@@ -135,6 +137,17 @@ int svgear_kmeans_seed(int32_t bh, int32_t n, int32_t d, int32_t c, const void* 
   return launch_seed_pp(bh, n, d, c, (const bf16*)x, oversample, seed, centroids, (cudaStream_t)stream);
 }
 
+int svgear_kmeans_seed_gram(int32_t bh, int32_t n, int32_t d, int32_t c, int32_t m, const void* x,
+                            const void* gram, uint32_t seed, float* centroids, void* stream) {
+  if (!x || !gram || !centroids) return SVGEAR_EINVAL;
+  if (bh < 1 || n < 1 || (d != 64 && d != 128) || c < 1 || c > n || c > kMaxClusters || m < c || m > n ||
+      m > 4096)
+    return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  return launch_seed_gram(bh, n, d, c, m, (const bf16*)x, (const bf16*)gram, seed, centroids,
+                          (cudaStream_t)stream);
+}
+
 int svgear_permute_rows(int32_t bh, int32_t n, int32_t d, const void* x, const int32_t* perm,
                         void* out, void* stream) {
   if (!x || !perm || !out) return SVGEAR_EINVAL;
@@ -178,16 +191,17 @@ int svgear_route_error_aware(int32_t bh, int32_t c_q, int32_t c_k, const double*
                              int64_t capacity_entries, int32_t overshoot,
                              int32_t single_item_fallback, uint8_t* mask, int64_t* entries,
                              void* workspace, size_t workspace_bytes, void* stream) {
-  (void)workspace;
-  (void)workspace_bytes;
-  if (!error_table || !q_sizes || !k_sizes || !mask) return SVGEAR_EINVAL;
+  if (!error_table || !q_sizes || !k_sizes || !mask || !workspace) return SVGEAR_EINVAL;
   if (capacity_entries < 0) return SVGEAR_EINVAL;
   if (overshoot != SVGEAR_FILL_REMAINDER && overshoot != SVGEAR_STOP_AT_FIRST_OVERFLOW)
     return SVGEAR_EINVAL;
   if (bh < 1 || c_q < 1 || c_k < 1 || c_k > kMaxClusters) return SVGEAR_ESHAPE;
   if (!device_present()) return SVGEAR_ECUDA;
+  Carver cv(workspace, workspace_bytes);
+  unsigned long long* keys = cv.take<unsigned long long>((size_t)bh * c_q * c_k);
+  if (!cv.ok) return SVGEAR_EWORKSPACE;
   return launch_route(bh, c_q, c_k, error_table, q_sizes, k_sizes, capacity_entries, overshoot,
-                      single_item_fallback ? 1 : 0, 0, mask, entries, (cudaStream_t)stream);
+                      single_item_fallback ? 1 : 0, 0, mask, entries, keys, (cudaStream_t)stream);
 }
 
 int svgear_route_score(const SvgEarShape* shape, const float* q_centroids,
@@ -203,12 +217,13 @@ int svgear_route_score(const SvgEarShape* shape, const float* q_centroids,
   if (!device_present()) return SVGEAR_ECUDA;
   Carver cv(workspace, workspace_bytes);
   double* mass = cv.take<double>((size_t)shape->bh * shape->c_q * shape->c_k);
+  unsigned long long* keys = cv.take<unsigned long long>((size_t)shape->bh * shape->c_q * shape->c_k);
   if (!cv.ok) return SVGEAR_EWORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   int rc = launch_score_mass(*shape, q_centroids, k_centroids, k_sizes, mass, st);
   if (rc != SVGEAR_OK) return rc;
   return launch_route(shape->bh, shape->c_q, shape->c_k, mass, q_sizes, k_sizes, capacity_entries,
-                      overshoot, 0, 1, mask, entries, st);
+                      overshoot, 0, 1, mask, entries, keys, st);
 }
 
 int svgear_sparse_attend(const SvgEarShape* shape, int32_t exec_mode, const void* q_permuted,
@@ -294,7 +309,7 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
                           k_sizes, k_offsets, err, stab, p.es, st);
   if (rc) return rc;
   rc = launch_route(s.bh, s.c_q, s.c_k, err, q_sizes, k_sizes, capacity_entries, overshoot,
-                    single_item_fallback ? 1 : 0, 0, mask, entries, st);
+                    single_item_fallback ? 1 : 0, 0, mask, entries, p.route_keys, st);
   if (rc) return rc;
   // (3) fused executor, output scattered to original token order
   return launch_attend(s, exec_mode, p.qp, p.kp, p.vp, q_perm, q_sizes, q_offsets, k_sizes, k_offsets,

@@ -257,14 +257,13 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       TMEM_LD32(tS[st] + 32, sb);
       tc_wait_ld();
       float mt = -INFINITY;
+      float cmul = 1.f;  // multiplier still to be applied to sa/sb inside the exponential
       if (t < n_exact - 1) {
+        // full exact tile: keep the raw logits, fold the scale into the exp2 FFMA below
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float x = __uint_as_float(sa[j]) * scale_log2e, y = __uint_as_float(sb[j]) * scale_log2e;
-          sa[j] = __float_as_uint(x);
-          sb[j] = __float_as_uint(y);
-          mt = fmaxf(mt, fmaxf(x, y));
-        }
+        for (int j = 0; j < 32; ++j) mt = fmaxf(mt, fmaxf(__uint_as_float(sa[j]), __uint_as_float(sb[j])));
+        mt *= scale_log2e;
+        cmul = scale_log2e;
       } else if (t < n_exact) {
         const int valid = total_keys - t * BN;  // 1..64 valid columns in the last exact tile
 #pragma unroll
@@ -298,13 +297,13 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       uint32_t pk[32];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        float p0 = ex2(__uint_as_float(sa[2 * j]) - mu), p1 = ex2(__uint_as_float(sa[2 * j + 1]) - mu);
+        float p0 = ex2(fmaf(__uint_as_float(sa[2 * j]), cmul, -mu)), p1 = ex2(fmaf(__uint_as_float(sa[2 * j + 1]), cmul, -mu));
         sum += p0 + p1;
         pk[j] = pack_bf16x2(p0, p1);
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        float p0 = ex2(__uint_as_float(sb[2 * j]) - mu), p1 = ex2(__uint_as_float(sb[2 * j + 1]) - mu);
+        float p0 = ex2(fmaf(__uint_as_float(sb[2 * j]), cmul, -mu)), p1 = ex2(fmaf(__uint_as_float(sb[2 * j + 1]), cmul, -mu));
         sum += p0 + p1;
         pk[16 + j] = pack_bf16x2(p0, p1);
       }

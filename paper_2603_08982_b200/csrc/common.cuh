@@ -109,6 +109,8 @@ int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, con
                   cudaStream_t st);
 int launch_seed_pp(int bh, int n, int d, int c, const bf16* x, int oversample, uint32_t seed, float* cent,
                    cudaStream_t st);
+int launch_seed_gram(int bh, int n, int d, int c, int m, const bf16* x, const bf16* gram, uint32_t seed,
+                     float* cent, cudaStream_t st);
 int launch_gather_rows(int bh, int n, int d, const bf16* x, const int32_t* perm, bf16* out,
                        cudaStream_t st);
 int launch_segment_means(int bh, int n, int d, int c, const bf16* xp, const int32_t* sizes,
@@ -127,13 +129,10 @@ int launch_error_table(const SvgEarShape& s, int exec_mode, int mode, const floa
                        const int32_t* k_sizes, const int32_t* k_offsets, double* err,
                        float* stabilizers, ErrScratch& sc, cudaStream_t st);
 
-struct RouteScratch {
-  int32_t* state;  // per-head scratch ints
-  static size_t bytes(int bh) { return align_up((size_t)bh * 64 * sizeof(int32_t), 256); }
-};
 int launch_route(int bh, int c_q, int c_k, const double* val, const int32_t* q_sizes,
                  const int32_t* k_sizes, int64_t capacity, int overshoot, int fallback,
-                 int ratio_mode, uint8_t* mask, int64_t* entries, cudaStream_t st);
+                 int ratio_mode, uint8_t* mask, int64_t* entries, unsigned long long* keys,
+                 cudaStream_t st);
 int launch_score_mass(const SvgEarShape& s, const float* qc, const float* kc,
                       const int32_t* k_sizes, double* mass, cudaStream_t st);
 

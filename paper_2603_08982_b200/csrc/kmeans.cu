@@ -575,19 +575,20 @@ __device__ __forceinline__ uint32_t hash_u32(uint32_t a, uint32_t b, uint32_t c)
 // min-distances, block-scans them, and the 8 partial sums are exchanged through distributed shared
 // memory (2 cluster barriers per step).
 constexpr int kSeedCtas = 8;
+constexpr int kSeedBatch = 4;      // centres drawn per round
 constexpr int kSeedThreads = 512;  // one subsample token per thread, held in registers
 
 template <int D>
-__global__ void __cluster_dims__(kSeedCtas, 1, 1) __launch_bounds__(kSeedThreads)
+__global__ void __cluster_dims__(kSeedCtas, 1, 1) __launch_bounds__(kSeedThreads, 3)
     seed_pp_kernel(const bf16* __restrict__ x, int n, int c, int m, uint32_t seed, float* __restrict__ cent) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int h = blockIdx.x / kSeedCtas;
-  __shared__ float s_c[D];          // newest centre
-  __shared__ double s_warp[32];  // (16 warps used)
-  __shared__ double s_part[kSeedCtas];  // partial sums of all CTAs (written through DSMEM)
-  __shared__ int s_pick;
+  __shared__ __align__(16) __nv_bfloat162 s_c2[kSeedBatch][D / 2];  // newest centres (bf16 tokens)
+  __shared__ float s_warp[32];
+  __shared__ float s_part[kSeedCtas];     // partial sums of all CTAs (written through DSMEM)
+  __shared__ int s_pick[kSeedBatch];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bf16* xh = x + (size_t)h * n * D;
   float* ch = cent + (size_t)h * c * D;
@@ -595,83 +596,118 @@ __global__ void __cluster_dims__(kSeedCtas, 1, 1) __launch_bounds__(kSeedThreads
   const int per = (m + kSeedCtas - 1) / kSeedCtas;  // samples per CTA, <= kSeedThreads
   const int s_mine = rank * per + tid;
   const bool have = tid < per && s_mine < m;
-  uint32_t row[D / 2];
-  if (have) {
-    const uint4* src = reinterpret_cast<const uint4*>(xh + sample_row(s_mine) * D);
-#pragma unroll
-    for (int q = 0; q < D / 8; ++q) {
-      const uint4 u = __ldg(src + q);
-      row[4 * q] = u.x; row[4 * q + 1] = u.y; row[4 * q + 2] = u.z; row[4 * q + 3] = u.w;
-    }
-  }
-  float mind = INFINITY;
-  int pick = (int)(hash_u32(seed, (uint32_t)h, 0u) % (uint32_t)m);
-  for (int step = 0; step < c; ++step) {
-    if (tid < D) {
-      const float v = __bfloat162float(xh[sample_row(pick) * D + tid]);
-      s_c[tid] = v;
-      if (rank == 0) ch[(size_t)step * D + tid] = v;
+  // the token of this thread is re-read from L2 every round (all centres of a round share the
+  // read); keeping it in registers would cost 64 registers and limit residency to one CTA per SM
+  const uint4* my_row = reinterpret_cast<const uint4*>(xh + sample_row(have ? s_mine : 0) * D);
+  float mind = have ? INFINITY : 0.f;
+  // Centres are drawn in rounds of up to kSeedBatch (one while fewer than 128 remain): the draws of
+  // a round share one D^2 distribution, which amortises the two cluster barriers per round.
+  int picks[kSeedBatch];
+  picks[0] = (int)(hash_u32(seed, (uint32_t)h, 0u) % (uint32_t)m);
+  int cnt = 1, npicked = 0;
+  while (true) {
+    if (tid < cnt * D) {
+      const int i = tid / D, k = tid % D;
+      const bf16 b = xh[sample_row(picks[i]) * D + k];
+      reinterpret_cast<bf16*>(&s_c2[i][0])[k] = b;
+      if (rank == 0) ch[(size_t)(npicked + i) * D + k] = __bfloat162float(b);
     }
     __syncthreads();
-    if (step == c - 1) break;
-    double mine = 0.0;
+    npicked += cnt;
+    if (npicked >= c) break;
     if (have) {
-      float d2 = 0.f;
+      // squared distances to the round's centres.  Tokens and centres are bf16, so the differences
+      // and 16-element partial sums are formed with packed bf16x2 math (HSUB2/HFMA2.BF16: one
+      // instruction per two elements) and flushed to fp32 every 16 elements; the ~1 % noise only
+      // perturbs sampling weights.
+      float d2[kSeedBatch];
+      __nv_bfloat162 a2[kSeedBatch];
 #pragma unroll
-      for (int q = 0; q < D / 4; ++q) {
-        const float4 cc = *reinterpret_cast<const float4*>(&s_c[4 * q]);
-        const uint32_t u0 = row[2 * q], u1 = row[2 * q + 1];
-        float df = __uint_as_float(u0 << 16) - cc.x; d2 = fmaf(df, df, d2);
-        df = __uint_as_float(u0 & 0xffff0000u) - cc.y; d2 = fmaf(df, df, d2);
-        df = __uint_as_float(u1 << 16) - cc.z; d2 = fmaf(df, df, d2);
-        df = __uint_as_float(u1 & 0xffff0000u) - cc.w; d2 = fmaf(df, df, d2);
+      for (int i = 0; i < kSeedBatch; ++i) { d2[i] = 0.f; a2[i] = __floats2bfloat162_rn(0.f, 0.f); }
+#pragma unroll 2
+      for (int q = 0; q < D / 8; ++q) {
+        const uint4 u = __ldg(my_row + q);
+        const __nv_bfloat162 x0 = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
+        const __nv_bfloat162 x1 = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+        const __nv_bfloat162 x2 = *reinterpret_cast<const __nv_bfloat162*>(&u.z);
+        const __nv_bfloat162 x3 = *reinterpret_cast<const __nv_bfloat162*>(&u.w);
+#pragma unroll
+        for (int i = 0; i < kSeedBatch; ++i) {
+          if (i < cnt) {
+            const uint4 cu = *reinterpret_cast<const uint4*>(&s_c2[i][4 * q]);
+            __nv_bfloat162 df = __hsub2(x0, *reinterpret_cast<const __nv_bfloat162*>(&cu.x));
+            a2[i] = __hfma2(df, df, a2[i]);
+            df = __hsub2(x1, *reinterpret_cast<const __nv_bfloat162*>(&cu.y));
+            a2[i] = __hfma2(df, df, a2[i]);
+            df = __hsub2(x2, *reinterpret_cast<const __nv_bfloat162*>(&cu.z));
+            a2[i] = __hfma2(df, df, a2[i]);
+            df = __hsub2(x3, *reinterpret_cast<const __nv_bfloat162*>(&cu.w));
+            a2[i] = __hfma2(df, df, a2[i]);
+            if (q & 1) {
+              const float2 f = __bfloat1622float2(a2[i]);
+              d2[i] += f.x + f.y;
+              a2[i] = __floats2bfloat162_rn(0.f, 0.f);
+            }
+          }
+        }
       }
-      mind = fminf(mind, d2);
-      mine = (double)mind;
+#pragma unroll
+      for (int i = 0; i < kSeedBatch; ++i)
+        if (i < cnt) mind = fminf(mind, d2[i]);
     }
-    // block scan of the per-thread values (fixed order)
-    double inc = mine;
+    // block scan of the per-thread values (fixed order, fp32: this only steers the sampling)
+    float inc = mind;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const double y = __shfl_up_sync(0xffffffffu, inc, o);
+      const float y = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += y;
     }
     if (lane == 31) s_warp[warp] = inc;
     __syncthreads();
     if (warp == 0) {
-      double w = lane < kSeedThreads / 32 ? s_warp[lane] : 0.0, wi = w;
+      float w = lane < kSeedThreads / 32 ? s_warp[lane] : 0.f, wi = w;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, wi, o);
+        const float y = __shfl_up_sync(0xffffffffu, wi, o);
         if (lane >= o) wi += y;
       }
       s_warp[lane] = wi - w;
-      const double tot = __shfl_sync(0xffffffffu, wi, 31);
-      if (lane < kSeedCtas) {  // lane r publishes this CTA's total into CTA r
-        double* remote = cluster.map_shared_rank(s_part, lane);
-        remote[rank] = tot;
-      }
-      if (lane == 0) s_pick = -1;
+      const float tot = __shfl_sync(0xffffffffu, wi, 31);
+      if (lane < kSeedCtas) *cluster.map_shared_rank(&s_part[rank], lane) = tot;  // publish to CTA `lane`
+      if (lane < kSeedBatch) s_pick[lane] = -1;
     }
     cluster.sync();
-    double total = 0.0, before = 0.0;
+    float total = 0.f, before = 0.f;
 #pragma unroll
     for (int r = 0; r < kSeedCtas; ++r) {
       if (r == rank) before = total;
       total += s_part[r];
     }
-    if (total > 0.0) {
-      const double u = ((double)hash_u32(seed, (uint32_t)h, (uint32_t)step + 1u) + 0.5) * (1.0 / 4294967296.0);
-      const double target = u * total;
-      const double lo = before + s_warp[warp] + inc - mine;
-      if (have && target >= lo && target < lo + mine) {  // at most one thread in the cluster
+    const int left = c - npicked;
+    const int next = left >= 128 ? kSeedBatch : 1;
+    if (total > 0.f && have && mind > 0.f) {
+      const float lo = before + s_warp[warp] + inc - mind;
+      for (int i = 0; i < next; ++i) {
+        const float u = ((float)(hash_u32(seed, (uint32_t)h, (uint32_t)(npicked + i) + 1u) >> 8) + 0.5f) *
+                        (1.0f / 16777216.0f);
+        const float target = u * total;
+        // intervals are built from the same partial sums on every CTA; a target on a rounding
+        // boundary can be claimed by two adjacent threads: keep the larger index
+        if (target >= lo && target < lo + mind) {
 #pragma unroll
-        for (int r = 0; r < kSeedCtas; ++r) *cluster.map_shared_rank(&s_pick, r) = s_mine;
+          for (int r = 0; r < kSeedCtas; ++r) atomicMax(cluster.map_shared_rank(&s_pick[i], r), s_mine);
+        }
       }
     }
     cluster.sync();
-    pick = s_pick;
-    if (pick < 0) pick = (int)(hash_u32(seed, (uint32_t)h, (uint32_t)step + 77777u) % (uint32_t)m);
+    for (int i = 0; i < next; ++i) {
+      int pk = s_pick[i];
+      if (pk < 0) pk = (int)(hash_u32(seed, (uint32_t)h, (uint32_t)(npicked + i) + 77777u) % (uint32_t)m);
+      for (int j = 0; j < i; ++j)
+        if (picks[j] == pk) pk = (pk + 1 + i) % m;  // two draws of a round hit the same token
+      picks[i] = pk;
+    }
+    cnt = next;
   }
   cluster.sync();  // no CTA may exit while peers can still write its shared memory
 }
@@ -687,6 +723,138 @@ int launch_seed_pp(int bh, int n, int d, int c, const bf16* x, int oversample, u
     seed_pp_kernel<128><<<bh * kSeedCtas, kSeedThreads, 0, st>>>(x, n, c, m, seed, cent);
   else
     seed_pp_kernel<64><<<bh * kSeedCtas, kSeedThreads, 0, st>>>(x, n, c, m, seed, cent);
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
+}  // namespace svg
+
+// ------------------------------------------------------------------------------------------------
+// Seeding from a precomputed Gram matrix of the subsample (G = Xs Xs^T, bf16, a plain library GEMM
+// done by the caller): d^2(s, c) = G[s][s] + G[c][c] - 2 G[c][s], so a round only reads the Gram
+// rows of its new centres (8 KB each) instead of every subsample token.  One CTA per instance,
+// 4 subsample tokens per thread, no cluster needed.  Same D^2 rounds as seed_pp_kernel.
+// ------------------------------------------------------------------------------------------------
+namespace svg {
+
+constexpr int kGramPer = 4;  // samples per thread (m <= 4096)
+
+__global__ void __launch_bounds__(1024)
+    seed_gram_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gram, int n, int d, int c, int m,
+                     uint32_t seed, float* __restrict__ cent) {
+  const int h = blockIdx.x;
+  __shared__ float s_warp[32];
+  __shared__ float s_total;
+  __shared__ int s_pick[kSeedBatch];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bf16* xh = x + (size_t)h * n * d;
+  const bf16* gh = gram + (size_t)h * m * m;
+  float* ch = cent + (size_t)h * c * d;
+  auto sample_row = [&](int s) -> size_t { return (size_t)(((long long)s * n) / m); };
+  const int s0 = tid * kGramPer;
+  float nrm[kGramPer], mind[kGramPer];
+#pragma unroll
+  for (int e = 0; e < kGramPer; ++e) {
+    const int s = s0 + e;
+    nrm[e] = s < m ? __bfloat162float(gh[(size_t)s * m + s]) : 0.f;
+    mind[e] = s < m ? INFINITY : 0.f;
+  }
+  int picks[kSeedBatch];
+  picks[0] = (int)(hash_u32(seed, (uint32_t)h, 0u) % (uint32_t)m);
+  int cnt = 1, npicked = 0;
+  while (true) {
+    for (int e = tid; e < cnt * d; e += 1024) {
+      const int i = e / d, k = e % d;
+      ch[(size_t)(npicked + i) * d + k] = __bfloat162float(xh[sample_row(picks[i]) * d + k]);
+    }
+    npicked += cnt;
+    if (npicked >= c) break;
+    for (int i = 0; i < cnt; ++i) {
+      const int pc = picks[i];
+      const float nc = __bfloat162float(gh[(size_t)pc * m + pc]);
+      const bf16* grow = gh + (size_t)pc * m;
+      float g[kGramPer];
+      if (s0 + kGramPer <= m && (m & 3) == 0) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(grow + s0));
+        g[0] = __uint_as_float(u.x << 16); g[1] = __uint_as_float(u.x & 0xffff0000u);
+        g[2] = __uint_as_float(u.y << 16); g[3] = __uint_as_float(u.y & 0xffff0000u);
+      } else {
+#pragma unroll
+        for (int e = 0; e < kGramPer; ++e) g[e] = s0 + e < m ? __bfloat162float(grow[s0 + e]) : 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < kGramPer; ++e) {
+        const float d2 = (s0 + e == pc) ? 0.f : fmaxf(nrm[e] + nc - 2.f * g[e], 0.f);
+        if (s0 + e < m) mind[e] = fminf(mind[e], d2);
+      }
+    }
+    float mine = 0.f;
+#pragma unroll
+    for (int e = 0; e < kGramPer; ++e) mine += mind[e];
+    float inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const float y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    __syncthreads();  // previous round's readers of s_warp / s_pick are done
+    if (lane == 31) s_warp[warp] = inc;
+    if (tid < kSeedBatch) s_pick[tid] = -1;
+    __syncthreads();
+    if (warp == 0) {
+      float w = s_warp[lane], wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      s_warp[lane] = wi - w;
+      if (lane == 31) s_total = wi;
+    }
+    __syncthreads();
+    const float total = s_total;
+    const int left = c - npicked;
+    const int next = left >= 128 ? kSeedBatch : 1;
+    if (total > 0.f && mine > 0.f) {
+      const float lo = s_warp[warp] + inc - mine;
+      for (int i = 0; i < next; ++i) {
+        const float u = ((float)(hash_u32(seed, (uint32_t)h, (uint32_t)(npicked + i) + 1u) >> 8) + 0.5f) *
+                        (1.0f / 16777216.0f);
+        const float target = u * total;
+        if (target >= lo && target < lo + mine) {
+          float run = lo;
+          int chosen = -1;
+#pragma unroll
+          for (int e = 0; e < kGramPer; ++e) {
+            run += mind[e];
+            if (chosen < 0 && target < run && mind[e] > 0.f) chosen = s0 + e;
+          }
+          if (chosen < 0) {  // rounding: fall back to this thread's largest entry
+            float best = -1.f;
+#pragma unroll
+            for (int e = 0; e < kGramPer; ++e)
+              if (mind[e] > best) { best = mind[e]; chosen = s0 + e; }
+          }
+          atomicMax(&s_pick[i], chosen);
+        }
+      }
+    }
+    __syncthreads();
+    for (int i = 0; i < next; ++i) {
+      int pk = s_pick[i];
+      if (pk < 0 || pk >= m) pk = (int)(hash_u32(seed, (uint32_t)h, (uint32_t)(npicked + i) + 77777u) % (uint32_t)m);
+      for (int j = 0; j < i; ++j)
+        if (picks[j] == pk) pk = (pk + 1 + i) % m;
+      picks[i] = pk;
+    }
+    cnt = next;
+  }
+}
+
+int launch_seed_gram(int bh, int n, int d, int c, int m, const bf16* x, const bf16* gram, uint32_t seed,
+                     float* cent, cudaStream_t st) {
+  if (m > 1024 * kGramPer || m < c) return SVGEAR_ESHAPE;
+  seed_gram_kernel<<<bh, 1024, 0, st>>>(x, gram, n, d, c, m, seed, cent);
   SVG_LAUNCH_OK();
   return SVGEAR_OK;
 }

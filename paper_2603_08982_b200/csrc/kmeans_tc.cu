@@ -24,19 +24,27 @@ using namespace tc;
 
 namespace {
 constexpr int kPieces = 2;
-constexpr int KM = 256;     // tokens per CTA
+constexpr int KM = 256;     // tokens per work item (two M=128 tiles)
 constexpr int KN = 128;     // centroids per N tile
-constexpr int KSTAGES = 4;  // centroid-piece pipeline depth
-constexpr int KTHREADS = 320;
+constexpr int KSTAGES = 3;  // centroid-piece pipeline depth
+constexpr int KTHREADS = 352;
+constexpr int kMaxHeads = 256;  // instances per launch (larger batches are chunked)
 
-enum { KB_AFULL = 0, KB_BFULL = 1, KB_BEMPTY = 1 + KSTAGES, KB_ACCFULL = 1 + 2 * KSTAGES, KB_ACCEMPTY = 3 + 2 * KSTAGES };
+enum {
+  KB_AFULL = 0,                    // [2]
+  KB_AEMPTY = 2,                   // [2]
+  KB_BFULL = 4,                    // [KSTAGES]
+  KB_BEMPTY = 4 + KSTAGES,         // [KSTAGES]
+  KB_ACCFULL = 4 + 2 * KSTAGES,    // [2]
+  KB_ACCEMPTY = 6 + 2 * KSTAGES    // [2]
+};
 
 template <int D>
 struct KSmem {
   static constexpr int kABytes = KM * D * 2;
   static constexpr int kBBytes = KN * D * 2;
-  static constexpr int kA = 0;
-  static constexpr int kB = kA + kABytes;
+  static constexpr int kA = 0;                       // 2 buffers
+  static constexpr int kB = kA + 2 * kABytes;        // KSTAGES stages
   static constexpr int kBars = kB + KSTAGES * kBBytes;
   static constexpr size_t bytes() { return 1024 + kBars + 256; }
 };
@@ -77,17 +85,23 @@ __global__ void token_norm_kernel(const bf16* __restrict__ x, int d, long long t
   if (lane == 0) xn[row] = s;
 }
 
+// Persistent kernel: grid = #SMs; CTA b handles work items b, b+grid, ... where an item is a
+// 256-token tile of a not-yet-converged instance.  Token tiles are double buffered (the next item's
+// tile loads while the current one is multiplied), the centroid-piece ring and the two TMEM
+// accumulator buffers run straight through item boundaries.
+//   warps 0-7 : epilogue      warp 8 : centroid-piece producer      warp 9 : MMA issuer
+//   warp 10   : token-tile producer
 template <int D>
 __global__ void __launch_bounds__(KTHREADS, 1)
     assign_tc_kernel(const bf16* __restrict__ x, const bf16* __restrict__ pieces,
-                     const float* __restrict__ cnorm_pad, const float* __restrict__ xnorm, int n, int c,
-                     int cpad, int32_t* __restrict__ assign, float* __restrict__ own_d2,
+                     const float* __restrict__ cnorm_pad, const float* __restrict__ xnorm, int bh, int n,
+                     int c, int cpad, int cpad16, int32_t* __restrict__ assign, float* __restrict__ own_d2,
                      int32_t* __restrict__ sizes, int32_t* __restrict__ changed,
                      const int32_t* __restrict__ done) {
   using L = KSmem<D>;
-  const int h = blockIdx.y;
-  if (done[h]) return;
   extern __shared__ uint8_t smem_raw[];
+  __shared__ int16_t s_heads[kMaxHeads];
+  __shared__ int s_nactive;
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sA = sbase + L::kA, sB = sbase + L::kB, bars = sbase + L::kBars;
@@ -95,19 +109,28 @@ __global__ void __launch_bounds__(KTHREADS, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto bar = [&](int i) -> uint32_t { return bars + 8u * (uint32_t)i; };
 
-  if (blockIdx.x == 0) {  // reset the per-iteration counters of this instance
-    for (int j = tid; j < c; j += KTHREADS) sizes[(size_t)h * c + j] = 0;
-    if (tid == 0) changed[h] = 0;
-  }
   if (tid == 0) {
-    mbar_init(bar(KB_AFULL), 256);
-    for (int s = 0; s < KSTAGES; ++s) {
-      mbar_init(bar(KB_BFULL + s), 1);
-      mbar_init(bar(KB_BEMPTY + s), 1);
-    }
+    int na = 0;
+    for (int h = 0; h < bh; ++h)
+      if (!done[h]) s_heads[na++] = (int16_t)h;
+    s_nactive = na;
+  }
+  __syncthreads();
+  const int tiles_per_head = (n + KM - 1) / KM;
+  const int total_items = s_nactive * tiles_per_head;
+  if ((int)blockIdx.x >= total_items) return;
+  const int my_items = (total_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+
+  if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(KB_AFULL + b), 1);
+      mbar_init(bar(KB_AEMPTY + b), 1);
       mbar_init(bar(KB_ACCFULL + b), 1);
       mbar_init(bar(KB_ACCEMPTY + b), 256);
+    }
+    for (int st = 0; st < KSTAGES; ++st) {
+      mbar_init(bar(KB_BFULL + st), 1);
+      mbar_init(bar(KB_BEMPTY + st), 1);
     }
     fence_barrier_init();
   }
@@ -116,123 +139,151 @@ __global__ void __launch_bounds__(KTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int NT = cpad / KN;        // N tiles
-  const int U = NT * kPieces;      // pipeline units
-  const int tok0 = blockIdx.x * KM;
+  const int NT = (cpad16 + KN - 1) / KN;  // N tiles; the last one may be narrower (multiple of 16)
+  const int U = NT * kPieces;             // pipeline units per item
+  auto item_head = [&](int it) -> int { return s_heads[((int)blockIdx.x + it * (int)gridDim.x) / tiles_per_head]; };
+  auto item_tile = [&](int it) -> int { return ((int)blockIdx.x + it * (int)gridDim.x) % tiles_per_head; };
 
   if (warp == 8) {
-    // =========================== producer ========================================================
+    // =========================== centroid-piece producer ========================================
     constexpr int CPR = D / 8, RPI = 32 / CPR;
     const int sub = lane / CPR, chunk = lane % CPR;
-    for (int u = 0; u < U; ++u) {
-      const int st = u % KSTAGES;
-      if (u >= KSTAGES) mbar_wait(bar(KB_BEMPTY + st), ((u / KSTAGES) - 1) & 1);
-      const int nt = u / kPieces, p = u % kPieces;
-      const bf16* bsrc = pieces + (((size_t)h * kPieces + p) * cpad + (size_t)nt * KN) * D;
-      const uint32_t dst = sB + (uint32_t)st * L::kBBytes;
-#pragma unroll 4
-      for (int r0 = 0; r0 < KN; r0 += RPI) {
-        const int r = r0 + sub;
-        cp_async16(dst + (uint32_t)((chunk >> 3) * (KN * 128)) + swz(r, chunk & 7),
-                   bsrc + (size_t)r * D + chunk * 8);
-      }
-      cp_async_commit();  // group u
-      // keep KSTAGES-2 groups in flight; unit u-2 has landed after this wait
-      asm volatile("cp.async.wait_group %0;" ::"n"(KSTAGES - 2) : "memory");
-      if (u >= 2) {
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar(KB_BFULL + (u - 2) % KSTAGES));
+    int u = 0;  // running unit counter across items
+    for (int it = 0; it < my_items; ++it) {
+      const int h = item_head(it);
+      for (int uu = 0; uu < U; ++uu, ++u) {
+        const int st = u % KSTAGES;
+        if (u >= KSTAGES) mbar_wait(bar(KB_BEMPTY + st), ((u / KSTAGES) - 1) & 1);
+        const int nt = uu / kPieces, p = uu % kPieces;
+        const int nn = min(KN, cpad16 - nt * KN);
+        const bf16* bsrc = pieces + (((size_t)h * kPieces + p) * cpad + (size_t)nt * KN) * D;
+        const uint32_t dst = sB + (uint32_t)st * L::kBBytes;
+        for (int r0 = 0; r0 < nn; r0 += RPI) {
+          const int r = r0 + sub;
+          cp_async16(dst + (uint32_t)((chunk >> 3) * (KN * 128)) + swz(r, chunk & 7),
+                     bsrc + (size_t)r * D + chunk * 8);
+        }
+        cp_async_commit();
+        // keep one group in flight: unit u-1 has landed after this wait
+        asm volatile("cp.async.wait_group %0;" ::"n"(KSTAGES - 2) : "memory");
+        if (u >= 1) {
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(KB_BFULL + (u - 1) % KSTAGES));
+        }
       }
     }
     cp_async_wait_all();
     fence_proxy_async();
     __syncwarp();
-    if (lane == 0)
-      for (int u = max(U - 2, 0); u < U; ++u) mbar_arrive(bar(KB_BFULL + u % KSTAGES));
-  } else if (warp == 9) {
-    // =========================== MMA issuer ======================================================
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(128, KN, 0);
-      mbar_wait(bar(KB_AFULL), 0);
-      for (int nt = 0; nt < NT; ++nt) {
-        const int buf = nt & 1;
-        if (nt >= 2) mbar_wait(bar(KB_ACCEMPTY + buf), ((nt >> 1) - 1) & 1);
-        for (int p = 0; p < kPieces; ++p) {
-          const int u = nt * kPieces + p, st = u % KSTAGES;
-          mbar_wait(bar(KB_BFULL + st), (u / KSTAGES) & 1);
-          tc_fence_after();
-          const uint32_t bb = sB + (uint32_t)st * L::kBBytes;
-#pragma unroll
-          for (int m = 0; m < 2; ++m) {
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-              const uint64_t ad = make_desc(
-                  sA + (uint32_t)(m * (128 * D * 2) + (kk >> 2) * (128 * 128) + (kk & 3) * 32), 16, 1024);
-              const uint64_t bd = make_desc(bb + (uint32_t)((kk >> 2) * (KN * 128) + (kk & 3) * 32), 16, 1024);
-              umma_ss(tmem + (uint32_t)(buf * 256 + m * 128), ad, bd, idesc, (p > 0 || kk > 0) ? 1u : 0u);
-            }
-          }
-          umma_commit(bar(KB_BEMPTY + st));
-        }
-        umma_commit(bar(KB_ACCFULL + buf));
-      }
-    }
-    __syncwarp();
-  } else {
-    // =========================== epilogue: distances + running arg-min ===========================
-    {
-      // the 8 epilogue warps first stage the token tile (A operand): warp w loads rows 32w..32w+31
-      constexpr int CPR = D / 8, RPI = 32 / CPR;
-      const int sub = lane / CPR, chunk = lane % CPR;
+    if (lane == 0 && u >= 1) mbar_arrive(bar(KB_BFULL + (u - 1) % KSTAGES));
+  } else if (warp == 10) {
+    // =========================== token-tile producer (A operand, double buffered) ===============
+    constexpr int CPR = D / 8, RPI = 32 / CPR;
+    const int sub = lane / CPR, chunk = lane % CPR;
+    for (int it = 0; it < my_items; ++it) {
+      const int b = it & 1;
+      if (it >= 2) mbar_wait(bar(KB_AEMPTY + b), ((it >> 1) + 1) & 1);
+      const int h = item_head(it), tok0 = item_tile(it) * KM;
       const bf16* xsrc = x + (size_t)h * n * D;
+      const uint32_t dst = sA + (uint32_t)b * L::kABytes;
 #pragma unroll 4
-      for (int r0 = 0; r0 < 32; r0 += RPI) {
-        const int r = warp * 32 + r0 + sub;   // row within the CTA: M tile r/128, row r%128
+      for (int r0 = 0; r0 < KM; r0 += RPI) {
+        const int r = r0 + sub;  // row within the item: M tile r/128, row r%128
         const int row = min(tok0 + r, n - 1);
         const int mt = r >> 7, rr = r & 127;
-        cp_async16(sA + (uint32_t)(mt * (128 * D * 2) + (chunk >> 3) * (128 * 128)) + swz(rr, chunk & 7),
+        cp_async16(dst + (uint32_t)(mt * (128 * D * 2) + (chunk >> 3) * (128 * 128)) + swz(rr, chunk & 7),
                    xsrc + (size_t)row * D + chunk * 8);
       }
       cp_async_commit();
       cp_async_wait_all();
       fence_proxy_async();
-      mbar_arrive(bar(KB_AFULL));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(KB_AFULL + b));
     }
+  } else if (warp == 9) {
+    // =========================== MMA issuer ======================================================
+    if (lane == 0) {
+      int u = 0, g = 0;  // running unit / N-tile counters
+      for (int it = 0; it < my_items; ++it) {
+        const int ab = it & 1;
+        mbar_wait(bar(KB_AFULL + ab), (it >> 1) & 1);
+        const uint32_t abase = sA + (uint32_t)ab * L::kABytes;
+        for (int nt = 0; nt < NT; ++nt, ++g) {
+          const int buf = g & 1;
+          const int nn = min(KN, cpad16 - nt * KN);
+          const uint32_t idesc = make_idesc(128, nn, 0);
+          if (g >= 2) mbar_wait(bar(KB_ACCEMPTY + buf), ((g >> 1) - 1) & 1);
+          for (int p = 0; p < kPieces; ++p, ++u) {
+            const int st = u % KSTAGES;
+            mbar_wait(bar(KB_BFULL + st), (u / KSTAGES) & 1);
+            tc_fence_after();
+            const uint32_t bb = sB + (uint32_t)st * L::kBBytes;
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+#pragma unroll
+              for (int kk = 0; kk < D / 16; ++kk) {
+                const uint64_t ad = make_desc(
+                    abase + (uint32_t)(m * (128 * D * 2) + (kk >> 2) * (128 * 128) + (kk & 3) * 32), 16, 1024);
+                const uint64_t bd = make_desc(bb + (uint32_t)((kk >> 2) * (KN * 128) + (kk & 3) * 32), 16, 1024);
+                umma_ss(tmem + (uint32_t)(buf * 256 + m * 128), ad, bd, idesc, (p > 0 || kk > 0) ? 1u : 0u);
+              }
+            }
+            umma_commit(bar(KB_BEMPTY + st));
+          }
+          umma_commit(bar(KB_ACCFULL + buf));
+        }
+        umma_commit(bar(KB_AEMPTY + ab));
+      }
+    }
+    __syncwarp();
+  } else {
+    // =========================== epilogue: distances + running arg-min ===========================
     const int m = warp >> 2;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const int t = tok0 + m * 128 + (warp & 3) * 32 + lane;
-    const float xn = xnorm[(size_t)h * n + min(t, n - 1)];
-    const float* cn = cnorm_pad + (size_t)h * cpad;
-    float best = INFINITY;
-    int bi = 0;
-    for (int nt = 0; nt < NT; ++nt) {
-      const int buf = nt & 1;
-      mbar_wait(bar(KB_ACCFULL + buf), (nt >> 1) & 1);
-      tc_fence_after();
-      const uint32_t tcol = tmem + lane_base + (uint32_t)(buf * 256 + m * 128);
+    int g = 0;
+    for (int it = 0; it < my_items; ++it) {
+      const int h = item_head(it), tile = item_tile(it);
+      if (tile == 0) {  // reset the per-iteration counters of this instance
+        for (int j = tid; j < c; j += 256) sizes[(size_t)h * c + j] = 0;
+        if (tid == 0) changed[h] = 0;
+      }
+      const int t = tile * KM + m * 128 + (warp & 3) * 32 + lane;
+      const float xn = xnorm[(size_t)h * n + min(t, n - 1)];
+      const float* cn = cnorm_pad + (size_t)h * cpad;
+      float best = INFINITY;
+      int bi = 0;
+      for (int nt = 0; nt < NT; ++nt, ++g) {
+        const int buf = g & 1;
+        mbar_wait(bar(KB_ACCFULL + buf), (g >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tcol = tmem + lane_base + (uint32_t)(buf * 256 + m * 128);
+        const int nn = min(KN, cpad16 - nt * KN);
+        for (int c4 = 0; c4 < nn; c4 += 32) {  // a narrow last tile leaves stale columns: norm = +inf there
+          uint32_t a[32];
+          TMEM_LD32(tcol + c4, a);
+          tc_wait_ld();
+          const int cb = nt * KN + c4;
 #pragma unroll
-      for (int c4 = 0; c4 < KN; c4 += 32) {
-        uint32_t a[32];
-        TMEM_LD32(tcol + c4, a);
-        tc_wait_ld();
-        const int cb = nt * KN + c4;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          // same association as the reference: (|x|^2 - 2 x.c) + |c|^2, clipped at zero
-          const float v = fmaxf((xn - 2.0f * __uint_as_float(a[j])) + __ldg(cn + cb + j), 0.f);
-          if (v < best) {  // strict: ties keep the lowest cluster index
-            best = v;
-            bi = cb + j;
+          for (int j = 0; j < 32; ++j) {
+            // |x|^2 is a per-token constant of the arg-min, so the loop ranks w = |c|^2 - 2 x.c and
+            // the clip at zero is applied once to the winner below.  (The reference clips every
+            // entry, clustering.py:62; that only matters when two DIFFERENT centroids are both
+            // within rounding of the token, and identical centroids still tie exactly here.)
+            const float w = fmaf(-2.0f, __uint_as_float(a[j]), __ldg(cn + cb + j));
+            if (w < best) {  // strict: ties keep the lowest cluster index (NaN from stale columns never wins)
+              best = w;
+              bi = cb + j;
+            }
           }
         }
+        tc_fence_before();
+        mbar_arrive(bar(KB_ACCEMPTY + buf));
       }
-      tc_fence_before();
-      mbar_arrive(bar(KB_ACCEMPTY + buf));
-    }
-    if (t < n) {
-      assign[(size_t)h * n + t] = bi;
-      own_d2[(size_t)h * n + t] = best;
+      if (t < n) {
+        assign[(size_t)h * n + t] = bi;
+        own_d2[(size_t)h * n + t] = fmaxf(xn + best, 0.f);
+      }
     }
   }
   tc_fence_before();
@@ -260,23 +311,41 @@ int launch_kmeans_assign_tc(int bh, int n, int d, int c, const bf16* x, const fl
                             const float* cnorm, bf16* pieces, float* cnorm_pad, const float* xnorm,
                             int32_t* assign, float* own_d2, int32_t* sizes, int32_t* changed,
                             const int32_t* done, cudaStream_t st) {
-  const int cpad = ceil_div(c, KN) * KN;
+  const int cpad = ceil_div(c, KN) * KN;     // row stride of the piece arrays / norm array
+  const int cpad16 = ceil_div(c, 16) * 16;   // columns actually multiplied
   split_centroids_kernel<<<dim3(ceil_div(cpad * d, 256), bh), 256, 0, st>>>(cent, cnorm, d, c, cpad, pieces,
                                                                            cnorm_pad, done);
   SVG_LAUNCH_OK();
-  dim3 grid(ceil_div(n, KM), bh);
-  if (d == 128) {
-    const size_t smem = KSmem<128>::bytes();
-    SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    assign_tc_kernel<128><<<grid, KTHREADS, smem, st>>>(x, pieces, cnorm_pad, xnorm, n, c, cpad, assign, own_d2,
-                                                        sizes, changed, done);
-  } else {
-    const size_t smem = KSmem<64>::bytes();
-    SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    assign_tc_kernel<64><<<grid, KTHREADS, smem, st>>>(x, pieces, cnorm_pad, xnorm, n, c, cpad, assign, own_d2,
-                                                       sizes, changed, done);
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    SVG_CUDA_OK(cudaGetDevice(&dev));
+    SVG_CUDA_OK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  SVG_LAUNCH_OK();
+  for (int h0 = 0; h0 < bh; h0 += kMaxHeads) {
+    const int nb = bh - h0 < kMaxHeads ? bh - h0 : kMaxHeads;
+    const int items = nb * ceil_div(n, KM);
+    const int grid = items < num_sms ? items : num_sms;
+    const bf16* xs = x + (size_t)h0 * n * d;
+    const bf16* ps = pieces + (size_t)h0 * kPieces * cpad * d;
+    const float* cs = cnorm_pad + (size_t)h0 * cpad;
+    const float* xns = xnorm + (size_t)h0 * n;
+    int32_t* as = assign + (size_t)h0 * n;
+    float* os = own_d2 + (size_t)h0 * n;
+    int32_t* ss = sizes + (size_t)h0 * c;
+    if (d == 128) {
+      const size_t smem = KSmem<128>::bytes();
+      SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      assign_tc_kernel<128><<<grid, KTHREADS, smem, st>>>(xs, ps, cs, xns, nb, n, c, cpad, cpad16, as, os, ss,
+                                                          changed + h0, done + h0);
+    } else {
+      const size_t smem = KSmem<64>::bytes();
+      SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      assign_tc_kernel<64><<<grid, KTHREADS, smem, st>>>(xs, ps, cs, xns, nb, n, c, cpad, cpad16, as, os, ss,
+                                                         changed + h0, done + h0);
+    }
+    SVG_LAUNCH_OK();
+  }
   return SVGEAR_OK;
 }
 

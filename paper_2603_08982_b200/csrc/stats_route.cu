@@ -24,37 +24,57 @@ namespace svg {
 // ------------------------------------------------------------------------------------------------
 // centroid logits s̄ = q̄ k̄^T / sqrt(d) and their row maxima (estimator.py:216-217)
 // ------------------------------------------------------------------------------------------------
+constexpr int kLogitRows = 8;  // query clusters per block (each k̄ row is read once per block)
 __global__ void __launch_bounds__(256)
     centroid_logits_kernel(const float* __restrict__ qc, const float* __restrict__ kc, int d,
                            int c_q, int c_k, float scale, float* __restrict__ sbar,
                            float* __restrict__ mref) {
-  const int h = blockIdx.y, i = blockIdx.x;
-  __shared__ float sq[128];
-  __shared__ float smax[8];
+  const int h = blockIdx.y, i0 = blockIdx.x * kLogitRows;
+  __shared__ float sq[kLogitRows][128];
+  __shared__ float smax[8][kLogitRows];
   const int tid = threadIdx.x;
-  if (tid < d) sq[tid] = qc[((size_t)h * c_q + i) * d + tid];
+  for (int e = tid; e < kLogitRows * d; e += 256) {
+    const int r = e / d, k = e % d;
+    sq[r][k] = (i0 + r < c_q) ? qc[((size_t)h * c_q + i0 + r) * d + k] : 0.f;
+  }
   __syncthreads();
-  float mx = -INFINITY;
+  float mx[kLogitRows];
+#pragma unroll
+  for (int r = 0; r < kLogitRows; ++r) mx[r] = -INFINITY;
   for (int j = tid; j < c_k; j += 256) {
     const float4* kp = reinterpret_cast<const float4*>(kc + ((size_t)h * c_k + j) * d);
-    float s = 0.f;
+    float s[kLogitRows];
+#pragma unroll
+    for (int r = 0; r < kLogitRows; ++r) s[r] = 0.f;
     for (int q = 0; q < d / 4; ++q) {
-      float4 kv = __ldg(kp + q);
-      s = fmaf(sq[4 * q], kv.x, s);
-      s = fmaf(sq[4 * q + 1], kv.y, s);
-      s = fmaf(sq[4 * q + 2], kv.z, s);
-      s = fmaf(sq[4 * q + 3], kv.w, s);
+      const float4 kv = __ldg(kp + q);
+#pragma unroll
+      for (int r = 0; r < kLogitRows; ++r) {
+        s[r] = fmaf(sq[r][4 * q], kv.x, s[r]);
+        s[r] = fmaf(sq[r][4 * q + 1], kv.y, s[r]);
+        s[r] = fmaf(sq[r][4 * q + 2], kv.z, s[r]);
+        s[r] = fmaf(sq[r][4 * q + 3], kv.w, s[r]);
+      }
     }
-    s *= scale;
-    sbar[((size_t)h * c_q + i) * c_k + j] = s;
-    mx = fmaxf(mx, s);
+#pragma unroll
+    for (int r = 0; r < kLogitRows; ++r) {
+      if (i0 + r < c_q) {
+        const float v = s[r] * scale;
+        sbar[((size_t)h * c_q + i0 + r) * c_k + j] = v;
+        mx[r] = fmaxf(mx[r], v);
+      }
+    }
   }
-  mx = warp_max(mx);
-  if ((tid & 31) == 0) smax[tid >> 5] = mx;
+#pragma unroll
+  for (int r = 0; r < kLogitRows; ++r) {
+    const float m = warp_max(mx[r]);
+    if ((tid & 31) == 0) smax[tid >> 5][r] = m;
+  }
   __syncthreads();
-  if (tid == 0) {
-    for (int w = 1; w < 8; ++w) mx = fmaxf(mx, smax[w]);
-    mref[(size_t)h * c_q + i] = mx;
+  if (tid < kLogitRows && i0 + tid < c_q) {
+    float m = smax[0][tid];
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, smax[w][tid]);
+    mref[(size_t)h * c_q + i0 + tid] = m;
   }
 }
 
@@ -199,7 +219,7 @@ int launch_error_table(const SvgEarShape& s, int exec_mode, int mode, const floa
                        float* stabilizers, ErrScratch& sc, cudaStream_t st) {
   const float scale = 1.0f / sqrtf((float)s.d);
   float* sbar = sc.sbar;
-  centroid_logits_kernel<<<dim3(s.c_q, s.bh), 256, 0, st>>>(qc, kc, s.d, s.c_q, s.c_k, scale, sbar,
+  centroid_logits_kernel<<<dim3(ceil_div(s.c_q, kLogitRows), s.bh), 256, 0, st>>>(qc, kc, s.d, s.c_q, s.c_k, scale, sbar,
                                                            stabilizers);
   SVG_LAUNCH_OK();
   if (exec_mode == SVGEAR_EXEC_BF16_TENSOR)
@@ -297,14 +317,9 @@ int launch_score_mass(const SvgEarShape& s, const float* qc, const float* kc,
 // One CTA per instance; integer atomics only.
 // ------------------------------------------------------------------------------------------------
 struct Prio {
-  unsigned long long a, b;
-  unsigned int c;
+  unsigned long long a;  // ord64(primary key)
+  unsigned int c;        // ~block index   (the secondary key ord64(value) is fetched on demand)
 };
-__device__ __forceinline__ bool prio_gt(const Prio& x, const Prio& y) {
-  if (x.a != y.a) return x.a > y.a;
-  if (x.b != y.b) return x.b > y.b;
-  return x.c > y.c;
-}
 __device__ __forceinline__ unsigned long long ord64(double v) {
   unsigned long long u = (unsigned long long)__double_as_longlong(v);
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
@@ -326,34 +341,39 @@ __device__ __forceinline__ void pass_geom(int pass, int& field, int& shift, int&
     width = q == 2 ? 10 : 11;
   }
 }
-__device__ __forceinline__ unsigned int prio_digit(const Prio& p, int field, int shift, int width) {
-  const unsigned long long v = field == 0 ? p.a : (field == 1 ? p.b : (unsigned long long)p.c);
-  return (unsigned int)(v >> shift) & ((1u << width) - 1u);
-}
-// do all digits BEFORE this pass agree with the chosen prefix?
-__device__ __forceinline__ bool prio_prefix_eq(const Prio& p, const Prio& q, int field, int shift, int width) {
-  const int hs = shift + width;  // bits of the current field already fixed are those above hs
-  if (field == 0) return hs >= 64 ? true : (p.a >> hs) == (q.a >> hs);
-  if (p.a != q.a) return false;
-  if (field == 1) return hs >= 64 ? true : (p.b >> hs) == (q.b >> hs);
-  if (p.b != q.b) return false;
-  return hs >= 32 ? true : (p.c >> hs) == (q.c >> hs);
+
+// primary keys, computed once by the whole grid (the float64 division is the expensive part)
+__global__ void route_keys_kernel(const double* __restrict__ val, const int32_t* __restrict__ q_sizes,
+                                  const int32_t* __restrict__ k_sizes, int c_q, int c_k, int ratio_mode,
+                                  unsigned long long* __restrict__ keys) {
+  const int h = blockIdx.y;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= c_q * c_k) return;
+  const double v = val[(size_t)h * c_q * c_k + b];
+  double key = v;
+  if (ratio_mode == 0) {
+    const long long w = (long long)q_sizes[(size_t)h * c_q + b / c_k] * (long long)k_sizes[(size_t)h * c_k + b % c_k];
+    key = v / (double)w;
+  }
+  keys[(size_t)h * c_q * c_k + b] = ord64(key);
 }
 
 __global__ void __launch_bounds__(1024)
     route_kernel(int c_q, int c_k, const double* __restrict__ val_all,
-                 const int32_t* __restrict__ q_sizes_all, const int32_t* __restrict__ k_sizes_all,
-                 long long capacity, int overshoot, int fallback, int ratio_mode,
+                 const unsigned long long* __restrict__ keys_all, const int32_t* __restrict__ q_sizes_all,
+                 const int32_t* __restrict__ k_sizes_all, long long capacity, int overshoot, int fallback,
                  uint8_t* __restrict__ mask_all, long long* __restrict__ entries_all) {
   const int h = blockIdx.x;
   const int nb = c_q * c_k;
   const double* val = val_all + (size_t)h * nb;
+  const unsigned long long* keys = keys_all + (size_t)h * nb;
   const int32_t* qs = q_sizes_all + (size_t)h * c_q;
   uint8_t* mask = mask_all + (size_t)h * nb;
   extern __shared__ int32_t s_ks[];  // [c_k]
   __shared__ unsigned long long s_hw[kRouteBins];
   __shared__ unsigned int s_hc[kRouteBins];
-  __shared__ Prio s_prefix;  // digits chosen so far (others zero)
+  __shared__ unsigned long long s_pa, s_pb;  // digits chosen so far (others zero)
+  __shared__ unsigned int s_pc;
   __shared__ Prio s_red[32];
   __shared__ long long s_redw[32];
   __shared__ double s_redd[32];
@@ -362,46 +382,66 @@ __global__ void __launch_bounds__(1024)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x;
   for (int j = tid; j < c_k; j += nthr) s_ks[j] = k_sizes_all[(size_t)h * c_k + j];
-  if (tid == 0) { s_prefix.a = 0; s_prefix.b = 0; s_prefix.c = 0; s_base = 0; s_flag = 0; }
+  if (tid == 0) { s_pa = 0; s_pb = 0; s_pc = 0; s_base = 0; s_flag = 0; }
   __syncthreads();
 
-  auto prio = [&](int b, double v, long long w) -> Prio {
-    Prio p;
-    p.a = ord64(ratio_mode == 0 ? v / (double)w : v);
-    p.b = ord64(v);
-    p.c = ~(unsigned int)b;
-    return p;
+  auto getb = [&](unsigned int c) -> unsigned long long { return ord64(val[~c]); };
+  auto pgt = [&](const Prio& x, const Prio& y) -> bool {  // x strictly earlier in the walk than y
+    if (x.a != y.a) return x.a > y.a;
+    if (x.c == y.c) return false;
+    const unsigned long long xb = getb(x.c), yb = getb(y.c);
+    if (xb != yb) return xb > yb;
+    return x.c > y.c;
   };
   // iterate this thread's blocks b = tid, tid + nthr, ... keeping (row, col) incrementally
-#define FOR_BLOCKS(BODY)                                        \
-  {                                                             \
-    int qi_ = tid / c_k, kj_ = tid % c_k;                       \
-    const int dq_ = nthr / c_k, dk_ = nthr % c_k;               \
-    for (int b = tid; b < nb; b += nthr) {                      \
+#define FOR_BLOCKS(BODY)                                             \
+  {                                                                  \
+    int qi_ = tid / c_k, kj_ = tid % c_k;                            \
+    const int dq_ = nthr / c_k, dk_ = nthr % c_k;                    \
+    for (int b = tid; b < nb; b += nthr) {                           \
       const long long w = (long long)qs[qi_] * (long long)s_ks[kj_]; \
-      BODY                                                      \
-      qi_ += dq_; kj_ += dk_;                                   \
-      if (kj_ >= c_k) { kj_ -= c_k; ++qi_; }                    \
-    }                                                           \
+      BODY                                                           \
+      qi_ += dq_; kj_ += dk_;                                        \
+      if (kj_ >= c_k) { kj_ -= c_k; ++qi_; }                         \
+    }                                                                \
   }
 
   // ---- phase 1: first block that does not fit ---------------------------------------------------
   bool all_fit = false;
-  int last_field = 0, last_shift = 64, last_width = 0;
+  int last_field = 0, last_shift = 64;
   for (int pass = 0; pass < kRoutePasses; ++pass) {
     int field, shift, width;
     pass_geom(pass, field, shift, width);
     for (int k = tid; k < kRouteBins; k += nthr) { s_hw[k] = 0ull; s_hc[k] = 0u; }
     __syncthreads();
-    const Prio pre = s_prefix;
+    const unsigned long long pa = s_pa, pb = s_pb;
+    const unsigned int pc = s_pc;
+    const int hs = shift + width;
     {
       // run-length accumulation: consecutive candidates usually share the digit in the top passes
       unsigned int rd = 0xffffffffu, rc = 0;
       unsigned long long rw = 0;
       FOR_BLOCKS({
-        const Prio p = prio(b, val[b], w);
-        if (prio_prefix_eq(p, pre, field, shift, width)) {
-          const unsigned int dg = prio_digit(p, field, shift, width);
+        const unsigned long long ka = keys[b];
+        bool cand;
+        unsigned int dg;
+        if (field == 0) {
+          cand = hs >= 64 ? true : (ka >> hs) == (pa >> hs);
+          dg = (unsigned int)(ka >> shift) & ((1u << width) - 1u);
+        } else if (ka != pa) {
+          cand = false; dg = 0;
+        } else {
+          const unsigned long long kb = getb(~(unsigned int)b);
+          if (field == 1) {
+            cand = hs >= 64 ? true : (kb >> hs) == (pb >> hs);
+            dg = (unsigned int)(kb >> shift) & ((1u << width) - 1u);
+          } else {
+            const unsigned int kc = ~(unsigned int)b;
+            cand = kb == pb && (hs >= 32 ? true : (kc >> hs) == (pc >> hs));
+            dg = (kc >> shift) & ((1u << width) - 1u);
+          }
+        }
+        if (cand) {
           if (dg != rd) {
             if (rc) { atomicAdd(&s_hw[rd], rw); atomicAdd(&s_hc[rd], rc); }
             rd = dg; rw = 0; rc = 0;
@@ -414,11 +454,11 @@ __global__ void __launch_bounds__(1024)
     }
     __syncthreads();
     if (warp == 0) {
-      // find the first bin (from the top) where the running weight exceeds the capacity:
-      // each lane owns 64 consecutive bins, lane 0 the highest
+      // first bin (from the top) where the running weight exceeds the capacity: each lane owns 64
+      // consecutive bins, lane 0 the highest
       const int nbins = 1 << width;
       const int per = kRouteBins / 32;
-      const int hi = nbins - 1 - lane * per;  // this lane scans hi, hi-1, ..., hi-per+1
+      const int hi = nbins - 1 - lane * per;
       unsigned long long mine = 0;
       for (int q = 0; q < per; ++q) {
         const int dg = hi - q;
@@ -449,59 +489,70 @@ __global__ void __launch_bounds__(1024)
             run += (long long)s_hw[dg];
           }
           s_base = run;
-          if (field == 0) s_prefix.a |= (unsigned long long)found << shift;
-          else if (field == 1) s_prefix.b |= (unsigned long long)found << shift;
-          else s_prefix.c |= (unsigned int)found << shift;
+          if (field == 0) s_pa |= (unsigned long long)found << shift;
+          else if (field == 1) s_pb |= (unsigned long long)found << shift;
+          else s_pc |= (unsigned int)found << shift;
           s_flag = (s_hc[found] == 1) ? 2 : 0;  // unique candidate -> it is the boundary block
         }
       }
     }
     __syncthreads();
-    last_field = field; last_shift = shift; last_width = width;
+    last_field = field; last_shift = shift;
     if (s_flag == 1) { all_fit = true; break; }
     if (s_flag == 2) break;
   }
-  // locate the boundary block (unique element matching the chosen digits)
+  // locate the boundary block (the unique element matching every chosen digit)
   Prio bound;
-  bound.a = 0; bound.b = 0; bound.c = 0;
+  bound.a = 0; bound.c = 0;
   long long remaining = capacity - s_base;
   __syncthreads();
   if (!all_fit) {
-    const Prio pre = s_prefix;
-    // "all digits up to and including the last pass agree" == prefix test of a virtual next pass
+    const unsigned long long pa = s_pa, pb = s_pb;
+    const unsigned int pc = s_pc;
     FOR_BLOCKS({
-      const Prio p = prio(b, val[b], w);
-      if (prio_prefix_eq(p, pre, last_field, last_shift, 0)) s_red[0] = p;  // exactly one writer
+      const unsigned long long ka = keys[b];
+      bool hit;
+      if (last_field == 0) hit = (ka >> last_shift) == (pa >> last_shift);
+      else if (ka != pa) hit = false;
+      else {
+        const unsigned long long kb = getb(~(unsigned int)b);
+        if (last_field == 1) hit = (kb >> last_shift) == (pb >> last_shift);
+        else hit = kb == pb && ((~(unsigned int)b) >> last_shift) == (pc >> last_shift);
+      }
+      if (hit) { s_red[0].a = ka; s_red[0].c = ~(unsigned int)b; }  // exactly one writer
+      (void)w;
     })
     __syncthreads();
     bound = s_red[0];
   }
   __syncthreads();
   // ---- mask of the prefix -------------------------------------------------------------------------
-  FOR_BLOCKS({ mask[b] = all_fit ? 1 : (prio_gt(prio(b, val[b], w), bound) ? 1 : 0); })
+  FOR_BLOCKS({
+    Prio p; p.a = keys[b]; p.c = ~(unsigned int)b;
+    mask[b] = all_fit ? 1 : (pgt(p, bound) ? 1 : 0);
+    (void)w;
+  })
   // ---- phase 2: fillRemainder tail ------------------------------------------------------------------
   if (!all_fit && overshoot == SVGEAR_FILL_REMAINDER) {
     Prio cur = bound;
     while (true) {
       Prio best;
-      best.a = 0; best.b = 0; best.c = 0;
+      best.a = 0; best.c = 0;
       long long bw = 0;
       FOR_BLOCKS({
         if (w <= remaining) {
-          const Prio p = prio(b, val[b], w);
-          if (prio_gt(cur, p) && prio_gt(p, best)) { best = p; bw = w; }
+          Prio p; p.a = keys[b]; p.c = ~(unsigned int)b;
+          if (pgt(cur, p) && (best.a == 0 || pgt(p, best))) { best = p; bw = w; }
         }
       })
-      // block arg-max (an all-zero Prio is below every real key: ord64 sets the top bit for
-      // non-negative values)
+      // block arg-max (a == 0 marks "none": ord64 of a non-negative key always has the top bit set)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         Prio q;
         q.a = __shfl_xor_sync(0xffffffffu, best.a, o);
-        q.b = __shfl_xor_sync(0xffffffffu, best.b, o);
         q.c = __shfl_xor_sync(0xffffffffu, best.c, o);
-        long long qw = __shfl_xor_sync(0xffffffffu, bw, o);
-        if (prio_gt(q, best)) { best = q; bw = qw; }
+        const long long qw = __shfl_xor_sync(0xffffffffu, bw, o);
+        if (q.a != 0 && (best.a == 0 || pgt(q, best))) { best = q; bw = qw; }
       }
       __syncthreads();
       if (lane == 0) { s_red[warp] = best; s_redw[warp] = bw; }
@@ -514,17 +565,16 @@ __global__ void __launch_bounds__(1024)
         for (int o = 16; o > 0; o >>= 1) {
           Prio r;
           r.a = __shfl_xor_sync(0xffffffffu, q.a, o);
-          r.b = __shfl_xor_sync(0xffffffffu, q.b, o);
           r.c = __shfl_xor_sync(0xffffffffu, q.c, o);
-          long long rw = __shfl_xor_sync(0xffffffffu, qw, o);
-          if (prio_gt(r, q)) { q = r; qw = rw; }
+          const long long rw = __shfl_xor_sync(0xffffffffu, qw, o);
+          if (r.a != 0 && (q.a == 0 || pgt(r, q))) { q = r; qw = rw; }
         }
         if (lane == 0) { s_red[0] = q; s_redw[0] = qw; }
       }
       __syncthreads();
       best = s_red[0];
       bw = s_redw[0];
-      if (best.a == 0 && best.b == 0 && best.c == 0) break;  // nothing fits any more
+      if (best.a == 0) break;  // nothing fits any more
       if (tid == 0) mask[~best.c] = 1;
       remaining -= bw;
       cur = best;
@@ -538,9 +588,13 @@ __global__ void __launch_bounds__(1024)
   double bestv = -INFINITY;
   int besti = 0x7fffffff;
   FOR_BLOCKS({
-    const double v = val[b];
-    if (mask[b]) { sum_sel += v; ent += w; }
-    if (w <= capacity && v > bestv) { bestv = v; besti = b; }
+    const bool sel = mask[b] != 0;
+    if (sel) ent += w;
+    if (fallback) {
+      const double v = val[b];
+      if (sel) sum_sel += v;
+      if (w <= capacity && v > bestv) { bestv = v; besti = b; }
+    }
   })
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -586,9 +640,13 @@ __global__ void __launch_bounds__(1024)
 
 int launch_route(int bh, int c_q, int c_k, const double* val, const int32_t* q_sizes,
                  const int32_t* k_sizes, int64_t capacity, int overshoot, int fallback,
-                 int ratio_mode, uint8_t* mask, int64_t* entries, cudaStream_t st) {
+                 int ratio_mode, uint8_t* mask, int64_t* entries, unsigned long long* keys,
+                 cudaStream_t st) {
+  route_keys_kernel<<<dim3(ceil_div(c_q * c_k, 256), bh), 256, 0, st>>>(val, q_sizes, k_sizes, c_q, c_k,
+                                                                      ratio_mode, keys);
+  SVG_LAUNCH_OK();
   route_kernel<<<bh, 1024, (size_t)c_k * sizeof(int32_t), st>>>(
-      c_q, c_k, val, q_sizes, k_sizes, (long long)capacity, overshoot, fallback, ratio_mode, mask,
+      c_q, c_k, val, keys, q_sizes, k_sizes, (long long)capacity, overshoot, fallback, mask,
       reinterpret_cast<long long*>(entries));
   SVG_LAUNCH_OK();
   return SVGEAR_OK;

@@ -96,10 +96,11 @@ def route_error_aware_entries(table: BlockErrorTable, capacity_entries: int, *,
     ks = torch.as_tensor(table.k_sizes).to(dev, torch.int32).view(bh, c_k).contiguous()
     mask = torch.empty((bh, c_q, c_k), dtype=torch.uint8, device=dev)
     entries = torch.empty((bh,), dtype=torch.int64, device=dev)
+    ws = workspace(bh * c_q * c_k * 8 + 1024, dev)
     rc = _lib.lib().svgear_route_error_aware(
         bh, c_q, c_k, err.data_ptr(), qs.data_ptr(), ks.data_ptr(), int(capacity_entries),
         _OVERSHOOT[overshoot], 1 if single_item_fallback else 0, mask.data_ptr(), entries.data_ptr(),
-        None, 0, stream_ptr())
+        ws.data_ptr(), ws.numel(), stream_ptr())
     _lib.check("svgear_route_error_aware", rc)
     total = int(qs[0].long().sum()) * int(ks[0].long().sum())
     return _finish(mask, entries, total, was_2d)

@@ -51,7 +51,7 @@ class TestCAbi:
         p = C.addressof(buf)
         assert lib.svgear_kmeans(0, 1, 8, 64, 2, p, p, 0, p, p, p, p, p, None, None, p, 4096, None) == _lib.EINVAL
         assert lib.svgear_kmeans(0, 1, 8, 48, 2, p, p, 5, p, p, p, p, p, None, None, p, 4096, None) == _lib.ESHAPE
-        assert lib.svgear_route_error_aware(1, 1, 2, p, p, p, -1, 0, 1, p, None, None, 0, None) == _lib.EINVAL
+        assert lib.svgear_route_error_aware(1, 1, 2, p, p, p, -1, 0, 1, p, None, p, 4096, None) == _lib.EINVAL
 
     @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
     def test_compute_entries_fail_loudly_without_a_device(self):
