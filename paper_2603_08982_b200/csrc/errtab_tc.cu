@@ -26,8 +26,8 @@ namespace {
 constexpr int EM = 128;       // query clusters per CTA (M)
 constexpr int ECH = 128;      // max keys per chunk
 constexpr int ERANGE = 16;    // key clusters per CTA
-constexpr int ETHREADS = 320;
-enum { EB_AFULL = 0, EB_BFULL = 1, EB_BEMPTY = 3, EB_ACCFULL = 5, EB_ACCEMPTY = 7 };
+constexpr int ETHREADS = 352;
+enum { EB_AFULL = 0, EB_BFULL = 1, EB_BEMPTY = 3, EB_ACCFULL = 5, EB_ACCEMPTY = 7, EB_STATEMPTY = 9 /* [2 groups][2 buffers] */ };
 
 template <int D>
 struct ESmem {
@@ -35,7 +35,7 @@ struct ESmem {
   static constexpr int kA = 0;                    // qh, ql
   static constexpr int kB = kA + 2 * kTile;       // 2 stages x (dh, dl)
   static constexpr int kStat = kB + 4 * kTile;     // 2 stages x 128 keys x float4
-  static constexpr int kBars = kStat + 2 * ECH * 16;
+  static constexpr int kBars = kStat + 4 * ECH * 16;  // stats: 2 groups x 2 buffers x 128 keys x float4
   static constexpr size_t bytes() { return 1024 + kBars + 256; }
 };
 
@@ -50,10 +50,10 @@ struct ESmem {
       : "memory")
 
 __device__ __forceinline__ float expm1_fast(float g) {
-  // |g| < 0.25: degree-6 Taylor (relative error < 2e-8); otherwise 2^(g log2 e) - 1
-  const float poly = g * fmaf(g, fmaf(g, fmaf(g, fmaf(g, fmaf(g, 1.f / 720.f, 1.f / 120.f), 1.f / 24.f), 1.f / 6.f), 0.5f), 1.f);
+  // |g| < 0.125: degree-4 Taylor (relative error < 3e-6); otherwise 2^(g log2 e) - 1 (< 1e-6)
+  const float poly = g * fmaf(g, fmaf(g, fmaf(g, 1.f / 24.f, 1.f / 6.f), 0.5f), 1.f);
   const float big = ex2(g * 1.4426950408889634f) - 1.f;
-  return fabsf(g) < 0.25f ? poly : big;
+  return fabsf(g) < 0.125f ? poly : big;
 }
 }  // namespace
 
@@ -165,6 +165,8 @@ __global__ void __launch_bounds__(ETHREADS, 1)
       mbar_init(bar(EB_BEMPTY + s), 1);
       mbar_init(bar(EB_ACCFULL + s), 1);
       mbar_init(bar(EB_ACCEMPTY + s), 128);
+      mbar_init(bar(EB_STATEMPTY + 2 * s), 128);
+      mbar_init(bar(EB_STATEMPTY + 2 * s + 1), 128);
     }
     fence_barrier_init();
   }
@@ -176,28 +178,35 @@ __global__ void __launch_bounds__(ETHREADS, 1)
   const int32_t* ksz = k_sizes + (size_t)h * c_k;
   const int32_t* kof = k_offsets + (size_t)h * c_k;
 
-  if (warp == 8) {
-    // =========================== producer ========================================================
+  if (warp == 8 || warp == 10) {
+    // =========================== producers =======================================================
+    // warp 8 stages the q̄ tiles and the even chunks (stage 0), warp 10 the odd chunks (stage 1);
+    // each blocks only on its own loads, so two chunk loads are always in flight.
     constexpr int CPR = D / 8, RPI = 32 / CPR;
     const int sub = lane / CPR, chunk = lane % CPR;
-    for (int p = 0; p < 2; ++p) {
-      const bf16* src = qsplit + (((size_t)h * 2 + p) * cqpad + (size_t)mt * EM) * D;
-      for (int r0 = 0; r0 < EM; r0 += RPI) {
-        const int r = r0 + sub;
-        cp_async16(sA + (uint32_t)(p * L::kTile + (chunk >> 3) * (EM * 128)) + swz(r, chunk & 7),
-                   src + (size_t)r * D + chunk * 8);
+    const int mine = warp == 8 ? 0 : 1;
+    if (warp == 8) {
+      for (int p = 0; p < 2; ++p) {
+        const bf16* src = qsplit + (((size_t)h * 2 + p) * cqpad + (size_t)mt * EM) * D;
+        for (int r0 = 0; r0 < EM; r0 += RPI) {
+          const int r = r0 + sub;
+          cp_async16(sA + (uint32_t)(p * L::kTile + (chunk >> 3) * (EM * 128)) + swz(r, chunk & 7),
+                     src + (size_t)r * D + chunk * 8);
+        }
       }
+      cp_async_commit();
+      cp_async_wait_all();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(EB_AFULL));
     }
-    cp_async_commit();
-    cp_async_wait_all();
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar(EB_AFULL));
     int u = 0, guses[2] = {0, 0};
     for (int j = j_lo; j < j_hi; ++j) {
       const int nj = ksz[j], o = kof[j];
       const int g = (j - j_lo) & 1;
       for (int s0 = 0; s0 < nj; s0 += ECH, ++u) {
+        const int gu = guses[g]++;  // use number of this chunk within its epilogue group
+        if ((u & 1) != mine) continue;
         const int st = u & 1;
         if (u >= 2) mbar_wait(bar(EB_BEMPTY + st), ((u >> 1) + 1) & 1);
         const int nn = ((min(ECH, nj - s0) + 15) >> 4) << 4;
@@ -211,12 +220,11 @@ __global__ void __launch_bounds__(ETHREADS, 1)
                        src + (size_t)row * D + chunk * 8);
           }
         }
-        // per-key scalars of this chunk go to the stat buffer of epilogue group g, which must have
-        // finished its previous chunk (same barrier the MMA issuer waits on)
-        if (guses[g] >= 1) mbar_wait(bar(EB_ACCEMPTY + g), (guses[g] - 1) & 1);
-        ++guses[g];
+        // per-key scalars: stat buffer (group g, use parity); its previous user was use gu-2
+        const int sb = g * 2 + (gu & 1);
+        if (gu >= 2) mbar_wait(bar(EB_STATEMPTY + sb), ((gu >> 1) + 1) & 1);
         for (int r = lane; r < nn; r += 32)
-          cp_async16(sStat + (uint32_t)((g * ECH + r) * 16), kstat + (size_t)h * n_k + min(o + s0 + r, n_k - 1));
+          cp_async16(sStat + (uint32_t)((sb * ECH + r) * 16), kstat + (size_t)h * n_k + min(o + s0 + r, n_k - 1));
         cp_async_commit();
         cp_async_wait_all();
         fence_proxy_async();
@@ -278,32 +286,47 @@ __global__ void __launch_bounds__(ETHREADS, 1)
       float M = 0.f, em = 1.f, em2 = 1.f, acc = 0.f;
       for (int s0 = 0; s0 < nj; s0 += ECH, ++uses, ++u) {
         const int valid = min(ECH, nj - s0);
-        const float4* ks = stat_smem + g * ECH;
+        const int sbuf = g * 2 + (uses & 1);
+        const float4* ks = stat_smem + sbuf * ECH;
         mbar_wait(bar(EB_ACCFULL + g), uses & 1);
         tc_fence_after();
+        // pass 1: chunk maximum of g for this query cluster -> raise the running maximum once
+        float gmax = -INFINITY;
+        for (int c0 = 0; c0 < valid; c0 += 16) {
+          uint32_t a[16];
+          TMEM_LD16(tcol + c0, a);
+          tc_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            gmax = fmaxf(gmax, c0 + q < valid ? __uint_as_float(a[q]) : -INFINITY);
+        }
+        gmax *= scale;
+        if (gmax > M) {
+          const float r = __expf(M - gmax);
+          acc *= r * r;
+          M = gmax;
+          em = __expf(-M);
+          em2 = em * em;
+        }
+        // pass 2: branch-free accumulation at the fixed maximum M:
+        //   xs = exp(g - M) - exp(-M) = em * expm1(g)   (g <= M; the clamp only guards overflow)
         for (int c0 = 0; c0 < valid; c0 += 16) {
           uint32_t a[16];
           TMEM_LD16(tcol + c0, a);
           tc_wait_ld();
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            if (c0 + q < valid) {
-              const float4 st4 = ks[c0 + q];
-              const float gg = __uint_as_float(a[q]) * scale;
-              if (gg > M) {
-                const float r = __expf(M - gg);
-                acc *= r * r;
-                M = gg;
-                em = __expf(-M);
-                em2 = em * em;
-              }
-              const float xs = gg < 20.f ? expm1_fast(gg) * em : (__expf(gg - M) - em);
-              acc += st4.x * em2 - (em * xs) * st4.y + (xs * xs) * st4.z;
-            }
+            const float4 st4 = ks[c0 + q];
+            const float gg = fminf(__uint_as_float(a[q]) * scale, 85.f);
+            const float xs = expm1_fast(gg) * em;
+            // A em^2 - 2B (em xs) + C xs^2, Horner in xs
+            const float term = fmaf(fmaf(st4.z, xs, -st4.y * em), xs, st4.x * em2);
+            acc += c0 + q < valid ? term : 0.f;
           }
         }
         tc_fence_before();
         mbar_arrive(bar(EB_ACCEMPTY + g));
+        mbar_arrive(bar(EB_STATEMPTY + sbuf));
       }
       if (live) {
         const double lift = 2.0 * ((double)sb - (double)mr + (double)M);

@@ -362,16 +362,34 @@ __global__ void __launch_bounds__(1024)
     route_kernel(int c_q, int c_k, const double* __restrict__ val_all,
                  const unsigned long long* __restrict__ keys_all, const int32_t* __restrict__ q_sizes_all,
                  const int32_t* __restrict__ k_sizes_all, long long capacity, int overshoot, int fallback,
-                 uint8_t* __restrict__ mask_all, long long* __restrict__ entries_all) {
+                 uint8_t* __restrict__ mask_all, long long* __restrict__ entries_all, int pieces,
+                 int piece_bits) {
   const int h = blockIdx.x;
   const int nb = c_q * c_k;
   const double* val = val_all + (size_t)h * nb;
   const unsigned long long* keys = keys_all + (size_t)h * nb;
   const int32_t* qs = q_sizes_all + (size_t)h * c_q;
   uint8_t* mask = mask_all + (size_t)h * nb;
-  extern __shared__ int32_t s_ks[];  // [c_k]
-  __shared__ unsigned long long s_hw[kRouteBins];
-  __shared__ unsigned int s_hc[kRouteBins];
+  // Weighted histograms use native 32-bit shared atomics: a block weight (up to 34 bits) is split
+  // into `pieces` fields of `piece_bits` bits, each summed in its own counter array (64-bit shared
+  // atomics compile to CAS loops and dominated this kernel).
+  extern __shared__ int32_t s_dyn[];
+  int32_t* s_ks = s_dyn;                                                        // [c_k]
+  unsigned int* s_hc = reinterpret_cast<unsigned int*>(s_dyn + ((c_k + 3) & ~3));  // [bins]
+  unsigned int* s_hp = s_hc + kRouteBins;                                         // [pieces][bins]
+  auto bin_weight = [&](int dg) -> unsigned long long {
+    unsigned long long t = 0;
+    for (int q = 0; q < pieces; ++q) t += (unsigned long long)s_hp[q * kRouteBins + dg] << (q * piece_bits);
+    return t;
+  };
+  auto bin_add = [&](unsigned int dg, unsigned long long wsum, unsigned int cnt) {
+    const unsigned long long m = (1ull << piece_bits) - 1ull;
+    for (int q = 0; q < pieces; ++q) {
+      const unsigned int part = (unsigned int)((wsum >> (q * piece_bits)) & m);
+      if (part) atomicAdd(&s_hp[q * kRouteBins + dg], part);
+    }
+    atomicAdd(&s_hc[dg], cnt);
+  };
   __shared__ unsigned long long s_pa, s_pb;  // digits chosen so far (others zero)
   __shared__ unsigned int s_pc;
   __shared__ Prio s_red[32];
@@ -412,7 +430,7 @@ __global__ void __launch_bounds__(1024)
   for (int pass = 0; pass < kRoutePasses; ++pass) {
     int field, shift, width;
     pass_geom(pass, field, shift, width);
-    for (int k = tid; k < kRouteBins; k += nthr) { s_hw[k] = 0ull; s_hc[k] = 0u; }
+    for (int k = tid; k < kRouteBins * (pieces + 1); k += nthr) s_hc[k] = 0u;  // counts + all pieces
     __syncthreads();
     const unsigned long long pa = s_pa, pb = s_pb;
     const unsigned int pc = s_pc;
@@ -442,15 +460,16 @@ __global__ void __launch_bounds__(1024)
           }
         }
         if (cand) {
-          if (dg != rd) {
-            if (rc) { atomicAdd(&s_hw[rd], rw); atomicAdd(&s_hc[rd], rc); }
+          // a run is flushed when the digit changes or before a piece field could overflow
+          if (dg != rd || rc >= 64u) {
+            if (rc) bin_add(rd, rw, rc);
             rd = dg; rw = 0; rc = 0;
           }
           rw += (unsigned long long)w;
           rc += 1;
         }
       })
-      if (rc) { atomicAdd(&s_hw[rd], rw); atomicAdd(&s_hc[rd], rc); }
+      if (rc) bin_add(rd, rw, rc);
     }
     __syncthreads();
     if (warp == 0) {
@@ -462,7 +481,7 @@ __global__ void __launch_bounds__(1024)
       unsigned long long mine = 0;
       for (int q = 0; q < per; ++q) {
         const int dg = hi - q;
-        if (dg >= 0) mine += s_hw[dg];
+        if (dg >= 0) mine += bin_weight(dg);
       }
       unsigned long long inc = mine;
 #pragma unroll
@@ -485,8 +504,9 @@ __global__ void __launch_bounds__(1024)
             const int dg = hi - q;
             if (dg < 0) break;
             if (s_hc[dg] == 0) continue;
-            if (run + (long long)s_hw[dg] > capacity) { found = dg; break; }
-            run += (long long)s_hw[dg];
+            const long long bwt = (long long)bin_weight(dg);
+            if (run + bwt > capacity) { found = dg; break; }
+            run += bwt;
           }
           s_base = run;
           if (field == 0) s_pa |= (unsigned long long)found << shift;
@@ -645,9 +665,19 @@ int launch_route(int bh, int c_q, int c_k, const double* val, const int32_t* q_s
   route_keys_kernel<<<dim3(ceil_div(c_q * c_k, 256), bh), 256, 0, st>>>(val, q_sizes, k_sizes, c_q, c_k,
                                                                       ratio_mode, keys);
   SVG_LAUNCH_OK();
-  route_kernel<<<bh, 1024, (size_t)c_k * sizeof(int32_t), st>>>(
-      c_q, c_k, val, keys, q_sizes, k_sizes, (long long)capacity, overshoot, fallback, mask,
-      reinterpret_cast<long long*>(entries));
+  // piece_bits: every counter receives at most nb partial sums of < 2^piece_bits ... but a flushed
+  // run holds up to 64 blocks, so a field sum stays below 2^32 when nb * 2^piece_bits <= 2^32
+  int lg = 0;
+  while ((1ll << lg) < (long long)c_q * c_k) ++lg;
+  int piece_bits = 31 - lg;
+  if (piece_bits > 17) piece_bits = 17;
+  if (piece_bits < 6) return SVGEAR_EUNSUPPORTED;
+  const int pieces = (40 + piece_bits - 1) / piece_bits;  // run sums: 34-bit weights x 64 blocks
+  const size_t smem = ((size_t)((c_k + 3) & ~3) + (size_t)kRouteBins * (pieces + 1)) * sizeof(int32_t);
+  SVG_CUDA_OK(cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  route_kernel<<<bh, 1024, smem, st>>>(c_q, c_k, val, keys, q_sizes, k_sizes, (long long)capacity, overshoot,
+                                       fallback, mask, reinterpret_cast<long long*>(entries), pieces,
+                                       piece_bits);
   SVG_LAUNCH_OK();
   return SVGEAR_OK;
 }
