@@ -51,6 +51,11 @@ enum {
   SVGEAR_EXEC_FP32_CHECK = 1   /* CUDA-core fp32 everywhere, fp32 output (the "fp32 check mode")  */
 };
 
+/* OR-ed into svgear_kmeans' exec_mode: evaluate every token against every centre in every Lloyd
+ * iteration.  Without it the tensor-core mode skips tokens whose distance bounds (Hamerly) prove
+ * that their cluster cannot change — the assignments are identical, only the work differs. */
+enum { SVGEAR_KMEANS_FULL_EVAL = 0x100 };
+
 /* Problem shape of one call (all `bh` instances share it). */
 typedef struct SvgEarShape {
   int32_t bh;  /* number of independent (Q,K,V) instances = batch * heads                         */
@@ -100,7 +105,7 @@ int svgear_workspace_bytes(const SvgEarShape* shape, size_t* bytes);
  * clusters repaired in ascending order from the farthest token of a cluster with >=2 members;
  * convergence is tested before the centroid update; final centroids are the member means;
  * permutation = stable sort by cluster.  Distances are evaluated in fp32 (reference: float64):
- * exec_mode SVGEAR_EXEC_BF16_TENSOR forms x.c on the tensor cores (tcgen05) from a 3-way bf16
+ * exec_mode SVGEAR_EXEC_BF16_TENSOR forms x.c on the tensor cores (tcgen05) from a 2-way bf16
  * split of the fp32 centroids with fp32 accumulation; SVGEAR_EXEC_FP32_CHECK uses fp32 FMAs.
  *   x            [bh][n][d] bf16          init_centroids [bh][c][d] f32
  *   assign,perm  [bh][n] i32              sizes,offsets  [bh][c] i32

@@ -25,6 +25,7 @@ OK, EINVAL, ESHAPE, ECUDA, EWORKSPACE, EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 EST_VALUE_AWARE, EST_PLAIN = 0, 1
 FILL_REMAINDER, STOP_AT_FIRST_OVERFLOW = 0, 1
 EXEC_BF16_TENSOR, EXEC_FP32_CHECK = 0, 1
+KMEANS_FULL_EVAL = 0x100
 
 
 class SvgEarError(RuntimeError):

@@ -107,8 +107,12 @@ def _pad_centers(tok_f32, centers, k):
     return centers
 
 
-def run_lloyd(x, starts, max_iters, fp32_check=False):
-    """x [bh,n,d] bf16, starts [bh,c,d] f32 -> dict of raw svgear_kmeans outputs."""
+def run_lloyd(x, starts, max_iters, fp32_check=False, full_eval=False):
+    """x [bh,n,d] bf16, starts [bh,c,d] f32 -> dict of raw svgear_kmeans outputs.
+
+    `full_eval` evaluates every token against every centre in every iteration; by default the
+    tensor-core mode skips tokens whose distance bounds prove their cluster cannot change (same
+    assignments, see SVGEAR_KMEANS_FULL_EVAL in include/svgear.h)."""
     bh, n, d = x.shape
     c = starts.shape[1]
     dev = x.device
@@ -124,7 +128,8 @@ def run_lloyd(x, starts, max_iters, fp32_check=False):
     shape = _lib.Shape(bh, n, n, d, c, c)
     ws = workspace(_lib.workspace_bytes(shape), dev)
     rc = _lib.lib().svgear_kmeans(
-        _lib.EXEC_FP32_CHECK if fp32_check else _lib.EXEC_BF16_TENSOR, bh, n, d, c, x.data_ptr(), starts.data_ptr(), int(max_iters), out["assign"].data_ptr(),
+        (_lib.EXEC_FP32_CHECK if fp32_check else _lib.EXEC_BF16_TENSOR) | (_lib.KMEANS_FULL_EVAL if full_eval else 0),
+        bh, n, d, c, x.data_ptr(), starts.data_ptr(), int(max_iters), out["assign"].data_ptr(),
         out["perm"].data_ptr(), out["sizes"].data_ptr(), out["offsets"].data_ptr(),
         out["centroids"].data_ptr(), out["iters"].data_ptr(), out["inertia"].data_ptr(),
         ws.data_ptr(), ws.numel(), stream_ptr())

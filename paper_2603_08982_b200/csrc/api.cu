@@ -116,7 +116,8 @@ int svgear_kmeans(int32_t exec_mode, int32_t bh, int32_t n, int32_t d, int32_t c
   if (!x || !init_centroids || !assign || !perm || !sizes || !offsets || !centroids || !workspace)
     return SVGEAR_EINVAL;
   if (max_iters < 1) return SVGEAR_EINVAL;
-  if (exec_mode != SVGEAR_EXEC_BF16_TENSOR && exec_mode != SVGEAR_EXEC_FP32_CHECK) return SVGEAR_EINVAL;
+  const int32_t base_mode = exec_mode & ~SVGEAR_KMEANS_FULL_EVAL;
+  if (base_mode != SVGEAR_EXEC_BF16_TENSOR && base_mode != SVGEAR_EXEC_FP32_CHECK) return SVGEAR_EINVAL;
   if (bh < 1 || n < 1 || (d != 64 && d != 128) || c < 1 || c > n || c > kMaxClusters)
     return SVGEAR_ESHAPE;
   if (!device_present()) return SVGEAR_ECUDA;

@@ -201,8 +201,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       if (lane == 0) mbar_arrive(bar(b_full + st));
     }
   } else if (warp == 6) {
-    // =========================== MMA issuer (one thread) =======================================
-    if (lane == 0) {
+    // =========================== MMA issuer (one elected thread) ===============================
+    if (elect_one()) {
       constexpr uint32_t idesc_qk = make_idesc(BM, BN, 0);
       constexpr uint32_t idesc_pv = make_idesc(BM, D, 1);
       const uint32_t tS[2] = {tmem, tmem + 64};

@@ -100,6 +100,14 @@ struct KmeansScratch {
   bf16* pieces;           // [bh][pieces][cpad][d]  split-bf16 centroids (tensor-core assignment)
   float* cnorm_pad;       // [bh][cpad]
   float* xnorm;           // [bh][n]
+  // exact bound-based skipping (tensor-core mode): per-token bounds, active lists, centre movement
+  float* ub;              // [bh][n]  >= distance to the assigned centre
+  float* lb;              // [bh][n]  <= distance to every other centre
+  int32_t* active;        // [bh][n]  tokens to re-evaluate this iteration (first nactive[h])
+  int32_t* nactive;       // [bh]
+  float* move;            // [bh][c]  |c_new - c_old| of the last update
+  uint8_t* dirty;         // [bh][c]  membership changed this iteration
+  int32_t* iters_run;     // [bh]     iterations executed (internal copy of `iters`)
   bool carve(Carver& cv, int bh, int n, int c, int d);
 };
 

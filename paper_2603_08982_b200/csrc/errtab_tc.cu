@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(ETHREADS, 1)
     }
   } else if (warp == 9) {
     // =========================== MMA issuer ======================================================
-    if (lane == 0) {
+    if (elect_one()) {
       mbar_wait(bar(EB_AFULL), 0);
       int u = 0, uses[2] = {0, 0};
       for (int j = j_lo; j < j_hi; ++j) {

@@ -138,9 +138,53 @@ __global__ void sizes_hist_kernel(const int32_t* __restrict__ assign, int n, int
 // empty-cluster repair (clustering.py:116-124): for each empty cluster in ascending order move the
 // token with the largest own distance (first maximum) among clusters of size >= 2.
 // ------------------------------------------------------------------------------------------------
+// The own distances the tensor-core assignment stores are |x|^2 - 2x.c + |c|^2 in fp32 (cancellation
+// noise ~1e-5 |x|^2) and, with bound-based skipping, stale for skipped tokens.  The repair rule
+// ranks tokens by own distance (clustering.py:118), so an instance that actually has an empty
+// cluster (rare) first gets all of them recomputed exactly — fp32 sum of squared differences against
+// the current centres — by this grid-wide kernel; other instances return after scanning their sizes.
+__global__ void __launch_bounds__(256)
+    own_refresh_kernel(int n, int c, int d, const bf16* __restrict__ x_all, const float* __restrict__ cent_all,
+                       const int32_t* __restrict__ assign_all, const int32_t* __restrict__ sizes_all,
+                       float* __restrict__ own_all, const int32_t* __restrict__ done) {
+  const int h = blockIdx.y;
+  if (done[h]) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int empty = 0;
+  for (int j = tid; j < c; j += 256) empty |= (sizes_all[(size_t)h * c + j] == 0);
+  if (!__syncthreads_or(empty)) return;
+  const bf16* x = x_all + (size_t)h * n * d;
+  const float* cent = cent_all + (size_t)h * c * d;
+  const int32_t* assign = assign_all + (size_t)h * n;
+  float* own = own_all + (size_t)h * n;
+  const int lo = blockIdx.x * kSortChunk, hi = min(n, lo + kSortChunk);
+  for (int t0 = lo + warp * 4; t0 < hi; t0 += 32) {  // 4 independent rows per warp step
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = min(t0 + u, hi - 1);
+      const float* cr = cent + (size_t)assign[t] * d;
+      for (int k = lane * 2; k < d; k += 64) {
+        const uint32_t xb = __ldg(reinterpret_cast<const uint32_t*>(x + (size_t)t * d + k));
+        const float2 cc = *reinterpret_cast<const float2*>(cr + k);
+        const float d0 = __uint_as_float(xb << 16) - cc.x, d1 = __uint_as_float(xb & 0xffff0000u) - cc.y;
+        acc[u] = fmaf(d0, d0, acc[u]);
+        acc[u] = fmaf(d1, d1, acc[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float v = warp_sum(acc[u]);
+      if (lane == 0 && t0 + u < hi) own[t0 + u] = v;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(1024)
-    repair_kernel(int n, int c, int32_t* __restrict__ assign_all, float* __restrict__ own_all,
-                  int32_t* __restrict__ sizes_all, const int32_t* __restrict__ done) {
+    repair_kernel(int n, int c, int32_t* __restrict__ assign_all,
+                  float* __restrict__ own_all, int32_t* __restrict__ sizes_all, float* __restrict__ ub_all,
+                  float* __restrict__ lb_all, uint8_t* __restrict__ dirty_all,
+                  const int32_t* __restrict__ done) {
   const int h = blockIdx.x;
   if (done[h]) return;
   int32_t* assign = assign_all + (size_t)h * n;
@@ -206,10 +250,17 @@ __global__ void __launch_bounds__(1024)
           if (ov > bv || (ov == bv && ox < bx)) { bv = ov; bx = ox; }
         }
         if (lane == 0 && bx != 0x7fffffff) {
-          sizes[assign[bx]] -= 1;
+          const int from = assign[bx];
+          sizes[from] -= 1;
           sizes[e] += 1;
           assign[bx] = e;
           own[bx] = 0.f;
+          if (dirty_all) {  // both memberships changed; the moved token is re-evaluated next time
+            dirty_all[(size_t)h * c + from] = 1;
+            dirty_all[(size_t)h * c + e] = 1;
+            ub_all[(size_t)h * n + bx] = 0.f;
+            lb_all[(size_t)h * n + bx] = 0.f;
+          }
         }
       }
     }
@@ -265,7 +316,8 @@ __global__ void __launch_bounds__(1024)
     scan_kernel(int n, int c, int nchunks, int iter, const int32_t* __restrict__ sizes_all,
                 int32_t* __restrict__ offsets_all, int32_t* __restrict__ chunk_counts,
                 const double* __restrict__ chunk_inertia, double* __restrict__ inertia,
-                int32_t* __restrict__ iters, const int32_t* __restrict__ changed,
+                int32_t* __restrict__ iters, int32_t* __restrict__ iters_run,
+                int32_t* __restrict__ nactive, const int32_t* __restrict__ changed,
                 int32_t* __restrict__ done) {
   const int h = blockIdx.x;
   if (done[h]) return;
@@ -325,6 +377,8 @@ __global__ void __launch_bounds__(1024)
     for (int chn = 0; chn < nchunks; ++chn) s += chunk_inertia[(size_t)h * nchunks + chn];
     if (inertia) inertia[h] = s;
     if (iters) iters[h] = iter + 1;
+    iters_run[h] = iter + 1;
+    nactive[h] = 0;  // the next iteration's filter appends to an empty list
     if (iter > 0 && !changed[h]) done[h] = 1;  // assignments unchanged -> converged
   }
 }
@@ -372,13 +426,19 @@ __global__ void __launch_bounds__(128)
     cluster_mean_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ perm, int n, int c,
                         const int32_t* __restrict__ sizes, const int32_t* __restrict__ offsets,
                         float* __restrict__ means, float* __restrict__ norms,
-                        const int32_t* __restrict__ done) {
+                        const int32_t* __restrict__ done, const uint8_t* __restrict__ dirty,
+                        float* __restrict__ move) {
   const int h = blockIdx.y;
   if (done && done[h]) return;
   const int j = blockIdx.x;
+  if (dirty && !dirty[(size_t)h * c + j]) {  // same members in the same order: the mean is unchanged
+    if (threadIdx.x == 0) move[(size_t)h * c + j] = 0.f;
+    return;
+  }
   constexpr int EPL = D / 32;
   __shared__ double part[4][D];
   __shared__ float s_c[D];
+  __shared__ float s_dc[D];  // new - old per component (for the centre movement)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nj = sizes[(size_t)h * c + j], o = offsets[(size_t)h * c + j];
   double acc[EPL];
@@ -417,22 +477,89 @@ __global__ void __launch_bounds__(128)
   if (tid < D) {
     float* out = means + ((size_t)h * c + j) * D;
     float m;
+    const float old = out[tid];
     if (nj > 0) {
       double s = (part[0][tid] + part[1][tid]) + (part[2][tid] + part[3][tid]);
       m = (float)(s / (double)nj);
       out[tid] = m;
     } else {
-      m = out[tid];
+      m = old;
     }
     s_c[tid] = m;
+    s_dc[tid] = m - old;
   }
   __syncthreads();
-  if (norms && warp == 0) {
-    float s = 0.f;
-    for (int k = lane; k < D; k += 32) s = fmaf(s_c[k], s_c[k], s);
+  if (warp == 0) {
+    float s = 0.f, mv = 0.f;
+    for (int k = lane; k < D; k += 32) {
+      s = fmaf(s_c[k], s_c[k], s);
+      mv = fmaf(s_dc[k], s_dc[k], mv);
+    }
     s = warp_sum(s);
-    if (lane == 0) norms[(size_t)h * c + j] = s;
+    mv = warp_sum(mv);
+    if (lane == 0) {
+      if (norms) norms[(size_t)h * c + j] = s;
+      if (move) move[(size_t)h * c + j] = sqrtf(mv);
+    }
   }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Inertia of the LAST distance evaluation (clustering.py:126, 189) when tokens were skipped: exact
+// fp32 squared distances of every token to its centre, summed in float64 in a fixed order.  Runs
+// only for instances that finished in this iteration (converged now, or the iteration cap), before
+// the centroid update overwrites the centres the evaluation used.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool finishing_now(int h, int iter, int last, const int32_t* done,
+                                              const int32_t* iters_run) {
+  if (iters_run[h] != iter + 1) return false;  // converged in an earlier iteration
+  return done[h] || last;
+}
+
+__global__ void __launch_bounds__(256)
+    exact_inertia_kernel(const bf16* __restrict__ x_all, const float* __restrict__ cent_all,
+                         const int32_t* __restrict__ assign_all, int n, int c, int d, int nchunks, int iter,
+                         int last, double* __restrict__ chunk_inertia, const int32_t* __restrict__ done,
+                         const int32_t* __restrict__ iters_run) {
+  const int h = blockIdx.y;
+  if (!finishing_now(h, iter, last, done, iters_run)) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bf16* x = x_all + (size_t)h * n * d;
+  const float* cent = cent_all + (size_t)h * c * d;
+  const int32_t* assign = assign_all + (size_t)h * n;
+  const int lo = blockIdx.x * kSortChunk, hi = min(n, lo + kSortChunk);
+  __shared__ double s_part[8];
+  double dsum = 0.0;
+  for (int t = lo + warp; t < hi; t += 8) {
+    const float* cr = cent + (size_t)assign[t] * d;
+    float acc = 0.f;
+    for (int k = lane * 2; k < d; k += 64) {
+      const uint32_t xb = __ldg(reinterpret_cast<const uint32_t*>(x + (size_t)t * d + k));
+      const float2 cc = *reinterpret_cast<const float2*>(cr + k);
+      const float d0 = __uint_as_float(xb << 16) - cc.x, d1 = __uint_as_float(xb & 0xffff0000u) - cc.y;
+      acc = fmaf(d0, d0, acc);
+      acc = fmaf(d1, d1, acc);
+    }
+    dsum += (double)warp_sum(acc);
+  }
+  if (lane == 0) s_part[warp] = dsum;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += s_part[w];
+    chunk_inertia[(size_t)h * nchunks + blockIdx.x] = s;
+  }
+}
+
+__global__ void inertia_sum_kernel(int bh, int nchunks, int iter, int last, const double* __restrict__ chunk_inertia,
+                                   double* __restrict__ inertia, const int32_t* __restrict__ done,
+                                   const int32_t* __restrict__ iters_run) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= bh) return;
+  if (!finishing_now(h, iter, last, done, iters_run)) return;
+  double s = 0.0;
+  for (int chn = 0; chn < nchunks; ++chn) s += chunk_inertia[(size_t)h * nchunks + chn];
+  inertia[h] = s;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -454,10 +581,9 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ x, const int32_t* _
 // ------------------------------------------------------------------------------------------------
 size_t kmeans_tc_scratch_bytes(int bh, int n, int c, int d);
 int launch_token_norms(int bh, int n, int d, const bf16* x, float* xnorm, cudaStream_t st);
-int launch_kmeans_assign_tc(int bh, int n, int d, int c, const bf16* x, const float* cent,
-                            const float* cnorm, bf16* pieces, float* cnorm_pad, const float* xnorm,
-                            int32_t* assign, float* own_d2, int32_t* sizes, int32_t* changed,
-                            const int32_t* done, cudaStream_t st);
+int launch_kmeans_assign_tc(int bh, int n, int d, int c, int iter, bool full_eval, const bf16* x,
+                            const float* cent, const float* cnorm, KmeansScratch& sc, int32_t* assign,
+                            int32_t* sizes, cudaStream_t st);
 
 bool KmeansScratch::carve(Carver& cv, int bh, int n, int c, int d) {
   const int nchunks = ceil_div(n, kSortChunk);
@@ -472,6 +598,13 @@ bool KmeansScratch::carve(Carver& cv, int bh, int n, int c, int d) {
   pieces = cv.take<bf16>((size_t)bh * 3 * cpad * d);
   cnorm_pad = cv.take<float>((size_t)bh * cpad);
   xnorm = cv.take<float>((size_t)bh * n);
+  ub = cv.take<float>((size_t)bh * n);
+  lb = cv.take<float>((size_t)bh * n);
+  active = cv.take<int32_t>((size_t)bh * n);
+  nactive = cv.take<int32_t>(bh);
+  move = cv.take<float>((size_t)bh * c);
+  dirty = cv.take<uint8_t>((size_t)bh * c);
+  iters_run = cv.take<int32_t>(bh);
   return cv.ok;
 }
 
@@ -486,18 +619,21 @@ int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, con
   SVG_CUDA_OK(cudaMemsetAsync(sc.changed, 0, (size_t)bh * 4, st));
   centroid_norm_kernel<<<ceil_div(bh * c, 8), 256, 0, st>>>(centroids, d, bh * c, sc.cnorm);
   SVG_LAUNCH_OK();
-  const bool use_tc = exec_mode == SVGEAR_EXEC_BF16_TENSOR;
+  const bool full_eval = (exec_mode & SVGEAR_KMEANS_FULL_EVAL) != 0;
+  const bool use_tc = (exec_mode & 0xff) == SVGEAR_EXEC_BF16_TENSOR;
+  const bool bounded = use_tc && !full_eval;  // skip tokens whose bounds prove they cannot move
   if (use_tc) {
     int rc = launch_token_norms(bh, n, d, x, sc.xnorm, st);
     if (rc) return rc;
+    SVG_CUDA_OK(cudaMemsetAsync(sc.nactive, 0, (size_t)bh * 4, st));
+    SVG_CUDA_OK(cudaMemsetAsync(sc.move, 0, (size_t)bh * c * 4, st));
   }
   const size_t hist_smem = (size_t)c * sizeof(int32_t);
   const int hist_blocks = max(1, min(64, ceil_div(n, 4096)));
   for (int it = 0; it < max_iters; ++it) {
     dim3 ga(ceil_div(n, 128), bh);
     if (use_tc) {
-      int rc = launch_kmeans_assign_tc(bh, n, d, c, x, centroids, sc.cnorm, sc.pieces, sc.cnorm_pad,
-                                       sc.xnorm, assign, sc.own_d2, sizes, sc.changed, sc.done, st);
+      int rc = launch_kmeans_assign_tc(bh, n, d, c, it, full_eval, x, centroids, sc.cnorm, sc, assign, sizes, st);
       if (rc) return rc;
     } else if (d == 128)
       assign_fp32_kernel<128><<<ga, 128, 0, st>>>(x, centroids, sc.cnorm, n, c, assign, sc.own_d2,
@@ -508,24 +644,40 @@ int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, con
     SVG_LAUNCH_OK();
     sizes_hist_kernel<<<dim3(hist_blocks, bh), 256, hist_smem, st>>>(assign, n, c, sizes, sc.done);
     SVG_LAUNCH_OK();
-    repair_kernel<<<bh, 1024, 0, st>>>(n, c, assign, sc.own_d2, sizes, sc.done);
+    if (use_tc) {  // exact own distances for the donor choice (the tensor-core ones are rounded / stale)
+      own_refresh_kernel<<<dim3(nchunks, bh), 256, 0, st>>>(n, c, d, x, centroids, assign, sizes, sc.own_d2,
+                                                           sc.done);
+      SVG_LAUNCH_OK();
+    }
+    repair_kernel<<<bh, 1024, 0, st>>>(n, c, assign, sc.own_d2, sizes, sc.ub, sc.lb,
+                                       use_tc ? sc.dirty : nullptr, sc.done);
     SVG_LAUNCH_OK();
     chunk_hist_kernel<<<dim3(nchunks, bh), 256, hist_smem, st>>>(
         assign, sc.prev_assign, sc.own_d2, n, c, nchunks, it, sc.chunk_counts, sc.chunk_inertia,
         sc.changed, sc.done);
     SVG_LAUNCH_OK();
     scan_kernel<<<bh, 1024, 0, st>>>(n, c, nchunks, it, sizes, offsets, sc.chunk_counts,
-                                     sc.chunk_inertia, inertia, iters, sc.changed, sc.done);
+                                     sc.chunk_inertia, inertia, iters, sc.iters_run, sc.nactive,
+                                     sc.changed, sc.done);
     SVG_LAUNCH_OK();
+    if (bounded && inertia) {  // own distances of skipped tokens are stale: recompute the sum exactly
+      const int last = it == max_iters - 1;
+      exact_inertia_kernel<<<dim3(nchunks, bh), 256, 0, st>>>(x, centroids, assign, n, c, d, nchunks, it, last,
+                                                             sc.chunk_inertia, sc.done, sc.iters_run);
+      SVG_LAUNCH_OK();
+      inertia_sum_kernel<<<ceil_div(bh, 128), 128, 0, st>>>(bh, nchunks, it, last, sc.chunk_inertia, inertia, sc.done, sc.iters_run);
+      SVG_LAUNCH_OK();
+    }
     scatter_perm_kernel<<<dim3(nchunks, bh), 256, hist_smem, st>>>(assign, n, c, nchunks,
                                                                    sc.chunk_counts, perm, sc.done);
     SVG_LAUNCH_OK();
+    const uint8_t* dirty = bounded ? sc.dirty : nullptr;
     if (d == 128)
-      cluster_mean_kernel<128><<<dim3(c, bh), 128, 0, st>>>(x, perm, n, c, sizes, offsets,
-                                                           centroids, sc.cnorm, sc.done);
+      cluster_mean_kernel<128><<<dim3(c, bh), 128, 0, st>>>(x, perm, n, c, sizes, offsets, centroids,
+                                                           sc.cnorm, sc.done, dirty, sc.move);
     else
-      cluster_mean_kernel<64><<<dim3(c, bh), 128, 0, st>>>(x, perm, n, c, sizes, offsets,
-                                                          centroids, sc.cnorm, sc.done);
+      cluster_mean_kernel<64><<<dim3(c, bh), 128, 0, st>>>(x, perm, n, c, sizes, offsets, centroids,
+                                                          sc.cnorm, sc.done, dirty, sc.move);
     SVG_LAUNCH_OK();
   }
   return SVGEAR_OK;
@@ -545,10 +697,10 @@ int launch_segment_means(int bh, int n, int d, int c, const bf16* xp, const int3
                          const int32_t* offsets, float* means, float* norms, cudaStream_t st) {
   if (d == 128)
     cluster_mean_kernel<128><<<dim3(c, bh), 128, 0, st>>>(xp, nullptr, n, c, sizes, offsets, means,
-                                                         norms, nullptr);
+                                                         norms, nullptr, nullptr, nullptr);
   else
     cluster_mean_kernel<64><<<dim3(c, bh), 128, 0, st>>>(xp, nullptr, n, c, sizes, offsets, means,
-                                                        norms, nullptr);
+                                                        norms, nullptr, nullptr, nullptr);
   SVG_LAUNCH_OK();
   return SVGEAR_OK;
 }

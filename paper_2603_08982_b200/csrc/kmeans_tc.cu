@@ -75,14 +75,113 @@ __global__ void token_norm_kernel(const bf16* __restrict__ x, int d, long long t
   if (row >= total) return;
   // sequential-in-k accumulation per lane chunk is not needed for parity: |x|^2 is a per-token
   // constant of the argmin; it only enters own_d2.  Lanes split the row, fixed shuffle tree.
+  // each lane takes d/32 consecutive elements (8-byte loads at d=128), fixed shuffle tree
   const bf16* p = x + row * d;
   float s = 0.f;
-  for (int k = lane; k < d; k += 32) {
-    const float f = __bfloat162float(p[k]);
-    s = fmaf(f, f, s);
+  if (d == 128) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p) + lane);
+    const float f0 = __uint_as_float(u.x << 16), f1 = __uint_as_float(u.x & 0xffff0000u);
+    const float f2 = __uint_as_float(u.y << 16), f3 = __uint_as_float(u.y & 0xffff0000u);
+    s = fmaf(f0, f0, s); s = fmaf(f1, f1, s); s = fmaf(f2, f2, s); s = fmaf(f3, f3, s);
+  } else {
+    for (int k = lane * 2; k < d; k += 64) {
+      const uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(p + k));
+      const float f0 = __uint_as_float(u << 16), f1 = __uint_as_float(u & 0xffff0000u);
+      s = fmaf(f0, f0, s); s = fmaf(f1, f1, s);
+    }
   }
   s = warp_sum(s);
   if (lane == 0) xn[row] = s;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Exact bound-based skipping (Hamerly's bounds) — same assignments as plain Lloyd, fewer distances.
+// Every token carries ub >= dist(x, c[assign]) and lb <= min_{j != assign} dist(x, c[j]).  After a
+// centroid update that moved centre j by move[j] (triangle inequality):
+//     ub += move[assign],   lb -= max_{j != assign} move[j].
+// A token whose ub is still below lb (with a margin that covers the fp32 / split-bf16 rounding of
+// the distances the tensor-core kernel would compute) keeps its cluster without being evaluated;
+// the others are compacted into the instance's `active` list and re-evaluated by assign_tc_kernel,
+// which refreshes both bounds.  Iteration 0 (and SVGEAR_KMEANS_FULL_EVAL) marks every token active.
+// Block 0 of each instance also resets the per-iteration counters (sizes, changed, dirty).
+// ------------------------------------------------------------------------------------------------
+constexpr int kFilterTokens = 2048;  // tokens per CTA
+
+__global__ void __launch_bounds__(256)
+    bound_filter_kernel(int n, int c, int all_active, const int32_t* __restrict__ assign,
+                        const float* __restrict__ move, const float* __restrict__ cnorm,
+                        const float* __restrict__ xnorm, float* __restrict__ ub, float* __restrict__ lb,
+                        int32_t* __restrict__ active, int32_t* __restrict__ nactive,
+                        int32_t* __restrict__ sizes, int32_t* __restrict__ changed,
+                        uint8_t* __restrict__ dirty, const int32_t* __restrict__ done) {
+  const int h = blockIdx.y;
+  if (done[h]) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lo = blockIdx.x * kFilterTokens, hi = min(n, lo + kFilterTokens);
+  if (blockIdx.x == 0) {
+    for (int j = tid; j < c; j += 256) {
+      sizes[(size_t)h * c + j] = 0;
+      dirty[(size_t)h * c + j] = all_active ? 1 : 0;
+    }
+    if (tid == 0) {
+      changed[h] = 0;
+      if (all_active) nactive[h] = n;
+    }
+  }
+  if (all_active) {
+    for (int t = lo + tid; t < hi; t += 256) active[(size_t)h * n + t] = t;
+    return;
+  }
+  // largest / second largest centre movement and the largest centre norm of this instance
+  __shared__ float s_m1[8], s_m2[8], s_cn[8];
+  __shared__ int s_a1[8];
+  float m1 = 0.f, m2 = 0.f, cn = 0.f;
+  int a1 = -1;
+  for (int j = tid; j < c; j += 256) {
+    const float v = move[(size_t)h * c + j];
+    if (v > m1) { m2 = m1; m1 = v; a1 = j; } else if (v > m2) m2 = v;
+    cn = fmaxf(cn, cnorm[(size_t)h * c + j]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om1 = __shfl_xor_sync(0xffffffffu, m1, o), om2 = __shfl_xor_sync(0xffffffffu, m2, o);
+    const int oa1 = __shfl_xor_sync(0xffffffffu, a1, o);
+    if (om1 > m1) { m2 = fmaxf(m1, om2); m1 = om1; a1 = oa1; } else m2 = fmaxf(m2, om1);
+    cn = fmaxf(cn, __shfl_xor_sync(0xffffffffu, cn, o));
+  }
+  if (lane == 0) { s_m1[warp] = m1; s_m2[warp] = m2; s_a1[warp] = a1; s_cn[warp] = cn; }
+  __syncthreads();
+  m1 = s_m1[0]; m2 = s_m2[0]; a1 = s_a1[0]; cn = s_cn[0];
+  for (int w = 1; w < 8; ++w) {
+    if (s_m1[w] > m1) { m2 = fmaxf(m1, s_m2[w]); m1 = s_m1[w]; a1 = s_a1[w]; } else m2 = fmaxf(m2, s_m1[w]);
+    cn = fmaxf(cn, s_cn[w]);
+  }
+  // movements are rounded fp32 norms: inflate them slightly so the bounds stay bounds
+  constexpr float kInfl = 1.0f + 1.0f / 65536.0f;
+  m1 *= kInfl; m2 *= kInfl;
+  for (int t0 = lo; t0 < hi; t0 += 256) {
+    const int t = t0 + tid;
+    bool act = false;
+    if (t < hi) {
+      const size_t g = (size_t)h * n + t;
+      const int a = assign[g];
+      const float u = ub[g] + move[(size_t)h * c + a] * kInfl;
+      const float l = lb[g] - (a == a1 ? m2 : m1);
+      ub[g] = u;
+      lb[g] = l;
+      // squared-space margin: the evaluated distances carry an absolute error of a few
+      // 2^-17 (|x|^2 + |c|^2) (2-piece bf16 split + fp32 accumulation); 2^-12 covers it 30x
+      const float marg = (xnorm[g] + cn) * (1.0f / 4096.0f);
+      act = !(l > 0.f && u * u * kInfl + marg < l * l * (2.0f - kInfl));
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    if (bal) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&nactive[h], __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (act) active[(size_t)h * n + base + __popc(bal & ((1u << lane) - 1u))] = t;
+    }
+  }
 }
 
 // Persistent kernel: grid = #SMs; CTA b handles work items b, b+grid, ... where an item is a
@@ -95,12 +194,14 @@ template <int D>
 __global__ void __launch_bounds__(KTHREADS, 1)
     assign_tc_kernel(const bf16* __restrict__ x, const bf16* __restrict__ pieces,
                      const float* __restrict__ cnorm_pad, const float* __restrict__ xnorm, int bh, int n,
-                     int c, int cpad, int cpad16, int32_t* __restrict__ assign, float* __restrict__ own_d2,
-                     int32_t* __restrict__ sizes, int32_t* __restrict__ changed,
-                     const int32_t* __restrict__ done) {
+                     int c, int cpad, int cpad16, int first_iter, int32_t* __restrict__ assign,
+                     float* __restrict__ own_d2, float* __restrict__ ub, float* __restrict__ lb,
+                     const int32_t* __restrict__ active, const int32_t* __restrict__ nactive,
+                     uint8_t* __restrict__ dirty, const int32_t* __restrict__ done) {
   using L = KSmem<D>;
   extern __shared__ uint8_t smem_raw[];
   __shared__ int16_t s_heads[kMaxHeads];
+  __shared__ int s_tstart[kMaxHeads + 1];  // first work item of each listed instance
   __shared__ int s_nactive;
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
@@ -110,14 +211,21 @@ __global__ void __launch_bounds__(KTHREADS, 1)
   auto bar = [&](int i) -> uint32_t { return bars + 8u * (uint32_t)i; };
 
   if (tid == 0) {
-    int na = 0;
-    for (int h = 0; h < bh; ++h)
-      if (!done[h]) s_heads[na++] = (int16_t)h;
+    int na = 0, items = 0;
+    for (int h = 0; h < bh; ++h) {
+      const int cnt = done[h] ? 0 : nactive[h];
+      if (cnt > 0) {
+        s_heads[na] = (int16_t)h;
+        s_tstart[na++] = items;
+        items += (cnt + KM - 1) / KM;
+      }
+    }
+    s_tstart[na] = items;
     s_nactive = na;
   }
   __syncthreads();
-  const int tiles_per_head = (n + KM - 1) / KM;
-  const int total_items = s_nactive * tiles_per_head;
+  const int nlisted = s_nactive;
+  const int total_items = s_tstart[nlisted];
   if ((int)blockIdx.x >= total_items) return;
   const int my_items = (total_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
 
@@ -141,8 +249,17 @@ __global__ void __launch_bounds__(KTHREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const int NT = (cpad16 + KN - 1) / KN;  // N tiles; the last one may be narrower (multiple of 16)
   const int U = NT * kPieces;             // pipeline units per item
-  auto item_head = [&](int it) -> int { return s_heads[((int)blockIdx.x + it * (int)gridDim.x) / tiles_per_head]; };
-  auto item_tile = [&](int it) -> int { return ((int)blockIdx.x + it * (int)gridDim.x) % tiles_per_head; };
+  // work item -> (instance, 256-token tile of its active list): binary search in the item prefix
+  auto locate = [&](int it, int& tile) -> int {
+    const int item = (int)blockIdx.x + it * (int)gridDim.x;
+    int lo = 0, hi = nlisted - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_tstart[mid] <= item) lo = mid; else hi = mid - 1;
+    }
+    tile = item - s_tstart[lo];
+    return s_heads[lo];
+  };
 
   if (warp == 8) {
     // =========================== centroid-piece producer ========================================
@@ -150,7 +267,8 @@ __global__ void __launch_bounds__(KTHREADS, 1)
     const int sub = lane / CPR, chunk = lane % CPR;
     int u = 0;  // running unit counter across items
     for (int it = 0; it < my_items; ++it) {
-      const int h = item_head(it);
+      int tile_unused;
+      const int h = locate(it, tile_unused);
       for (int uu = 0; uu < U; ++uu, ++u) {
         const int st = u % KSTAGES;
         if (u >= KSTAGES) mbar_wait(bar(KB_BEMPTY + st), ((u / KSTAGES) - 1) & 1);
@@ -184,13 +302,16 @@ __global__ void __launch_bounds__(KTHREADS, 1)
     for (int it = 0; it < my_items; ++it) {
       const int b = it & 1;
       if (it >= 2) mbar_wait(bar(KB_AEMPTY + b), ((it >> 1) + 1) & 1);
-      const int h = item_head(it), tok0 = item_tile(it) * KM;
+      int tile;
+      const int h = locate(it, tile);
+      const int tok0 = tile * KM, na = nactive[h];
       const bf16* xsrc = x + (size_t)h * n * D;
+      const int32_t* alist = active + (size_t)h * n;
       const uint32_t dst = sA + (uint32_t)b * L::kABytes;
 #pragma unroll 4
       for (int r0 = 0; r0 < KM; r0 += RPI) {
         const int r = r0 + sub;  // row within the item: M tile r/128, row r%128
-        const int row = min(tok0 + r, n - 1);
+        const int row = __ldg(alist + min(tok0 + r, na - 1));
         const int mt = r >> 7, rr = r & 127;
         cp_async16(dst + (uint32_t)(mt * (128 * D * 2) + (chunk >> 3) * (128 * 128)) + swz(rr, chunk & 7),
                    xsrc + (size_t)row * D + chunk * 8);
@@ -203,7 +324,7 @@ __global__ void __launch_bounds__(KTHREADS, 1)
     }
   } else if (warp == 9) {
     // =========================== MMA issuer ======================================================
-    if (lane == 0) {
+    if (elect_one()) {
       int u = 0, g = 0;  // running unit / N-tile counters
       for (int it = 0; it < my_items; ++it) {
         const int ab = it & 1;
@@ -243,15 +364,14 @@ __global__ void __launch_bounds__(KTHREADS, 1)
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     int g = 0;
     for (int it = 0; it < my_items; ++it) {
-      const int h = item_head(it), tile = item_tile(it);
-      if (tile == 0) {  // reset the per-iteration counters of this instance
-        for (int j = tid; j < c; j += 256) sizes[(size_t)h * c + j] = 0;
-        if (tid == 0) changed[h] = 0;
-      }
-      const int t = tile * KM + m * 128 + (warp & 3) * 32 + lane;
-      const float xn = xnorm[(size_t)h * n + min(t, n - 1)];
+      int tile;
+      const int h = locate(it, tile);
+      const int na = nactive[h];
+      const int ti = tile * KM + m * 128 + (warp & 3) * 32 + lane;  // position in the active list
+      const int t = __ldg(active + (size_t)h * n + min(ti, na - 1));
+      const float xn = xnorm[(size_t)h * n + t];
       const float* cn = cnorm_pad + (size_t)h * cpad;
-      float best = INFINITY;
+      float best = INFINITY, second = INFINITY;
       int bi = 0;
       for (int nt = 0; nt < NT; ++nt, ++g) {
         const int buf = g & 1;
@@ -271,6 +391,7 @@ __global__ void __launch_bounds__(KTHREADS, 1)
             // entry, clustering.py:62; that only matters when two DIFFERENT centroids are both
             // within rounding of the token, and identical centroids still tie exactly here.)
             const float w = fmaf(-2.0f, __uint_as_float(a[j]), __ldg(cn + cb + j));
+            second = fminf(second, fmaxf(w, best));  // runner-up distance (lower bound for skipping)
             if (w < best) {  // strict: ties keep the lowest cluster index (NaN from stale columns never wins)
               best = w;
               bi = cb + j;
@@ -280,9 +401,20 @@ __global__ void __launch_bounds__(KTHREADS, 1)
         tc_fence_before();
         mbar_arrive(bar(KB_ACCEMPTY + buf));
       }
-      if (t < n) {
-        assign[(size_t)h * n + t] = bi;
-        own_d2[(size_t)h * n + t] = fmaxf(xn + best, 0.f);
+      if (ti < na) {
+        const size_t gi = (size_t)h * n + t;
+        const float d2 = fmaxf(xn + best, 0.f);
+        if (!first_iter) {
+          const int prev = assign[gi];
+          if (prev != bi) {  // membership of both clusters changed: their means must be recomputed
+            dirty[(size_t)h * c + prev] = 1;
+            dirty[(size_t)h * c + bi] = 1;
+          }
+        }
+        assign[gi] = bi;
+        own_d2[gi] = d2;
+        ub[gi] = sqrtf(d2);
+        lb[gi] = sqrtf(fmaxf(xn + second, 0.f));
       }
     }
   }
@@ -307,14 +439,18 @@ int launch_token_norms(int bh, int n, int d, const bf16* x, float* xnorm, cudaSt
   return SVGEAR_OK;
 }
 
-int launch_kmeans_assign_tc(int bh, int n, int d, int c, const bf16* x, const float* cent,
-                            const float* cnorm, bf16* pieces, float* cnorm_pad, const float* xnorm,
-                            int32_t* assign, float* own_d2, int32_t* sizes, int32_t* changed,
-                            const int32_t* done, cudaStream_t st) {
+int launch_kmeans_assign_tc(int bh, int n, int d, int c, int iter, bool full_eval, const bf16* x,
+                            const float* cent, const float* cnorm, KmeansScratch& sc, int32_t* assign,
+                            int32_t* sizes, cudaStream_t st) {
   const int cpad = ceil_div(c, KN) * KN;     // row stride of the piece arrays / norm array
   const int cpad16 = ceil_div(c, 16) * 16;   // columns actually multiplied
-  split_centroids_kernel<<<dim3(ceil_div(cpad * d, 256), bh), 256, 0, st>>>(cent, cnorm, d, c, cpad, pieces,
-                                                                           cnorm_pad, done);
+  split_centroids_kernel<<<dim3(ceil_div(cpad * d, 256), bh), 256, 0, st>>>(cent, cnorm, d, c, cpad, sc.pieces,
+                                                                           sc.cnorm_pad, sc.done);
+  SVG_LAUNCH_OK();
+  const int all_active = (iter == 0 || full_eval) ? 1 : 0;
+  bound_filter_kernel<<<dim3(ceil_div(n, kFilterTokens), bh), 256, 0, st>>>(
+      n, c, all_active, assign, sc.move, cnorm, sc.xnorm, sc.ub, sc.lb, sc.active, sc.nactive, sizes,
+      sc.changed, sc.dirty, sc.done);
   SVG_LAUNCH_OK();
   static int num_sms = 0;
   if (num_sms == 0) {
@@ -324,25 +460,28 @@ int launch_kmeans_assign_tc(int bh, int n, int d, int c, const bf16* x, const fl
   }
   for (int h0 = 0; h0 < bh; h0 += kMaxHeads) {
     const int nb = bh - h0 < kMaxHeads ? bh - h0 : kMaxHeads;
-    const int items = nb * ceil_div(n, KM);
+    const int items = nb * ceil_div(n, KM);  // upper bound; the kernel reads the real counts
     const int grid = items < num_sms ? items : num_sms;
     const bf16* xs = x + (size_t)h0 * n * d;
-    const bf16* ps = pieces + (size_t)h0 * kPieces * cpad * d;
-    const float* cs = cnorm_pad + (size_t)h0 * cpad;
-    const float* xns = xnorm + (size_t)h0 * n;
+    const bf16* ps = sc.pieces + (size_t)h0 * kPieces * cpad * d;
+    const float* cs = sc.cnorm_pad + (size_t)h0 * cpad;
+    const float* xns = sc.xnorm + (size_t)h0 * n;
     int32_t* as = assign + (size_t)h0 * n;
-    float* os = own_d2 + (size_t)h0 * n;
-    int32_t* ss = sizes + (size_t)h0 * c;
+    float* os = sc.own_d2 + (size_t)h0 * n;
+    float* us = sc.ub + (size_t)h0 * n;
+    float* ls = sc.lb + (size_t)h0 * n;
+    const int32_t* al = sc.active + (size_t)h0 * n;
+    uint8_t* dt = sc.dirty + (size_t)h0 * c;
     if (d == 128) {
       const size_t smem = KSmem<128>::bytes();
       SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      assign_tc_kernel<128><<<grid, KTHREADS, smem, st>>>(xs, ps, cs, xns, nb, n, c, cpad, cpad16, as, os, ss,
-                                                          changed + h0, done + h0);
+      assign_tc_kernel<128><<<grid, KTHREADS, smem, st>>>(xs, ps, cs, xns, nb, n, c, cpad, cpad16, iter == 0, as, os,
+                                                          us, ls, al, sc.nactive + h0, dt, sc.done + h0);
     } else {
       const size_t smem = KSmem<64>::bytes();
       SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      assign_tc_kernel<64><<<grid, KTHREADS, smem, st>>>(xs, ps, cs, xns, nb, n, c, cpad, cpad16, as, os, ss,
-                                                         changed + h0, done + h0);
+      assign_tc_kernel<64><<<grid, KTHREADS, smem, st>>>(xs, ps, cs, xns, nb, n, c, cpad, cpad16, iter == 0, as, os,
+                                                         us, ls, al, sc.nactive + h0, dt, sc.done + h0);
     }
     SVG_LAUNCH_OK();
   }

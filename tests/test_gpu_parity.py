@@ -446,3 +446,56 @@ class TestDeviceSeeding:
                                              return_aux=True)
         assert int(aux["q_iters"]) <= 16 and int(aux["k_iters"]) <= 16
         assert bool(torch.isfinite(out.float()).all())
+
+
+# --------------------------------------------------------------------------------------------
+# bound-based skipping in the tensor-core Lloyd loop must not change any result
+# (SVGEAR_KMEANS_FULL_EVAL evaluates every token against every centre in every iteration)
+# --------------------------------------------------------------------------------------------
+class TestBoundedLloyd:
+    @staticmethod
+    def both(x, starts, iters=25):
+        from paper_2603_08982_b200.clustering import run_lloyd
+        a = run_lloyd(x, starts, iters)
+        b = run_lloyd(x, starts, iters, full_eval=True)
+        torch.cuda.synchronize()
+        return a, b
+
+    @staticmethod
+    def same(a, b):
+        for key in ("assign", "perm", "sizes", "offsets", "iters"):
+            assert torch.equal(a[key], b[key]), key
+        assert torch.equal(a["centroids"], b["centroids"])  # same members, same order -> same bits
+        # bounded: exact fp32 distances; full evaluation: |x|^2 - 2x.c + |c|^2 from the tensor cores
+        assert torch.allclose(a["inertia"], b["inertia"], rtol=2e-4, atol=1e-6)
+
+    @pytest.mark.parametrize("kind,n,c,d", [("blobs", 6000, 40, 128), ("blobs", 5000, 97, 64),
+                                            ("gauss", 4000, 33, 128), ("gauss", 3000, 300, 64)])
+    def test_same_result_as_full_evaluation(self, kind, n, c, d):
+        heads = []
+        for h in range(3):
+            if kind == "blobs":
+                heads.append(O.round_to_bf16(O.blob_instance(n, n, d, c, c, 0.1, h)[0]))
+            else:
+                heads.append(O.round_to_bf16(np.random.default_rng(h).normal(size=(n, d))))
+        x = dev(np.stack(heads))
+        starts = P.device_start(x, c, seed=7)
+        a, b = self.both(x, starts)
+        self.same(a, b)
+        # and against the float64 oracle from the same start (bit-exact permutation)
+        labels, inertia, iters = O.lloyd(heads[0].astype(np.float64), c, 25, host(starts[0]).astype(np.float64))
+        mism = float((host(a["assign"][0]) != labels).mean())
+        assert mism == 0.0, f"assignment mismatch rate vs float64 oracle {mism}"
+        assert int(a["iters"][0]) == iters
+        assert abs(float(a["inertia"][0]) - inertia) <= 1e-4 * inertia
+
+    def test_duplicates_trigger_repair_with_skipped_tokens(self):
+        # many exact duplicates: empty clusters appear after the first update, when most tokens
+        # are already skipped -> exercises the lazy own-distance refresh in the repair kernel
+        rng = np.random.default_rng(4)
+        base = O.round_to_bf16(rng.normal(size=(12, 64)))
+        x = dev(np.repeat(base, 200, axis=0)[rng.permutation(2400)][None])
+        starts = x[:, :40].float().contiguous()  # 40 starts for 12 distinct points
+        a, b = self.both(x, starts, iters=10)
+        self.same(a, b)
+        assert bool((a["sizes"] >= 1).all())
