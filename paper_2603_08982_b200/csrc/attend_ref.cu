@@ -239,7 +239,7 @@ int launch_attend(const SvgEarShape& s, int exec_mode, const bf16* qp, const bf1
   prep_centroids_kernel<<<dim3(ceil_div(ckpad * s.d, 256), s.bh), 256, 0, st>>>(
       kc, vc, k_sizes, s.d, s.c_k, ckpad, sc.kbar_bf16, sc.vbar_bf16, sc.lnw);
   SVG_LAUNCH_OK();
-  const int rows = exec_mode == SVGEAR_EXEC_FP32_CHECK ? 16 : 128;
+  const int rows = exec_mode == SVGEAR_EXEC_FP32_CHECK ? 16 : attend_tc_rows_per_tile();
   const int mt = AttendScratch::max_tiles(s.n_q, s.c_q, rows);
   build_tiles_kernel<<<s.bh, 1024, 0, st>>>(s.c_q, rows, mt, q_sizes, q_offsets, sc.tile_list,
                                             sc.tile_count);

@@ -8,17 +8,7 @@
 //     whose block is selected are masked to -inf (attention.py:130,146).
 // The output row is normalised once and scattered back to original token order.
 //
-// One CTA = one 128-row query tile of one query cluster (tile list built by build_tiles_kernel);
-// two CTAs are co-resident per SM (each: 256 TMEM columns, ~108 KB shared memory) so one CTA's
-// softmax overlaps the other's MMAs.
-//   warps 0-3 : softmax + epilogue, one thread per query row (TMEM lane == row)
-//   warp  4   : K producer   (cp.async gathers into the canonical SWIZZLE_128B layout)
-//   warp  5   : V producer
-//   warp  6   : TMEM allocator + single-thread tcgen05.mma issuer
-// TMEM columns: S0 [0,64)  S1 [64,128)  O [128,128+D).  P (bf16) overwrites its S buffer and is the
-// A operand of the P.V MMA straight from TMEM; S is double buffered so QK^T of tile t+1 runs while
-// the softmax of tile t is in flight.  The running maximum is only raised when it grows by more
-// than 2^8 (lazy rescale), which keeps the O accumulator in TMEM untouched on almost every tile.
+// Kernel structure: see the comment above attend_tc_kernel.
 #include "tc_common.cuh"
 
 namespace svg {
@@ -27,52 +17,99 @@ using namespace tc;
 
 namespace {
 
-constexpr int BM = 128;      // query rows per CTA
+constexpr int BM = 256;      // query rows per CTA: two M=128 halves that share every K/V tile
 constexpr int BN = 64;       // keys per tile
-constexpr int NTHREADS = 224;
+constexpr int NTHREADS = 384;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
-template <int D>
+template <int D, int NS>
 struct Smem {
   static constexpr int kQBytes = BM * D * 2;
   static constexpr int kTileBytes = BN * D * 2;
   static constexpr int kQ = 0;
-  static constexpr int kK = kQ + kQBytes;            // 2 stages
-  static constexpr int kV = kK + 2 * kTileBytes;     // 2 stages
-  static constexpr int kBars = kV + 2 * kTileBytes;  // 16 mbarriers + tmem ptr
-  static constexpr int kLists = kBars + 256;
+  static constexpr int kK = kQ + kQBytes;             // NS stages
+  static constexpr int kV = kK + NS * kTileBytes;     // NS stages
+  static constexpr int kBars = kV + NS * kTileBytes;  // mbarriers + tmem ptr + counters
+  static constexpr int kLists = kBars + 512;
   static size_t bytes(int ckpad) { return 1024 + kLists + (size_t)(ckpad + 64) * 12; }
 };
 
-enum { B_QFULL = 0, B_KFULL = 1, B_KEMPTY = 3, B_VFULL = 5, B_VEMPTY = 7, B_SFULL = 9, B_PFULL = 11, B_ODONE = 13 };
+// mbarrier indices
+template <int NS>
+struct Bars {
+  static constexpr int QFULL = 0;
+  static constexpr int KFULL = 1;              // [NS]
+  static constexpr int KEMPTY = KFULL + NS;    // [NS]
+  static constexpr int VFULL = KEMPTY + NS;    // [NS]
+  static constexpr int VEMPTY = VFULL + NS;    // [NS]
+  static constexpr int SFULL = VEMPTY + NS;    // [half][buffer]
+  static constexpr int PFULL = SFULL + 4;      // [half][buffer]
+  static constexpr int ODONE = PFULL + 4;      // [half]
+  static constexpr int COUNT = ODONE + 2;
+};
+
+// Tensor maps of one launch (passed as a __grid_constant__ kernel parameter).  K and V (permuted,
+// cluster-contiguous) are gathered as CONTIGUOUS ROW RUNS: a run is split into power-of-two row
+// boxes, box height 2^i rows x 64 columns, SWIZZLE_128B — the hardware writes the canonical UMMA
+// layout, a handful of bulk-tensor instructions replace 1024 16-byte cp.async gathers per tile.
+struct TmaSet {
+  CUtensorMap k[7];   // [bh*n_k][D] bf16, box {64 cols, 1<<i rows}
+  CUtensorMap v[7];
+  CUtensorMap kbar;   // [bh*ckpad][D] bf16, box {64, 64}
+  CUtensorMap vbar;
+  CUtensorMap q;      // [bh*n_q][D] bf16, box {64, 64}
+};
+
+// 2-D tiled bulk tensor load: box at (col, row) -> shared memory, completes tx bytes on `bar`
+__device__ __forceinline__ void tma_box(uint32_t dst, const CUtensorMap* tm, int col, int row, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(tm), "r"(col), "r"(row), "r"(bar)
+      : "memory");
+}
 
 }  // namespace
 
-template <int D>
-__global__ void __launch_bounds__(NTHREADS, 2)
-    attend_tc_kernel(const bf16* __restrict__ qp, const bf16* __restrict__ kp, const bf16* __restrict__ vp,
-                     const bf16* __restrict__ kbar, const bf16* __restrict__ vbar,
+// One CTA = up to 256 consecutive rows of one query cluster (tile list built by build_tiles_kernel),
+// one CTA per SM (512 TMEM columns).  Both 128-row halves see the same selected key clusters, so a
+// K/V tile is gathered into shared memory once and multiplied twice — half the L2->smem traffic of
+// one CTA per 128 rows, which is what bound the previous version.
+//   warps 0-3 : softmax + epilogue of half 0 (thread == query row, TMEM lane == row)
+//   warps 4-7 : same for half 1 (idle when the tile has <= 128 rows)
+//   warp  8   : K producer — cp.async gathers into the canonical SWIZZLE_128B layout, NS-stage ring,
+//               LAG tiles in flight
+//   warp  9   : Q tile, then V producer
+//   warps 10,11 : one elected tcgen05.mma issuer per half (warp 10 also allocates TMEM)
+// TMEM columns: S[half][buf] at half*128 + buf*64 (64 fp32 columns; P (bf16) overwrites the first 32
+// and is the A operand of P.V straight from TMEM), O[half] at 256 + half*D.  S is double buffered
+// per half, so QK^T of tile t+1 runs under the softmax of tile t; the two halves interleave on the
+// tensor pipe.  The running maximum is only raised when it grows by more than 2^8 (lazy rescale).
+template <int D, int NS>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    attend_tc_kernel(const __grid_constant__ TmaSet tm, int oob_row,
                      const float* __restrict__ lnw, const int32_t* __restrict__ q_perm,
                      const int32_t* __restrict__ k_sizes, const int32_t* __restrict__ k_offsets,
                      const uint8_t* __restrict__ mask, const int32_t* __restrict__ tile_list,
                      const int32_t* __restrict__ tile_count, int max_tiles, int n_q, int n_k, int c_q,
                      int c_k, int ckpad, float scale_log2e, bf16* __restrict__ out,
                      float* __restrict__ lse) {
-  using L = Smem<D>;
+  using L = Smem<D, NS>;
+  using B = Bars<NS>;
   const int h = blockIdx.y;
   if ((int)blockIdx.x >= tile_count[h]) return;
   const int32_t* te = tile_list + ((size_t)h * max_tiles + blockIdx.x) * 4;
   const int qcl = te[0], row0 = te[1], nrows = te[2];
+  const int halves = nrows > 128 ? 2 : 1;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sQ = sbase + L::kQ, sK = sbase + L::kK, sV = sbase + L::kV;
   const uint32_t bars = sbase + L::kBars;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kBars + 128);
-  int32_t* s_total = reinterpret_cast<int32_t*>(smem + L::kBars + 136);  // [0]=selected keys
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kBars + 384);
+  int32_t* s_total = reinterpret_cast<int32_t*>(smem + L::kBars + 392);  // [0]=selected keys
   int32_t* s_pre = reinterpret_cast<int32_t*>(smem + L::kLists);          // [nsel+1] key prefix
   int32_t* s_row = s_pre + (ckpad + 64);                                    // [nsel] first row
   float* s_bias = reinterpret_cast<float*>(s_row + (ckpad + 64));          // [ckpad] log2 domain
@@ -82,19 +119,22 @@ __global__ void __launch_bounds__(NTHREADS, 2)
 
   // ---- prologue: barriers, TMEM, per-cluster selection lists ------------------------------------
   if (tid == 0) {
-    mbar_init(bar(B_QFULL), 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(bar(B_KFULL + s), 1);
-      mbar_init(bar(B_KEMPTY + s), 1);
-      mbar_init(bar(B_VFULL + s), 1);
-      mbar_init(bar(B_VEMPTY + s), 1);
-      mbar_init(bar(B_SFULL + s), 1);
-      mbar_init(bar(B_PFULL + s), 128);
+    mbar_init(bar(B::QFULL), 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(bar(B::KFULL + s), 1);
+      mbar_init(bar(B::KEMPTY + s), halves);  // one commit per MMA issuer (half)
+      mbar_init(bar(B::VFULL + s), 1);
+      mbar_init(bar(B::VEMPTY + s), halves);
     }
-    mbar_init(bar(B_ODONE), 1);
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(bar(B::SFULL + s), 1);
+      mbar_init(bar(B::PFULL + s), 4);  // one elected lane per softmax warp
+    }
+    mbar_init(bar(B::ODONE), 1);
+    mbar_init(bar(B::ODONE + 1), 1);
     fence_barrier_init();
   }
-  if (warp == 6) tmem_alloc(smem_u32(tmem_slot), 256);
+  if (warp == 10) tmem_alloc(smem_u32(tmem_slot), 512);
   const uint8_t* mrow = mask + ((size_t)h * c_q + qcl) * c_k;
   if (warp == 0) {
     // compact the selected key clusters of this query cluster: (first row, key-count prefix)
@@ -123,8 +163,8 @@ __global__ void __launch_bounds__(NTHREADS, 2)
       s_total[0] = total;
       s_total[1] = nsel;
     }
-  } else if (warp >= 1 && warp <= 3) {
-    for (int j = tid - 32; j < ckpad; j += 96)
+  } else if (warp >= 1 && warp <= 7) {
+    for (int j = tid - 32; j < ckpad; j += 224)
       s_bias[j] = (j < c_k && mrow[j] == 0) ? lnw[(size_t)h * c_k + j] * kLog2e : -INFINITY;
   }
   tc_fence_before();
@@ -136,201 +176,271 @@ __global__ void __launch_bounds__(NTHREADS, 2)
   const int n_cent = ckpad / BN;
   const int T = n_exact + n_cent;
 
-  if (warp == 4 || warp == 5) {
-    // =========================== producers: K (warp 4) / V (warp 5) ===========================
-    const bool is_k = warp == 4;
-    const bf16* src_tok = (is_k ? kp : vp) + (size_t)h * n_k * D;
-    const bf16* src_cen = (is_k ? kbar : vbar) + (size_t)h * ckpad * D;
-    const uint32_t sbuf = is_k ? sK : sV;
-    const int b_full = is_k ? B_KFULL : B_VFULL, b_empty = is_k ? B_KEMPTY : B_VEMPTY;
-    constexpr int CPR = D / 8;          // 16-byte chunks per row
-    constexpr int RPI = 32 / CPR;       // rows covered by one warp-wide cp.async
-    const int sub = lane / CPR, chunk = lane % CPR;
-    if (is_k) {
-      // Q tile first (contiguous rows of the permuted Q, clamped at the end of the instance)
-      const bf16* qsrc = qp + (size_t)h * n_q * D;
-      for (int r0 = 0; r0 < BM; r0 += RPI) {
-        const int r = r0 + sub;
-        const int row = min(row0 + r, n_q - 1);
-        cp_async16(sQ + (uint32_t)((chunk >> 3) * (BM * 128)) + swz(r, chunk & 7),
-                   qsrc + (size_t)row * D + chunk * 8);
-      }
-      cp_async_commit();
-      cp_async_wait_all();
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar(B_QFULL));
-    }
-    uint32_t xo[8 / RPI];  // ((chunk & 7) ^ (row & 7)) << 4 for the 8/RPI row phases of this lane
-#pragma unroll
-    for (int j = 0; j < 8 / RPI; ++j) xo[j] = (uint32_t)(((chunk & 7) ^ ((j * RPI + sub) & 7)) << 4);
-    int cur0 = 0, cur1 = 0;  // cursors into the selection list for slots lane and lane+32
-    const int last_key = max(total_keys - 1, 0);
-    for (int t = 0; t < T; ++t) {
-      const int st = t & 1;
-      if (t >= 2) mbar_wait(bar(b_empty + st), ((t >> 1) + 1) & 1);
-      // source row of tile slots `lane` and `lane + 32`
-      const bf16* base;
-      int r_lo, r_hi;
-      if (t < n_exact) {
-        base = src_tok;
-        int u0 = min(t * BN + lane, last_key), u1 = min(t * BN + lane + 32, last_key);
-        while (s_pre[cur0 + 1] <= u0) ++cur0;
-        if (cur1 < cur0) cur1 = cur0;
-        while (s_pre[cur1 + 1] <= u1) ++cur1;
-        r_lo = s_row[cur0] + (u0 - s_pre[cur0]);
-        r_hi = s_row[cur1] + (u1 - s_pre[cur1]);
-      } else {
-        base = src_cen;
-        r_lo = (t - n_exact) * BN + lane;
-        r_hi = r_lo + 32;
-      }
-      // lane-constant parts of the swizzled destination: the XOR pattern repeats every 8 rows
-      const uint32_t dst = sbuf + (uint32_t)st * L::kTileBytes + (uint32_t)((chunk >> 3) * (BN * 128)) +
-                           (uint32_t)(sub * 128);
-      const char* src = reinterpret_cast<const char*>(base) + chunk * 16;
-#pragma unroll
-      for (int r0 = 0; r0 < BN; r0 += RPI) {
-        const int srow = __shfl_sync(0xffffffffu, r0 < 32 ? r_lo : r_hi, (r0 & 31) + sub);
-        cp_async16(dst + (uint32_t)(r0 * 128) + xo[(r0 / RPI) % (8 / RPI)], src + (size_t)srow * (D * 2));
-      }
-      cp_async_commit();
-      cp_async_wait_all();
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar(b_full + st));
-    }
-  } else if (warp == 6) {
-    // =========================== MMA issuer (one elected thread) ===============================
+  if (warp == 8 || warp == 9) {
+    // =========================== producers: K (warp 8) / Q then V (warp 9), one elected thread ===
+    const bool is_k = warp == 8;
     if (elect_one()) {
-      constexpr uint32_t idesc_qk = make_idesc(BM, BN, 0);
-      constexpr uint32_t idesc_pv = make_idesc(BM, D, 1);
-      const uint32_t tS[2] = {tmem, tmem + 64};
-      const uint32_t tO = tmem + 128;
+      const CUtensorMap* maps = is_k ? tm.k : tm.v;
+      const CUtensorMap* cmap = is_k ? &tm.kbar : &tm.vbar;
+      const uint32_t sbuf = is_k ? sK : sV;
+      const int b_full = is_k ? B::KFULL : B::VFULL, b_empty = is_k ? B::KEMPTY : B::VEMPTY;
+      constexpr int SLABS = D / 64;  // 64-column (128-byte) slabs of a row
+      if (!is_k) {
+        // Q tile: rows row0.. of the permuted Q (rows past the tile belong to the next cluster or are
+        // zero-filled past the end of the array; they are computed but never stored)
+        mbar_expect_tx(bar(B::QFULL), (uint32_t)(halves * 128 * D * 2));
+        for (int hf = 0; hf < halves; ++hf)
+          for (int sl = 0; sl < SLABS; ++sl)
+            for (int rb = 0; rb < 2; ++rb)
+              tma_box(sQ + (uint32_t)(hf * (128 * D * 2) + sl * (128 * 128) + rb * (64 * 128)), &tm.q, sl * 64,
+                      h * n_q + row0 + hf * 128 + rb * 64, bar(B::QFULL));
+      }
+      int cur = 0;  // cursor into the selection list
+      const int rowbase = h * n_k;
+      for (int t = 0; t < T; ++t) {
+        const int st = t % NS;
+        if (t >= NS) mbar_wait(bar(b_empty + st), ((t / NS) - 1) & 1);
+        const uint32_t dst = sbuf + (uint32_t)st * L::kTileBytes;
+        const uint32_t fb = bar(b_full + st);
+        mbar_expect_tx(fb, (uint32_t)L::kTileBytes);
+        if (t < n_exact) {
+          int u = t * BN;
+          const int uend = min(u + BN, total_keys);
+          while (u < uend) {
+            while (s_pre[cur + 1] <= u) ++cur;
+            int len = min(s_pre[cur + 1], uend) - u;
+            int src = rowbase + s_row[cur] + (u - s_pre[cur]);
+            while (len > 0) {  // largest power-of-two box first
+              const int b = 31 - __clz(len), nb = 1 << b;
+              const uint32_t d0 = dst + (uint32_t)((u - t * BN) * 128);
+#pragma unroll
+              for (int sl = 0; sl < SLABS; ++sl) tma_box(d0 + (uint32_t)(sl * (BN * 128)), maps + b, sl * 64, src, fb);
+              u += nb;
+              src += nb;
+              len -= nb;
+            }
+          }
+          // ragged last tile: the remaining slots are filled with zeros (out-of-bounds boxes); their
+          // logits are masked to -inf, and 0 * finite keeps the P.V accumulation clean
+          int slot = uend - t * BN, pad = BN - slot;
+          while (pad > 0) {
+            const int b = 31 - __clz(pad), nb = 1 << b;
+#pragma unroll
+            for (int sl = 0; sl < SLABS; ++sl)
+              tma_box(dst + (uint32_t)(slot * 128 + sl * (BN * 128)), maps + b, sl * 64, oob_row, fb);
+            slot += nb;
+            pad -= nb;
+          }
+        } else {
+#pragma unroll
+          for (int sl = 0; sl < SLABS; ++sl)
+            tma_box(dst + (uint32_t)(sl * (BN * 128)), cmap, sl * 64, h * ckpad + (t - n_exact) * BN, fb);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 10) {
+    // =========================== MMA issuers: warp 10 -> half 0, warp 11 -> half 1 =============
+    // One elected thread per half runs its own QK^T / P.V sequence, so a barrier round trip of one
+    // half never stalls the other half's MMAs; K/V stages are released by both (count = halves).
+    const int hf = warp - 10;
+    if (hf < halves && elect_one()) {
+      constexpr uint32_t idesc_qk = make_idesc(128, BN, 0);
+      constexpr uint32_t idesc_pv = make_idesc(128, D, 1);
+      const uint32_t qb = sQ + (uint32_t)(hf * (128 * D * 2));
+      const uint32_t tSb = tmem + (uint32_t)(hf * 128);
+      const uint32_t tO = tmem + (uint32_t)(256 + hf * D);
       auto issue_qk = [&](int t) {
-        const int st = t & 1;
-        mbar_wait(bar(B_KFULL + st), (t >> 1) & 1);
+        const int st = t % NS;
+        mbar_wait(bar(B::KFULL + st), (t / NS) & 1);
         tc_fence_after();
         const uint32_t kb = sK + (uint32_t)st * L::kTileBytes;
+        const uint32_t tS = tSb + (uint32_t)((t & 1) * 64);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t ad = make_desc(sQ + (uint32_t)((kk >> 2) * (BM * 128) + (kk & 3) * 32), 16, 1024);
+          const uint64_t ad = make_desc(qb + (uint32_t)((kk >> 2) * (128 * 128) + (kk & 3) * 32), 16, 1024);
           const uint64_t bd = make_desc(kb + (uint32_t)((kk >> 2) * (BN * 128) + (kk & 3) * 32), 16, 1024);
-          umma_ss(tS[st], ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
+          umma_ss(tS, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
         }
-        umma_commit(bar(B_SFULL + st));
-        umma_commit(bar(B_KEMPTY + st));
+        umma_commit(bar(B::SFULL + hf * 2 + (t & 1)));
+        umma_commit(bar(B::KEMPTY + st));
       };
-      mbar_wait(bar(B_QFULL), 0);
+      mbar_wait(bar(B::QFULL), 0);
+      // stagger the halves by one softmax pass so that the two softmax warps of an SM sub-partition
+      // are not in their exponential phase (or in their hand-off gap) at the same time
+      if (hf == 1) mbar_wait(bar(B::PFULL + 0), 0);
       issue_qk(0);
       for (int t = 0; t < T; ++t) {
-        const int st = t & 1;
+        const int st = t % NS;
         if (t + 1 < T) issue_qk(t + 1);
-        mbar_wait(bar(B_VFULL + st), (t >> 1) & 1);
-        mbar_wait(bar(B_PFULL + st), (t >> 1) & 1);
+        mbar_wait(bar(B::VFULL + st), (t / NS) & 1);
+        mbar_wait(bar(B::PFULL + hf * 2 + (t & 1)), (t >> 1) & 1);
         tc_fence_after();
         const uint32_t vb = sV + (uint32_t)st * L::kTileBytes;
+        const uint32_t tP = tSb + (uint32_t)((t & 1) * 64);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
           // V tile [64 keys x D] is the MN-major B operand: 16 keys per MMA = 2048 B along K,
           // LBO = stride between the 64-column slabs, SBO = stride between 8-key groups
           const uint64_t bd = make_desc(vb + (uint32_t)(kk * 2048), BN * 128, 1024);
-          umma_ts(tO, tS[st] + (uint32_t)(kk * 8), bd, idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
+          umma_ts(tO, tP + (uint32_t)(kk * 8), bd, idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit(bar(B_VEMPTY + st));
-        umma_commit(bar(B_ODONE));
+        umma_commit(bar(B::ODONE + hf));
+        umma_commit(bar(B::VEMPTY + st));
       }
     }
     __syncwarp();
-  } else {
-    // =========================== softmax + epilogue (warps 0-3, thread == row) ==================
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    const uint32_t tS[2] = {tmem + lane_base, tmem + lane_base + 64};
-    const uint32_t tO = tmem + lane_base + 128;
+  } else if ((warp >> 2) < halves) {
+    // =========================== softmax + epilogue (warps 0-7, thread == row) ==================
+    const int hf = warp >> 2;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tSb = tmem + lane_base + (uint32_t)(hf * 128);
+    const uint32_t tO = tmem + lane_base + (uint32_t)(256 + hf * D);
+    const int b_sfull = B::SFULL + hf * 2, b_pfull = B::PFULL + hf * 2, b_odone = B::ODONE + hf;
     float m = -INFINITY, l = 0.f;
+    // The S tile is consumed as two 32-column blocks; the TMEM load of the next block is always in
+    // flight under the arithmetic of the current one (TMEM reads run at 64 B/clk/SM, as long as the
+    // MMAs of the tile).  Exponentials are taken SPECULATIVELY against the running maximum m; the
+    // block maxima are collected on the side and, only if some row of the warp has to raise m
+    // (tile max > m + 2^8, rare after the first tiles), the tile is redone from TMEM the exact way.
+    uint32_t sa[32], sb[32], pk[32];
+    const int last_valid = total_keys - (n_exact - 1) * BN;  // valid columns of the last exact tile
+    mbar_wait(bar(b_sfull), 0);
+    tc_fence_after();
+    TMEM_LD32(tSb, sa);
     for (int t = 0; t < T; ++t) {
       const int st = t & 1;
-      mbar_wait(bar(B_SFULL + st), (t >> 1) & 1);
-      tc_fence_after();
-      uint32_t sa[32], sb[32];
-      TMEM_LD32(tS[st], sa);
-      TMEM_LD32(tS[st] + 32, sb);
-      tc_wait_ld();
-      float mt = -INFINITY;
-      float cmul = 1.f;  // multiplier still to be applied to sa/sb inside the exponential
-      if (t < n_exact - 1) {
-        // full exact tile: keep the raw logits, fold the scale into the exp2 FFMA below
+      const uint32_t tS = tSb + (uint32_t)(st * 64);
+      // tile kind: 0 = full exact tile (raw logits), 1 = last exact tile (ragged), 2 = centroid tile
+      const int kind = t < n_exact - 1 ? 0 : (t < n_exact ? 1 : 2);
+      const float* bias = s_bias + (kind == 2 ? (t - n_exact) * BN : 0);
+      const float mu = (m == -INFINITY) ? 0.f : m;
+      float sum0 = 0.f, sum1 = 0.f, sum2 = 0.f, sum3 = 0.f;
+      float x0 = -INFINITY, x1 = -INFINITY, x2 = -INFINITY, x3 = -INFINITY;  // block maxima (log2 domain)
+      tc_wait_ld();                 // sa = columns 0-31 of tile t
+      TMEM_LD32(tS + 32, sb);       // columns 32-63 load under the arithmetic on sa
+      auto block = [&](uint32_t(&v)[32], int col0, int pk0) {
+        if (kind == 0) {
+          // half of the exponentials go to the MUFU, half to the FMA pipe (packed polynomial): the
+          // MUFU alone (16/clk/SM) would need as long as the tile's MMAs
+          const uint64_t sc2 = pack2(scale_log2e, scale_log2e), nm2 = pack2(-mu, -mu);
+          uint64_t acc01 = pack2(0.f, 0.f), acc23 = pack2(0.f, 0.f);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) mt = fmaxf(mt, fmaxf(__uint_as_float(sa[j]), __uint_as_float(sb[j])));
-        mt *= scale_log2e;
-        cmul = scale_log2e;
-      } else if (t < n_exact) {
-        const int valid = total_keys - t * BN;  // 1..64 valid columns in the last exact tile
+          for (int j = 0; j < 32; j += 4) {
+            const float v0 = __uint_as_float(v[j]), v1 = __uint_as_float(v[j + 1]);
+            const float v2 = __uint_as_float(v[j + 2]), v3 = __uint_as_float(v[j + 3]);
+            x0 = fmaxf(x0, fmaxf(v0, v1));
+            x1 = fmaxf(x1, fmaxf(v2, v3));
+            float a0, a1, p0, p1, p2, p3;
+            unpack2(ffma2(pack2(v0, v1), sc2, nm2), a0, a1);
+            p0 = ex2(a0);
+            p1 = ex2(a1);
+            exp2_poly2(ffma2(pack2(v2, v3), sc2, nm2), p2, p3);
+            acc01 = fadd2(acc01, pack2(p0, p1));
+            acc23 = fadd2(acc23, pack2(p2, p3));
+            pk[pk0 + j / 2] = pack_bf16x2(p0, p1);
+            pk[pk0 + j / 2 + 1] = pack_bf16x2(p2, p3);
+          }
+          float s0, s1, s2, s3;
+          unpack2(acc01, s0, s1);
+          unpack2(acc23, s2, s3);
+          sum0 += s0 + s1;
+          sum1 += s2 + s3;
+        } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float x = j < valid ? __uint_as_float(sa[j]) * scale_log2e : -INFINITY;
-          float y = j + 32 < valid ? __uint_as_float(sb[j]) * scale_log2e : -INFINITY;
-          sa[j] = __float_as_uint(x);
-          sb[j] = __float_as_uint(y);
-          mt = fmaxf(mt, fmaxf(x, y));
+          for (int j = 0; j < 32; j += 2) {
+            float b0, b1;
+            if (kind == 2) {
+              b0 = bias[col0 + j];
+              b1 = bias[col0 + j + 1];
+            } else {
+              b0 = col0 + j < last_valid ? 0.f : -INFINITY;
+              b1 = col0 + j + 1 < last_valid ? 0.f : -INFINITY;
+            }
+            const float v0 = fmaf(__uint_as_float(v[j]), scale_log2e, b0);
+            const float v1 = fmaf(__uint_as_float(v[j + 1]), scale_log2e, b1);
+            x2 = fmaxf(x2, fmaxf(v0, v1));
+            const float p0 = ex2(v0 - mu), p1 = ex2(v1 - mu);
+            sum2 += p0 + p1;
+            pk[pk0 + j / 2] = pack_bf16x2(p0, p1);
+          }
         }
-      } else {
-        const float* bias = s_bias + (t - n_exact) * BN;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          float x = fmaf(__uint_as_float(sa[j]), scale_log2e, bias[j]);
-          float y = fmaf(__uint_as_float(sb[j]), scale_log2e, bias[j + 32]);
-          sa[j] = __float_as_uint(x);
-          sb[j] = __float_as_uint(y);
-          mt = fmaxf(mt, fmaxf(x, y));
-        }
+      };
+      block(sa, 0, 0);
+      tc_wait_ld();                 // sb landed
+      // first block of the next tile: prefetch it under the arithmetic on sb if S(t+1) is already
+      // there (warp-uniform decision), otherwise right after this block
+      bool fetched = t + 1 >= T;
+      if (!fetched && __all_sync(0xffffffffu, mbar_test(bar(b_sfull + (st ^ 1)), ((t + 1) >> 1) & 1))) {
+        tc_fence_after();
+        TMEM_LD32(tSb + (uint32_t)((st ^ 1) * 64), sa);
+        fetched = true;
       }
+      block(sb, 32, 16);
+      float mt = kind == 0 ? fmaxf(x0, x1) * scale_log2e : fmaxf(x2, x3);
+      float sum = (sum0 + sum1) + (sum2 + sum3);
       // lazy running max: only move it when it grows by more than 2^kRescaleThreshold
       float alpha = 1.f;
       const bool bump = mt > m + kRescaleThreshold || (m == -INFINITY && mt > -INFINITY);
-      if (bump) {
-        alpha = ex2(m - mt);  // m = -inf -> 0
-        m = mt;
-      }
-      const float mu = (m == -INFINITY) ? 0.f : m;
-      float sum = 0.f;
-      uint32_t pk[32];
+      const bool redo = __any_sync(0xffffffffu, bump);
+      if (redo) {
+        // exact path for the whole warp: raise m where needed and take the exponentials again
+        if (bump) {
+          alpha = ex2(m - mt);  // m = -inf -> 0
+          m = mt;
+        }
+        const float mu2 = (m == -INFINITY) ? 0.f : m;
+        tc_wait_ld();  // keep the prefetched block of tile t+1 intact in sa
+        sum = 0.f;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        float p0 = ex2(fmaf(__uint_as_float(sa[2 * j]), cmul, -mu)), p1 = ex2(fmaf(__uint_as_float(sa[2 * j + 1]), cmul, -mu));
-        sum += p0 + p1;
-        pk[j] = pack_bf16x2(p0, p1);
-      }
+        for (int half = 0; half < 2; ++half) {
+          TMEM_LD32(tS + half * 32, sb);
+          tc_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        float p0 = ex2(fmaf(__uint_as_float(sb[2 * j]), cmul, -mu)), p1 = ex2(fmaf(__uint_as_float(sb[2 * j + 1]), cmul, -mu));
-        sum += p0 + p1;
-        pk[16 + j] = pack_bf16x2(p0, p1);
+          for (int j = 0; j < 32; j += 2) {
+            float v0 = __uint_as_float(sb[j]) * scale_log2e, v1 = __uint_as_float(sb[j + 1]) * scale_log2e;
+            if (kind == 2) {
+              v0 += bias[half * 32 + j];
+              v1 += bias[half * 32 + j + 1];
+            } else if (kind == 1) {
+              if (half * 32 + j >= last_valid) v0 = -INFINITY;
+              if (half * 32 + j + 1 >= last_valid) v1 = -INFINITY;
+            }
+            const float p0 = ex2(v0 - mu2), p1 = ex2(v1 - mu2);
+            sum += p0 + p1;
+            pk[half * 16 + j / 2] = pack_bf16x2(p0, p1);
+          }
+        }
       }
       l = l * alpha + sum;
-      TMEM_ST32(tS[st], pk);  // P (bf16 pairs) over the first 32 columns of this S buffer
-      if (t > 0 && __any_sync(0xffffffffu, bump)) {
+      TMEM_ST32(tS, pk);  // P (bf16 pairs) over the first 32 columns of this S buffer
+      if (redo && t > 0) {
         // rescale the O accumulator; P.V of tile t-1 must have landed first
-        mbar_wait(bar(B_ODONE), (t - 1) & 1);
+        mbar_wait(bar(b_odone), (t - 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < D; c += 32) {
-          uint32_t o[32];
-          TMEM_LD32(tO + c, o);
+          TMEM_LD32(tO + c, sb);
           tc_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-          TMEM_ST32(tO + c, o);
+          for (int j = 0; j < 32; ++j) sb[j] = __float_as_uint(__uint_as_float(sb[j]) * alpha);
+          TMEM_ST32(tO + c, sb);
         }
       }
       tc_wait_st();
       tc_fence_before();
-      mbar_arrive(bar(B_PFULL + st));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(b_pfull + st));
+      if (!fetched) {
+        mbar_wait(bar(b_sfull + (st ^ 1)), ((t + 1) >> 1) & 1);
+        tc_fence_after();
+        TMEM_LD32(tSb + (uint32_t)((st ^ 1) * 64), sa);
+      }
     }
     // ---- epilogue: O / l -> bf16 -> global, scattered to original token order -----------------
-    mbar_wait(bar(B_ODONE), (T - 1) & 1);
+    mbar_wait(bar(b_odone), (T - 1) & 1);
     tc_fence_after();
-    const int r = tid;
+    const int r = tid;  // row within the CTA tile (warps 0-7 <-> rows 0-255)
     const bool live = r < nrows;
     const int prow = min(row0 + r, n_q - 1);
     const int dst = q_perm ? q_perm[(size_t)h * n_q + prow] : prow;
@@ -357,10 +467,49 @@ __global__ void __launch_bounds__(NTHREADS, 2)
     tc_fence_before();
   }
   __syncthreads();
-  if (warp == 6) {
+  if (warp == 10) {
     tc_fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, 512);
   }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// [rows][d] bf16 row-major, box = 64 columns x box_rows rows, SWIZZLE_128B, zero fill out of bounds
+static bool encode_rows_map(CUtensorMap* tm, const void* base, uint64_t rows, int d, int box_rows) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) != cudaSuccess || !p) {
+      (void)cudaGetLastError();
+      return false;
+    }
+    fn = (EncodeTiledFn)p;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)d, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int D, int NS>
+static int launch_attend_tc_ns(const SvgEarShape& s, const TmaSet& tm, const int32_t* q_perm,
+                               const int32_t* k_sizes, const int32_t* k_offsets, const uint8_t* mask, bf16* out,
+                               float* lse, AttendScratch& sc, int ckpad, int mt, float scale_log2e,
+                               cudaStream_t st) {
+  const size_t smem = Smem<D, NS>::bytes(ckpad);
+  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  attend_tc_kernel<D, NS><<<dim3(mt, s.bh), NTHREADS, smem, st>>>(
+      tm, s.bh * s.n_k, sc.lnw, q_perm, k_sizes, k_offsets, mask, sc.tile_list, sc.tile_count, mt, s.n_q, s.n_k,
+      s.c_q, s.c_k, ckpad, scale_log2e, out, lse);
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
 }
 
 int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const bf16* vp,
@@ -369,25 +518,32 @@ int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const
   const int ckpad = ceil_div(s.c_k, 64) * 64;
   const int mt = AttendScratch::max_tiles(s.n_q, s.c_q, BM);
   const float scale_log2e = kLog2e / sqrtf((float)s.d);
-  if (s.d == 128) {
-    const size_t smem = Smem<128>::bytes(ckpad);
-    if (smem > 227 * 1024) return SVGEAR_EUNSUPPORTED;
-    SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    attend_tc_kernel<128><<<dim3(mt, s.bh), NTHREADS, smem, st>>>(
-        qp, kp, vp, sc.kbar_bf16, sc.vbar_bf16, sc.lnw, q_perm, k_sizes, k_offsets, mask, sc.tile_list,
-        sc.tile_count, mt, s.n_q, s.n_k, s.c_q, s.c_k, ckpad, scale_log2e, out, lse);
-  } else {
-    const size_t smem = Smem<64>::bytes(ckpad);
-    if (smem > 227 * 1024) return SVGEAR_EUNSUPPORTED;
-    SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    attend_tc_kernel<64><<<dim3(mt, s.bh), NTHREADS, smem, st>>>(
-        qp, kp, vp, sc.kbar_bf16, sc.vbar_bf16, sc.lnw, q_perm, k_sizes, k_offsets, mask, sc.tile_list,
-        sc.tile_count, mt, s.n_q, s.n_k, s.c_q, s.c_k, ckpad, scale_log2e, out, lse);
+  if ((long long)s.bh * s.n_k >= (1ll << 31) - 64 || (long long)s.bh * s.n_q >= (1ll << 31) - 512)
+    return SVGEAR_EUNSUPPORTED;  // TMA row coordinates are int32
+  TmaSet tm;
+  bool ok = true;
+  for (int i = 0; i < 7; ++i) {
+    ok = ok && encode_rows_map(&tm.k[i], kp, (uint64_t)s.bh * s.n_k, s.d, 1 << i);
+    ok = ok && encode_rows_map(&tm.v[i], vp, (uint64_t)s.bh * s.n_k, s.d, 1 << i);
   }
-  SVG_LAUNCH_OK();
-  return SVGEAR_OK;
+  ok = ok && encode_rows_map(&tm.kbar, sc.kbar_bf16, (uint64_t)s.bh * ckpad, s.d, 64);
+  ok = ok && encode_rows_map(&tm.vbar, sc.vbar_bf16, (uint64_t)s.bh * ckpad, s.d, 64);
+  ok = ok && encode_rows_map(&tm.q, qp, (uint64_t)s.bh * s.n_q, s.d, 64);
+  if (!ok) return SVGEAR_ECUDA;
+  const size_t cap = 227 * 1024;
+#define SVG_TRY(DD, NSS)                                                                                 \
+  if (s.d == DD && Smem<DD, NSS>::bytes(ckpad) <= cap)                                                   \
+    return launch_attend_tc_ns<DD, NSS>(s, tm, q_perm, k_sizes, k_offsets, mask, out, lse, sc, ckpad, mt, \
+                                        scale_log2e, st);
+  SVG_TRY(128, 4)
+  SVG_TRY(128, 3)
+  SVG_TRY(128, 2)
+  SVG_TRY(64, 4)
+  SVG_TRY(64, 2)
+#undef SVG_TRY
+  return SVGEAR_EUNSUPPORTED;
 }
+
+int attend_tc_rows_per_tile() { return BM; }
 
 }  // namespace svg

@@ -160,6 +160,7 @@ int launch_attend(const SvgEarShape& s, int exec_mode, const bf16* qp, const bf1
                   const float* kc, const float* vc, const uint8_t* mask, void* out, float* lse,
                   AttendScratch& sc, cudaStream_t st);
 // tcgen05 path (attend_tc.cu)
+int attend_tc_rows_per_tile();
 int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const bf16* vp,
                      const int32_t* q_perm, const int32_t* k_sizes, const int32_t* k_offsets,
                      const uint8_t* mask, bf16* out, float* lse, AttendScratch& sc,

@@ -46,6 +46,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "}" ::"r"(bar), "r"(parity)
       : "memory");
 }
+// non-blocking phase test
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t"
+      "}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // One lane of a converged warp (elect.sync).  Unlike `lane == 0`, the compiler knows that exactly
 // one thread is active behind this predicate, so tcgen05 operands move to uniform registers with
 // plain R2URs instead of a per-instruction ELECT / R2UR.BROADCAST / BRA.U.ANY waterfall loop.
@@ -145,6 +159,48 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// ---- packed fp32x2 arithmetic (sm_100: one issue slot for two lanes of a 64-bit register pair) ----
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void unpack2(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^x for a PAIR of arguments on the FMA pipe (no MUFU): round-to-nearest split x = r + f with the
+// 1.5*2^23 magic constant, degree-3 minimax polynomial for 2^f on [-0.5, 0.5] (max relative error
+// 7.6e-5, well below the bf16 rounding of P), exponent patched in with one integer shift-add per
+// lane.  Arguments are clamped at -126; callers guarantee x <= ~2^7.
+__device__ __forceinline__ void exp2_poly2(uint64_t x01, float& p0, float& p1) {
+  float x0, x1;
+  unpack2(x01, x0, x1);
+  const uint64_t xc = pack2(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t magic = pack2(12582912.f, 12582912.f), nmagic = pack2(-12582912.f, -12582912.f);
+  const uint64_t t = fadd2(xc, magic);
+  const uint64_t r = fadd2(t, nmagic);
+  const uint64_t f = ffma2(r, pack2(-1.f, -1.f), xc);
+  uint64_t p = ffma2(f, pack2(0.0552055052f, 0.0552055052f), pack2(0.242613964f, 0.242613964f));
+  p = ffma2(p, f, pack2(0.693254762f, 0.693254762f));
+  p = ffma2(p, f, pack2(0.999927725f, 0.999927725f));
+  float q0, q1, t0, t1;
+  unpack2(p, q0, q1);
+  unpack2(t, t0, t1);
+  p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
+  p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
 }
 
 // shared-memory matrix descriptor, SWIZZLE_128B (cute::UMMA::SmemDescriptor: start>>4 [0,14),
