@@ -333,7 +333,7 @@ def run_ours(args):
 def stage_times(torch, P, _lib, q, k, v, cq, ck, args, reps):
     """Run the layer through the STAGED C-ABI entry points (same kernels as svgear_forward) with
     CUDA events between stages.  Returns ({stage: ms}, attention algorithmic FLOPs, density, iters)."""
-    from paper_2603_08982_b200.clustering import ClusterModel, device_start, run_lloyd, strided_start
+    from paper_2603_08982_b200.clustering import ClusterModel, device_start_pair, run_lloyd, strided_start
     from paper_2603_08982_b200 import router as R
 
     qb, kb, vb = q[0], k[0], v[0]
@@ -347,7 +347,7 @@ def stage_times(torch, P, _lib, q, k, v, cq, ck, args, reps):
         def mark(name):
             e = ev(); e.record(); marks.append((name, e))
         if args.init == "device":
-            qi, ki = device_start(qb, cq, 0), device_start(kb, ck, 0x9E37)
+            qi, ki = device_start_pair(qb, cq, kb, ck, 0)
         else:
             qi, ki = strided_start(qb, cq), strided_start(kb, ck)
         mark("kmeans_seed")

@@ -68,19 +68,25 @@ def strided_start(tokens, k):
     return tokens.index_select(-2, idx).float().contiguous()
 
 
-def device_start(tokens, k, seed=0, oversample=8, gram=True):
-    """Device-side k-means++ start on a strided subsample (svgear_kmeans_seed).  Deterministic, but
-    NOT the reference's numpy draw — use `seeded_start` / init="reference" for parity runs."""
+def _seed_inputs(tokens, k, oversample):
+    """Output buffer and (when the subsample can hold k centres) the Gram matrix of the strided
+    subsample — one plain batched library GEMM (bf16 in, bf16 out)."""
     x = tokens if tokens.ndim == 3 else tokens.unsqueeze(0)
     x = x.contiguous()
     bh, n, d = x.shape
     out = torch.empty((bh, k, d), dtype=torch.float32, device=x.device)
     m = min(n, int(oversample) * k, 4096)
-    if gram and m >= k:
-        # Gram matrix of the strided subsample: one plain batched library GEMM (bf16 in, bf16 out)
+    g = None
+    if m >= k:
         idx = torch.div(torch.arange(m, device=x.device, dtype=torch.int64) * n, m, rounding_mode="floor")
         xs = x.index_select(1, idx)
         g = torch.bmm(xs, xs.transpose(1, 2)).contiguous()
+    return x, out, g, m
+
+
+def _seed_launch(x, out, g, m, k, seed, oversample):
+    bh, n, d = x.shape
+    if g is not None:
         rc = _lib.lib().svgear_kmeans_seed_gram(bh, n, d, k, m, x.data_ptr(), g.data_ptr(),
                                                 int(seed) & 0xFFFFFFFF, out.data_ptr(), stream_ptr())
         _lib.check("svgear_kmeans_seed_gram", rc)
@@ -88,7 +94,37 @@ def device_start(tokens, k, seed=0, oversample=8, gram=True):
         rc = _lib.lib().svgear_kmeans_seed(bh, n, d, k, x.data_ptr(), int(oversample), int(seed) & 0xFFFFFFFF,
                                            out.data_ptr(), stream_ptr())
         _lib.check("svgear_kmeans_seed", rc)
+
+
+def device_start(tokens, k, seed=0, oversample=8, gram=True):
+    """Device-side k-means++ start on a strided subsample (svgear_kmeans_seed).  Deterministic, but
+    NOT the reference's numpy draw — use `seeded_start` / init="reference" for parity runs."""
+    x, out, g, m = _seed_inputs(tokens, k, oversample)
+    _seed_launch(x, out, g if gram else None, m, k, seed, oversample)
     return out if tokens.ndim == 3 else out[0]
+
+
+_SIDE_STREAMS = {}
+
+
+def device_start_pair(q, c_q, k, c_k, seed=0, oversample=8):
+    """device_start for the query and the key side with the two seeding KERNELS on two streams:
+    each runs one CTA per instance (c sequential D^2 rounds), so the sides overlap on disjoint SMs.
+    Every tensor is allocated on the current stream; the helper stream only carries one kernel and
+    is joined before returning."""
+    xq, oq, gq, mq = _seed_inputs(q, c_q, oversample)
+    xk, ok, gk, mk = _seed_inputs(k, c_k, oversample)
+    dev = xq.device
+    cur = torch.cuda.current_stream(dev)
+    side = _SIDE_STREAMS.get(dev.index)
+    if side is None:
+        side = _SIDE_STREAMS[dev.index] = torch.cuda.Stream(device=dev)
+    side.wait_stream(cur)
+    with torch.cuda.stream(side):
+        _seed_launch(xk, ok, gk, mk, c_k, seed + 0x9E37, oversample)
+    _seed_launch(xq, oq, gq, mq, c_q, seed, oversample)
+    cur.wait_stream(side)
+    return (oq if q.ndim == 3 else oq[0]), (ok if k.ndim == 3 else ok[0])
 
 
 def _pad_centers(tok_f32, centers, k):

@@ -1,5 +1,7 @@
 // extern "C" entry points of libsvgear.so (declared in include/svgear.h).
 #include <math.h>
+
+#include <mutex>
 #include <string.h>
 
 #include "common.cuh"
@@ -24,7 +26,8 @@ bool shape_ok(const SvgEarShape* s) {
 // Everything svgear_forward keeps in the workspace.  The same routine sizes (base == nullptr) and
 // carves it, so the two can never disagree.
 struct ForwardPlan {
-  KmeansScratch km;  // shared by both sides (sized for the larger)
+  KmeansScratch km;   // query side (also what svgear_kmeans alone uses)
+  KmeansScratch km2;  // key side: the two Lloyd loops run concurrently on two streams
   AttendScratch at;
   ErrScratch es;
   int32_t *q_assign, *k_assign, *q_perm, *k_perm, *q_sizes, *k_sizes, *q_offsets, *k_offsets;
@@ -40,6 +43,7 @@ bool plan_forward(const SvgEarShape& s, Carver& cv, ForwardPlan& p) {
   const int nmax = s.n_q > s.n_k ? s.n_q : s.n_k;
   const int cmax = s.c_q > s.c_k ? s.c_q : s.c_k;
   p.km.carve(cv, s.bh, nmax, cmax, s.d);
+  p.km2.carve(cv, s.bh, s.n_k, s.c_k, s.d);
   p.at.carve(cv, s);
   p.q_assign = cv.take<int32_t>((size_t)s.bh * s.n_q);
   p.k_assign = cv.take<int32_t>((size_t)s.bh * s.n_k);
@@ -290,21 +294,43 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
   int64_t* entries = a.mask_entries ? a.mask_entries : p.entries;
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
-  // (1) cluster Q and K independently; V follows K (analysis.py:228-238)
-  rc = launch_kmeans(exec_mode, s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign, q_perm,
-                     q_sizes, q_offsets, q_cent, q_iters, nullptr, p.km, st);
+  // (1) cluster Q and K independently; V follows K (analysis.py:228-238).  The two sides share
+  // nothing, and the late Lloyd iterations are short latency-bound launches, so the key side is
+  // forked onto a helper stream; the join below makes the caller's stream the only one anything
+  // downstream depends on.  The helper stream and its two events are created once per process
+  // (stream creation can serialise with running work, so it is kept out of the per-call path).
+  static std::mutex fork_mu;
+  static cudaStream_t side = nullptr;
+  static cudaEvent_t fork = nullptr, join = nullptr;
+  int rc_k = SVGEAR_ECUDA;
+  rc = SVGEAR_ECUDA;
+  {
+    std::lock_guard<std::mutex> lock(fork_mu);
+    if (!side) {
+      if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess) {
+        side = nullptr;
+        return SVGEAR_ECUDA;
+      }
+    }
+    if (cudaEventRecord(fork, st) == cudaSuccess && cudaStreamWaitEvent(side, fork, 0) == cudaSuccess) {
+      rc_k = launch_kmeans(exec_mode, s.bh, s.n_k, s.d, s.c_k, (const bf16*)k, k_init, kmeans_iters, k_assign,
+                           k_perm, k_sizes, k_offsets, k_cent, k_iters, nullptr, p.km2, side);
+      if (!rc_k) rc_k = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)k, k_perm, p.kp, side);
+      if (!rc_k) rc_k = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)v, k_perm, p.vp, side);
+      if (!rc_k)
+        rc_k = launch_segment_means(s.bh, s.n_k, s.d, s.c_k, p.vp, k_sizes, k_offsets, v_cent, nullptr, side);
+      rc = launch_kmeans(exec_mode, s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign,
+                         q_perm, q_sizes, q_offsets, q_cent, q_iters, nullptr, p.km, st);
+      if (!rc) rc = launch_gather_rows(s.bh, s.n_q, s.d, (const bf16*)q, q_perm, p.qp, st);
+      // join unconditionally so that the helper stream never outlives the caller's ordering
+      if (cudaEventRecord(join, side) != cudaSuccess || cudaStreamWaitEvent(st, join, 0) != cudaSuccess)
+        rc = SVGEAR_ECUDA;
+    }
+  }
   if (rc) return rc;
-  rc = launch_kmeans(exec_mode, s.bh, s.n_k, s.d, s.c_k, (const bf16*)k, k_init, kmeans_iters, k_assign, k_perm,
-                     k_sizes, k_offsets, k_cent, k_iters, nullptr, p.km, st);
-  if (rc) return rc;
-  rc = launch_gather_rows(s.bh, s.n_q, s.d, (const bf16*)q, q_perm, p.qp, st);
-  if (rc) return rc;
-  rc = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)k, k_perm, p.kp, st);
-  if (rc) return rc;
-  rc = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)v, k_perm, p.vp, st);
-  if (rc) return rc;
-  rc = launch_segment_means(s.bh, s.n_k, s.d, s.c_k, p.vp, k_sizes, k_offsets, v_cent, nullptr, st);
-  if (rc) return rc;
+  if (rc_k) return rc_k;
   // (2) error table + routing
   rc = launch_error_table(s, exec_mode, estimator_mode, q_cent, k_cent, v_cent, p.kp, p.vp, q_sizes,
                           k_sizes, k_offsets, err, stab, p.es, st);

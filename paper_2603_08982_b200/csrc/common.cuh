@@ -108,6 +108,9 @@ struct KmeansScratch {
   float* move;            // [bh][c]  |c_new - c_old| of the last update
   uint8_t* dirty;         // [bh][c]  membership changed this iteration
   int32_t* iters_run;     // [bh]     iterations executed (internal copy of `iters`)
+  int32_t* ticket;        // [bh]     block ticket counter of sizes_hist_kernel
+  int32_t* has_empty;     // [bh]     some cluster is empty after this iteration's assignment
+  int32_t* resid_nz;      // [bh]     the second bf16 piece of some centre is non-zero
   bool carve(Carver& cv, int bh, int n, int c, int d);
 };
 

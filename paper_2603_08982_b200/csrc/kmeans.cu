@@ -119,8 +119,11 @@ __global__ void __launch_bounds__(128)
 // ------------------------------------------------------------------------------------------------
 // cluster sizes (integer atomics -> deterministic)
 // ------------------------------------------------------------------------------------------------
+// The last block of an instance to finish (ticket counter) also records whether any cluster is
+// empty, so that the repair helpers can return after reading one flag.
 __global__ void sizes_hist_kernel(const int32_t* __restrict__ assign, int n, int c,
-                                  int32_t* __restrict__ sizes, const int32_t* __restrict__ done) {
+                                  int32_t* __restrict__ sizes, int32_t* __restrict__ ticket,
+                                  int32_t* __restrict__ has_empty, const int32_t* __restrict__ done) {
   const int h = blockIdx.y;
   if (done[h]) return;
   extern __shared__ int32_t hist[];
@@ -132,6 +135,20 @@ __global__ void sizes_hist_kernel(const int32_t* __restrict__ assign, int n, int
   __syncthreads();
   for (int j = threadIdx.x; j < c; j += blockDim.x)
     if (hist[j]) atomicAdd(&sizes[(size_t)h * c + j], hist[j]);
+  __threadfence();
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&ticket[h], 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  int empty = 0;
+  for (int j = threadIdx.x; j < c; j += blockDim.x) empty |= (__ldcg(&sizes[(size_t)h * c + j]) == 0);
+  empty = __syncthreads_or(empty);
+  if (threadIdx.x == 0) {
+    has_empty[h] = empty;
+    ticket[h] = 0;
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -145,19 +162,17 @@ __global__ void sizes_hist_kernel(const int32_t* __restrict__ assign, int n, int
 // the current centres — by this grid-wide kernel; other instances return after scanning their sizes.
 __global__ void __launch_bounds__(256)
     own_refresh_kernel(int n, int c, int d, const bf16* __restrict__ x_all, const float* __restrict__ cent_all,
-                       const int32_t* __restrict__ assign_all, const int32_t* __restrict__ sizes_all,
+                       const int32_t* __restrict__ assign_all, const int32_t* __restrict__ has_empty,
                        float* __restrict__ own_all, const int32_t* __restrict__ done) {
   const int h = blockIdx.y;
-  if (done[h]) return;
+  if (done[h] || !has_empty[h]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int empty = 0;
-  for (int j = tid; j < c; j += 256) empty |= (sizes_all[(size_t)h * c + j] == 0);
-  if (!__syncthreads_or(empty)) return;
   const bf16* x = x_all + (size_t)h * n * d;
   const float* cent = cent_all + (size_t)h * c * d;
   const int32_t* assign = assign_all + (size_t)h * n;
   float* own = own_all + (size_t)h * n;
-  const int lo = blockIdx.x * kSortChunk, hi = min(n, lo + kSortChunk);
+  for (int lo = blockIdx.x * kSortChunk; lo < n; lo += gridDim.x * kSortChunk) {
+  const int hi = min(n, lo + kSortChunk);
   for (int t0 = lo + warp * 4; t0 < hi; t0 += 32) {  // 4 independent rows per warp step
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -177,6 +192,7 @@ __global__ void __launch_bounds__(256)
       const float v = warp_sum(acc[u]);
       if (lane == 0 && t0 + u < hi) own[t0 + u] = v;
     }
+  }
   }
 }
 
@@ -317,8 +333,8 @@ __global__ void __launch_bounds__(1024)
                 int32_t* __restrict__ offsets_all, int32_t* __restrict__ chunk_counts,
                 const double* __restrict__ chunk_inertia, double* __restrict__ inertia,
                 int32_t* __restrict__ iters, int32_t* __restrict__ iters_run,
-                int32_t* __restrict__ nactive, const int32_t* __restrict__ changed,
-                int32_t* __restrict__ done) {
+                int32_t* __restrict__ nactive, int32_t* __restrict__ resid_nz,
+                const int32_t* __restrict__ changed, int32_t* __restrict__ done) {
   const int h = blockIdx.x;
   if (done[h]) return;
   const int32_t* sizes = sizes_all + (size_t)h * c;
@@ -379,6 +395,7 @@ __global__ void __launch_bounds__(1024)
     if (iters) iters[h] = iter + 1;
     iters_run[h] = iter + 1;
     nactive[h] = 0;  // the next iteration's filter appends to an empty list
+    resid_nz[h] = 0;
     if (iter > 0 && !changed[h]) done[h] = 1;  // assignments unchanged -> converged
   }
 }
@@ -422,15 +439,11 @@ __global__ void __launch_bounds__(256)
 // perm == nullptr means `x` is already cluster-contiguous (segment_means).
 // ------------------------------------------------------------------------------------------------
 template <int D>
-__global__ void __launch_bounds__(128)
-    cluster_mean_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ perm, int n, int c,
-                        const int32_t* __restrict__ sizes, const int32_t* __restrict__ offsets,
-                        float* __restrict__ means, float* __restrict__ norms,
-                        const int32_t* __restrict__ done, const uint8_t* __restrict__ dirty,
-                        float* __restrict__ move) {
-  const int h = blockIdx.y;
-  if (done && done[h]) return;
-  const int j = blockIdx.x;
+__device__ __forceinline__ void cluster_mean_one(const bf16* __restrict__ x, const int32_t* __restrict__ perm,
+                                                 int n, int c, int h, int j, const int32_t* __restrict__ sizes,
+                                                 const int32_t* __restrict__ offsets, float* __restrict__ means,
+                                                 float* __restrict__ norms, const uint8_t* __restrict__ dirty,
+                                                 float* __restrict__ move) {
   if (dirty && !dirty[(size_t)h * c + j]) {  // same members in the same order: the mean is unchanged
     if (threadIdx.x == 0) move[(size_t)h * c + j] = 0.f;
     return;
@@ -501,6 +514,24 @@ __global__ void __launch_bounds__(128)
       if (norms) norms[(size_t)h * c + j] = s;
       if (move) move[(size_t)h * c + j] = sqrtf(mv);
     }
+  }
+}
+
+// grid = (min(c, kMeanBlocks), bh): a block walks clusters blockIdx.x, blockIdx.x + gridDim.x, ...
+// (instances that have converged cost one block-exit per block, not one per cluster)
+constexpr int kMeanBlocks = 160;
+template <int D>
+__global__ void __launch_bounds__(128)
+    cluster_mean_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ perm, int n, int c,
+                        const int32_t* __restrict__ sizes, const int32_t* __restrict__ offsets,
+                        float* __restrict__ means, float* __restrict__ norms,
+                        const int32_t* __restrict__ done, const uint8_t* __restrict__ dirty,
+                        float* __restrict__ move) {
+  const int h = blockIdx.y;
+  if (done && done[h]) return;
+  for (int j = blockIdx.x; j < c; j += gridDim.x) {
+    cluster_mean_one<D>(x, perm, n, c, h, j, sizes, offsets, means, norms, dirty, move);
+    __syncthreads();  // shared partials are reused by the next cluster
   }
 }
 
@@ -605,6 +636,9 @@ bool KmeansScratch::carve(Carver& cv, int bh, int n, int c, int d) {
   move = cv.take<float>((size_t)bh * c);
   dirty = cv.take<uint8_t>((size_t)bh * c);
   iters_run = cv.take<int32_t>(bh);
+  ticket = cv.take<int32_t>(bh);
+  has_empty = cv.take<int32_t>(bh);
+  resid_nz = cv.take<int32_t>(bh);
   return cv.ok;
 }
 
@@ -617,6 +651,8 @@ int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, con
                               cudaMemcpyDeviceToDevice, st));
   SVG_CUDA_OK(cudaMemsetAsync(sc.done, 0, (size_t)bh * 4, st));
   SVG_CUDA_OK(cudaMemsetAsync(sc.changed, 0, (size_t)bh * 4, st));
+  SVG_CUDA_OK(cudaMemsetAsync(sc.ticket, 0, (size_t)bh * 4, st));
+  SVG_CUDA_OK(cudaMemsetAsync(sc.resid_nz, 0, (size_t)bh * 4, st));
   centroid_norm_kernel<<<ceil_div(bh * c, 8), 256, 0, st>>>(centroids, d, bh * c, sc.cnorm);
   SVG_LAUNCH_OK();
   const bool full_eval = (exec_mode & SVGEAR_KMEANS_FULL_EVAL) != 0;
@@ -642,11 +678,12 @@ int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, con
       assign_fp32_kernel<64><<<ga, 128, 0, st>>>(x, centroids, sc.cnorm, n, c, assign, sc.own_d2,
                                                  sizes, sc.changed, sc.done);
     SVG_LAUNCH_OK();
-    sizes_hist_kernel<<<dim3(hist_blocks, bh), 256, hist_smem, st>>>(assign, n, c, sizes, sc.done);
+    sizes_hist_kernel<<<dim3(hist_blocks, bh), 256, hist_smem, st>>>(assign, n, c, sizes, sc.ticket,
+                                                                     sc.has_empty, sc.done);
     SVG_LAUNCH_OK();
     if (use_tc) {  // exact own distances for the donor choice (the tensor-core ones are rounded / stale)
-      own_refresh_kernel<<<dim3(nchunks, bh), 256, 0, st>>>(n, c, d, x, centroids, assign, sizes, sc.own_d2,
-                                                           sc.done);
+      own_refresh_kernel<<<dim3(min(nchunks, 32), bh), 256, 0, st>>>(n, c, d, x, centroids, assign, sc.has_empty,
+                                                           sc.own_d2, sc.done);
       SVG_LAUNCH_OK();
     }
     repair_kernel<<<bh, 1024, 0, st>>>(n, c, assign, sc.own_d2, sizes, sc.ub, sc.lb,
@@ -658,7 +695,7 @@ int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, con
     SVG_LAUNCH_OK();
     scan_kernel<<<bh, 1024, 0, st>>>(n, c, nchunks, it, sizes, offsets, sc.chunk_counts,
                                      sc.chunk_inertia, inertia, iters, sc.iters_run, sc.nactive,
-                                     sc.changed, sc.done);
+                                     sc.resid_nz, sc.changed, sc.done);
     SVG_LAUNCH_OK();
     if (bounded && inertia) {  // own distances of skipped tokens are stale: recompute the sum exactly
       const int last = it == max_iters - 1;
@@ -673,10 +710,10 @@ int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, con
     SVG_LAUNCH_OK();
     const uint8_t* dirty = bounded ? sc.dirty : nullptr;
     if (d == 128)
-      cluster_mean_kernel<128><<<dim3(c, bh), 128, 0, st>>>(x, perm, n, c, sizes, offsets, centroids,
+      cluster_mean_kernel<128><<<dim3(min(c, kMeanBlocks), bh), 128, 0, st>>>(x, perm, n, c, sizes, offsets, centroids,
                                                            sc.cnorm, sc.done, dirty, sc.move);
     else
-      cluster_mean_kernel<64><<<dim3(c, bh), 128, 0, st>>>(x, perm, n, c, sizes, offsets, centroids,
+      cluster_mean_kernel<64><<<dim3(min(c, kMeanBlocks), bh), 128, 0, st>>>(x, perm, n, c, sizes, offsets, centroids,
                                                           sc.cnorm, sc.done, dirty, sc.move);
     SVG_LAUNCH_OK();
   }
@@ -696,10 +733,10 @@ int launch_gather_rows(int bh, int n, int d, const bf16* x, const int32_t* perm,
 int launch_segment_means(int bh, int n, int d, int c, const bf16* xp, const int32_t* sizes,
                          const int32_t* offsets, float* means, float* norms, cudaStream_t st) {
   if (d == 128)
-    cluster_mean_kernel<128><<<dim3(c, bh), 128, 0, st>>>(xp, nullptr, n, c, sizes, offsets, means,
+    cluster_mean_kernel<128><<<dim3(min(c, kMeanBlocks), bh), 128, 0, st>>>(xp, nullptr, n, c, sizes, offsets, means,
                                                          norms, nullptr, nullptr, nullptr);
   else
-    cluster_mean_kernel<64><<<dim3(c, bh), 128, 0, st>>>(xp, nullptr, n, c, sizes, offsets, means,
+    cluster_mean_kernel<64><<<dim3(min(c, kMeanBlocks), bh), 128, 0, st>>>(xp, nullptr, n, c, sizes, offsets, means,
                                                         norms, nullptr, nullptr, nullptr);
   SVG_LAUNCH_OK();
   return SVGEAR_OK;

@@ -53,26 +53,32 @@ struct KSmem {
 // fp32 centroids -> kPieces bf16 pieces [bh][piece][cpad][d] + padded norms (inf beyond c)
 __global__ void split_centroids_kernel(const float* __restrict__ cent, const float* __restrict__ cnorm,
                                        int d, int c, int cpad, bf16* __restrict__ pieces,
-                                       float* __restrict__ cnorm_pad, const int32_t* __restrict__ done) {
+                                       float* __restrict__ cnorm_pad, int32_t* __restrict__ resid_nz,
+                                       const int32_t* __restrict__ done) {
   const int h = blockIdx.y;
   if (done[h]) return;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= cpad * d) return;
-  const int j = idx / d;
-  float v = j < c ? cent[(size_t)h * c * d + idx] : 0.f;
+  int nz = 0;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < cpad * d; idx += gridDim.x * blockDim.x) {
+    const int j = idx / d;
+    float v = j < c ? cent[(size_t)h * c * d + idx] : 0.f;
 #pragma unroll
-  for (int p = 0; p < kPieces; ++p) {
-    const bf16 b = __float2bfloat16_rn(v);
-    pieces[((size_t)h * kPieces + p) * cpad * d + idx] = b;
-    v -= __bfloat162float(b);
+    for (int p = 0; p < kPieces; ++p) {
+      const bf16 b = __float2bfloat16_rn(v);
+      pieces[((size_t)h * kPieces + p) * cpad * d + idx] = b;
+      v -= __bfloat162float(b);
+      if (p == 0) nz |= (v != 0.f);
+    }
+    if (idx % d == 0) cnorm_pad[(size_t)h * cpad + j] = j < c ? cnorm[(size_t)h * c + j] : INFINITY;
   }
-  if (idx % d == 0) cnorm_pad[(size_t)h * cpad + j] = j < c ? cnorm[(size_t)h * c + j] : INFINITY;
+  // centres that are exactly bf16 (start centres picked from the tokens) need only the first piece
+  if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&resid_nz[h], 1);
 }
 
 __global__ void token_norm_kernel(const bf16* __restrict__ x, int d, long long total, float* __restrict__ xn) {
-  const long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
-  if (row >= total) return;
+  const long long warp_id = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x / 32);
+  for (long long row = warp_id; row < total; row += nwarps) {
   // sequential-in-k accumulation per lane chunk is not needed for parity: |x|^2 is a per-token
   // constant of the argmin; it only enters own_d2.  Lanes split the row, fixed shuffle tree.
   // each lane takes d/32 consecutive elements (8-byte loads at d=128), fixed shuffle tree
@@ -92,6 +98,7 @@ __global__ void token_norm_kernel(const bf16* __restrict__ x, int d, long long t
   }
   s = warp_sum(s);
   if (lane == 0) xn[row] = s;
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -197,7 +204,8 @@ __global__ void __launch_bounds__(KTHREADS, 1)
                      int c, int cpad, int cpad16, int first_iter, int32_t* __restrict__ assign,
                      float* __restrict__ own_d2, float* __restrict__ ub, float* __restrict__ lb,
                      const int32_t* __restrict__ active, const int32_t* __restrict__ nactive,
-                     uint8_t* __restrict__ dirty, const int32_t* __restrict__ done) {
+                     uint8_t* __restrict__ dirty, const int32_t* __restrict__ resid_nz,
+                     const int32_t* __restrict__ done) {
   using L = KSmem<D>;
   extern __shared__ uint8_t smem_raw[];
   __shared__ int16_t s_heads[kMaxHeads];
@@ -248,7 +256,6 @@ __global__ void __launch_bounds__(KTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int NT = (cpad16 + KN - 1) / KN;  // N tiles; the last one may be narrower (multiple of 16)
-  const int U = NT * kPieces;             // pipeline units per item
   // work item -> (instance, 256-token tile of its active list): binary search in the item prefix
   auto locate = [&](int it, int& tile) -> int {
     const int item = (int)blockIdx.x + it * (int)gridDim.x;
@@ -269,10 +276,12 @@ __global__ void __launch_bounds__(KTHREADS, 1)
     for (int it = 0; it < my_items; ++it) {
       int tile_unused;
       const int h = locate(it, tile_unused);
+      const int np = resid_nz[h] ? kPieces : 1;  // pieces that are not identically zero
+      const int U = NT * np;                      // pipeline units of this item
       for (int uu = 0; uu < U; ++uu, ++u) {
         const int st = u % KSTAGES;
         if (u >= KSTAGES) mbar_wait(bar(KB_BEMPTY + st), ((u / KSTAGES) - 1) & 1);
-        const int nt = uu / kPieces, p = uu % kPieces;
+        const int nt = uu / np, p = uu % np;
         const int nn = min(KN, cpad16 - nt * KN);
         const bf16* bsrc = pieces + (((size_t)h * kPieces + p) * cpad + (size_t)nt * KN) * D;
         const uint32_t dst = sB + (uint32_t)st * L::kBBytes;
@@ -328,6 +337,8 @@ __global__ void __launch_bounds__(KTHREADS, 1)
       int u = 0, g = 0;  // running unit / N-tile counters
       for (int it = 0; it < my_items; ++it) {
         const int ab = it & 1;
+        int tile_unused;
+        const int np = resid_nz[locate(it, tile_unused)] ? kPieces : 1;
         mbar_wait(bar(KB_AFULL + ab), (it >> 1) & 1);
         const uint32_t abase = sA + (uint32_t)ab * L::kABytes;
         for (int nt = 0; nt < NT; ++nt, ++g) {
@@ -335,7 +346,7 @@ __global__ void __launch_bounds__(KTHREADS, 1)
           const int nn = min(KN, cpad16 - nt * KN);
           const uint32_t idesc = make_idesc(128, nn, 0);
           if (g >= 2) mbar_wait(bar(KB_ACCEMPTY + buf), ((g >> 1) - 1) & 1);
-          for (int p = 0; p < kPieces; ++p, ++u) {
+          for (int p = 0; p < np; ++p, ++u) {
             const int st = u % KSTAGES;
             mbar_wait(bar(KB_BFULL + st), (u / KSTAGES) & 1);
             tc_fence_after();
@@ -434,7 +445,7 @@ size_t kmeans_tc_scratch_bytes(int bh, int n, int c, int d) {
 
 int launch_token_norms(int bh, int n, int d, const bf16* x, float* xnorm, cudaStream_t st) {
   const long long total = (long long)bh * n;
-  token_norm_kernel<<<(unsigned)((total + 7) / 8), 256, 0, st>>>(x, d, total, xnorm);
+  token_norm_kernel<<<(unsigned)((total + 63) / 64 < 148 * 32 ? (total + 63) / 64 : 148 * 32), 256, 0, st>>>(x, d, total, xnorm);
   SVG_LAUNCH_OK();
   return SVGEAR_OK;
 }
@@ -444,8 +455,8 @@ int launch_kmeans_assign_tc(int bh, int n, int d, int c, int iter, bool full_eva
                             int32_t* sizes, cudaStream_t st) {
   const int cpad = ceil_div(c, KN) * KN;     // row stride of the piece arrays / norm array
   const int cpad16 = ceil_div(c, 16) * 16;   // columns actually multiplied
-  split_centroids_kernel<<<dim3(ceil_div(cpad * d, 256), bh), 256, 0, st>>>(cent, cnorm, d, c, cpad, sc.pieces,
-                                                                           sc.cnorm_pad, sc.done);
+  split_centroids_kernel<<<dim3(min(ceil_div(cpad * d, 256), 64), bh), 256, 0, st>>>(cent, cnorm, d, c, cpad, sc.pieces,
+                                                                           sc.cnorm_pad, sc.resid_nz, sc.done);
   SVG_LAUNCH_OK();
   const int all_active = (iter == 0 || full_eval) ? 1 : 0;
   bound_filter_kernel<<<dim3(ceil_div(n, kFilterTokens), bh), 256, 0, st>>>(
@@ -476,12 +487,12 @@ int launch_kmeans_assign_tc(int bh, int n, int d, int c, int iter, bool full_eva
       const size_t smem = KSmem<128>::bytes();
       SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       assign_tc_kernel<128><<<grid, KTHREADS, smem, st>>>(xs, ps, cs, xns, nb, n, c, cpad, cpad16, iter == 0, as, os,
-                                                          us, ls, al, sc.nactive + h0, dt, sc.done + h0);
+                                                          us, ls, al, sc.nactive + h0, dt, sc.resid_nz + h0, sc.done + h0);
     } else {
       const size_t smem = KSmem<64>::bytes();
       SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       assign_tc_kernel<64><<<grid, KTHREADS, smem, st>>>(xs, ps, cs, xns, nb, n, c, cpad, cpad16, iter == 0, as, os,
-                                                         us, ls, al, sc.nactive + h0, dt, sc.done + h0);
+                                                         us, ls, al, sc.nactive + h0, dt, sc.resid_nz + h0, sc.done + h0);
     }
     SVG_LAUNCH_OK();
   }

@@ -16,7 +16,7 @@ import torch
 from . import _lib
 from ._tensors import ShapeError, require_cuda, stream_ptr, workspace
 from .analysis import side_seeds
-from .clustering import device_start, seeded_start, strided_start
+from .clustering import device_start, device_start_pair, seeded_start, strided_start
 from .router import _OVERSHOOT, entry_capacity
 
 _EST = {"valueAware": _lib.EST_VALUE_AWARE, "plain": _lib.EST_PLAIN}
@@ -93,7 +93,7 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
         if init == "reference":
             rq, rk = reference_init(qb, kb, c_q, c_k, seed)
         elif init == "device":
-            rq, rk = device_start(qb, c_q, seed), device_start(kb, c_k, seed + 0x9E37)
+            rq, rk = device_start_pair(qb, c_q, kb, c_k, seed)
         else:
             rq, rk = strided_start(qb, c_q), strided_start(kb, c_k)
         q_init = rq if q_init is None else q_init
