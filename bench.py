@@ -231,13 +231,52 @@ def run_ours(args):
     hm = torch.empty((1, H if world > 1 else hl, cq, ck), dtype=torch.bool).pin_memory()
     dq, dk, dv = (torch.empty_like(t) for t in (q, k, v))
 
+    # The e2e leg streams the layer through the public operator in head groups: while group g is
+    # computed, the host->device copy of group g+1 and the device->host copy of group g-1 run on a
+    # copy stream (heads are independent instances, so the grouping does not change any result of
+    # a head except the device-side seeding draw, which is keyed by the instance index).
+    n_groups = 4 if (hl >= 8 and world == 1) else 1
+    bounds = [hl * g // n_groups for g in range(n_groups + 1)]
+    copy_stream = torch.cuda.Stream(device=dev)   # host -> device
+    back_stream = torch.cuda.Stream(device=dev)   # device -> host (PCIe is full duplex)
+    gmax = max(bounds[g + 1] - bounds[g] for g in range(n_groups))
+    ws_g = ws if n_groups == 1 else torch.empty(
+        _lib.workspace_bytes(_lib.Shape(max(gmax, 1), S, S, d, cq, ck)), dtype=torch.uint8, device=dev)
+    do = torch.empty((1, hl, S, d), dtype=out_dtype, device=dev)
+    dm = torch.empty((1, hl, cq, ck), dtype=torch.bool, device=dev)
+
     def step_e2e():
-        dq.copy_(hq, non_blocking=True); dk.copy_(hk, non_blocking=True); dv.copy_(hv, non_blocking=True)
-        res = layer(dq, dk, dv)
-        o, m = res
-        if world > 1:
-            o, m = gather_heads(o, H), gather_heads(m, H)
-        ho.copy_(o, non_blocking=True); hm.copy_(m, non_blocking=True)
+        if n_groups == 1:
+            dq.copy_(hq, non_blocking=True); dk.copy_(hk, non_blocking=True); dv.copy_(hv, non_blocking=True)
+            o, m = layer(dq, dk, dv)
+            if world > 1:
+                o, m = gather_heads(o, H), gather_heads(m, H)
+            ho.copy_(o, non_blocking=True); hm.copy_(m, non_blocking=True)
+            return
+        cur = torch.cuda.current_stream(dev)
+        copy_stream.wait_stream(cur)
+        h2d, done = [], []
+        with torch.cuda.stream(copy_stream):
+            for g in range(n_groups):
+                a, b = bounds[g], bounds[g + 1]
+                dq[:, a:b].copy_(hq[:, a:b], non_blocking=True)
+                dk[:, a:b].copy_(hk[:, a:b], non_blocking=True)
+                dv[:, a:b].copy_(hv[:, a:b], non_blocking=True)
+                ev = torch.cuda.Event(); ev.record(copy_stream); h2d.append(ev)
+        for g in range(n_groups):
+            a, b = bounds[g], bounds[g + 1]
+            cur.wait_event(h2d[g])
+            o, m = P.svg_ear_attention(dq[:, a:b], dk[:, a:b], dv[:, a:b], cq, ck, args.rho, seed=a,
+                                       init=args.init, kmeans_iters=args.kmeans_iters,
+                                       check_fp32=args.fp32_check, workspace_buffer=ws_g)
+            do[:, a:b].copy_(o); dm[:, a:b].copy_(m)
+            ev = torch.cuda.Event(); ev.record(cur); done.append(ev)
+            with torch.cuda.stream(back_stream):
+                back_stream.wait_event(ev)
+                ho[:, a:b].copy_(do[:, a:b], non_blocking=True)
+                hm[:, a:b].copy_(dm[:, a:b], non_blocking=True)
+        cur.wait_stream(back_stream)
+        cur.wait_stream(copy_stream)
 
     def timed(fn, steps):
         if world > 1:
@@ -314,7 +353,8 @@ def run_ours(args):
                        "inputs": f"per-head blob mixture sigma={args.sigma}, generated on device",
                        "executor": "fp32-check" if args.fp32_check else "bf16-tcgen05",
                        "density_achieved": density, "parallelism": f"head-parallel x{world}",
-                       "l2": "inputs (%.0f MB/rank) exceed the 126 MB L2; no explicit flush" % (in_bytes / 1e6)},
+                       "l2": "inputs (%.0f MB/rank) exceed the 126 MB L2; no explicit flush" % (in_bytes / 1e6),
+                       "e2e_pipeline": f"{n_groups} head groups, H2D and D2H on their own streams"},
             "clocks": clocks,
             "e2e": {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms_e2e,
                     "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": out_bytes},

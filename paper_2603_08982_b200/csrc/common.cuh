@@ -28,7 +28,7 @@ extern long long g_launches;  // diagnostic: kernels launched by this library in
 typedef __nv_bfloat16 bf16;
 
 constexpr int kMaxClusters = 4096;
-constexpr int kSortChunk = 1024;  // tokens per counting-sort chunk
+constexpr int kSortChunk = 2048;  // tokens per counting-sort chunk
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }

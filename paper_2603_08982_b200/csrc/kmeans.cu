@@ -171,8 +171,9 @@ __global__ void __launch_bounds__(256)
   const float* cent = cent_all + (size_t)h * c * d;
   const int32_t* assign = assign_all + (size_t)h * n;
   float* own = own_all + (size_t)h * n;
-  for (int lo = blockIdx.x * kSortChunk; lo < n; lo += gridDim.x * kSortChunk) {
-  const int hi = min(n, lo + kSortChunk);
+  constexpr int kSpan = 1024;  // tokens per block step
+  for (int lo = blockIdx.x * kSpan; lo < n; lo += gridDim.x * kSpan) {
+  const int hi = min(n, lo + kSpan);
   for (int t0 = lo + warp * 4; t0 < hi; t0 += 32) {  // 4 independent rows per warp step
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -682,7 +683,7 @@ int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, con
                                                                      sc.has_empty, sc.done);
     SVG_LAUNCH_OK();
     if (use_tc) {  // exact own distances for the donor choice (the tensor-core ones are rounded / stale)
-      own_refresh_kernel<<<dim3(min(nchunks, 32), bh), 256, 0, st>>>(n, c, d, x, centroids, assign, sc.has_empty,
+      own_refresh_kernel<<<dim3(min(ceil_div(n, 1024), 64), bh), 256, 0, st>>>(n, c, d, x, centroids, assign, sc.has_empty,
                                                            sc.own_d2, sc.done);
       SVG_LAUNCH_OK();
     }

@@ -341,6 +341,22 @@ class TestExecutor:
         want = O.softmax_rows(logits) @ O.segment_means(vp, km)
         assert rel_l2(host(res.output.float()), want) <= tol
 
+    @pytest.mark.parametrize("dtype,tol", [(torch.float32, TOL_FP32), (torch.bfloat16, TOL_BF16)])
+    @pytest.mark.parametrize("d", [64, 128])
+    def test_query_clusters_spanning_several_cta_tiles(self, dtype, tol, d):
+        # query clusters of ~700 rows: 256-row CTA tiles (two 128-row halves) plus a ragged last
+        # tile with a single live half; key clusters of 1..300 rows cross the 64-key tile borders
+        prep, qm, km, qp, kp, vp = self._instance(11, n_q=1400, n_k=1100, d=d, c_q=2, c_k=9)
+        rng = np.random.default_rng(3)
+        for rho in (0.25, 0.6):
+            sel = rng.random((2, 9)) < rho
+            mask = P.mask_from_selected(torch.from_numpy(sel).cuda(), self._sizes(prep))
+            res = P.sparse_attend(prep.q, prep.k, prep.v, prep.q_model, prep.k_model, mask, dtype=dtype)
+            want = O.mixed_logit_output(qp, kp, vp, qm, km, sel)
+            assert rel_l2(host(res.output.float()), want) <= tol, rho
+            _, o_lse = O.sparse_attend(qp, kp, vp, qm, km, sel)
+            assert np.abs(host(res.lse) - o_lse).max() <= (1e-4 if dtype == torch.float32 else 2e-2)
+
     def test_unpermute_scatters_rows(self):
         prep, qm, km, qp, kp, vp = self._instance(9)
         mask = P.mask_from_selected((torch.rand(4, 6) < 0.5).cuda(), self._sizes(prep))
