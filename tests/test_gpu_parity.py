@@ -515,3 +515,38 @@ class TestBoundedLloyd:
         a, b = self.both(x, starts, iters=10)
         self.same(a, b)
         assert bool((a["sizes"] >= 1).all())
+
+
+# --------------------------------------------------------------------------------------------
+# BASELINE config 4 (budget sweep): error-aware routing vs SVG2 score routing on one clustering,
+# output error against dense attention (reference analogue: acceptance criterion 06,
+# tests/test_acceptance.py, analysis.py:308-342)
+# --------------------------------------------------------------------------------------------
+class TestBudgetSweep:
+    def test_error_aware_beats_score_routing_on_blobs(self):
+        S, d, cq, ck = 8192, 64, 32, 96
+        heads = [tuple(O.round_to_bf16(t) for t in O.blob_instance(S, S, d, cq, ck, 0.1, h)) for h in range(2)]
+        q, k, v = (dev(np.stack([hd[i] for hd in heads])) for i in range(3))
+        from paper_2603_08982_b200.clustering import ClusterModel, device_start_pair, run_lloyd
+        from paper_2603_08982_b200 import router as R
+        qi, ki = device_start_pair(q, cq, k, ck, 0)
+        rq, rk = run_lloyd(q, qi, 25), run_lloyd(k, ki, 25)
+        qm = ClusterModel(cq, rq["assign"], rq["centroids"], rq["sizes"], rq["perm"], rq["offsets"])
+        km = ClusterModel(ck, rk["assign"], rk["centroids"], rk["sizes"], rk["perm"], rk["offsets"])
+        qp, kp, vp = P.permute_rows(q, qm), P.permute_rows(k, km), P.permute_rows(v, km)
+        table = P.estimate_errors_streaming(qm, km, kp, vp)
+        dense = torch.nn.functional.scaled_dot_product_attention(q.float(), k.float(), v.float())
+        wins, errs = 0, []
+        rhos = (0.05, 0.1, 0.2, 0.3, 0.5)
+        for rho in rhos:
+            b = R.DensityBudget.global_density(rho)
+            e = {}
+            for name, mask in (("ear", R.route_error_aware(table, b)),
+                               ("score", R.route_score(qm.centroids, km.centroids, qm.sizes, km.sizes, b))):
+                assert float(mask.density.max()) <= rho + 1e-9
+                res = P.sparse_attend(qp, kp, vp, qm, km, mask, unpermute=True, dtype=torch.bfloat16)
+                e[name] = rel_l2(host(res.output.float()), host(dense))
+            errs.append(e)
+            wins += e["ear"] <= e["score"] * 1.001
+        assert wins >= len(rhos) - 1, errs
+        assert errs[-1]["ear"] <= errs[0]["ear"]  # more exact budget never hurts on this instance
