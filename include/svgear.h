@@ -170,6 +170,18 @@ int svgear_route_score(const SvgEarShape* shape, const float* q_centroids,
                        int64_t capacity_entries, int32_t overshoot, uint8_t* mask,
                        int64_t* entries, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Error-aware routing under the per-query-cluster top-p budget — router.route_error_aware with
+ * DensityBudget.top_p(p) (router.py:172-190): row i may spend the entries of the minimal set of
+ * key clusters whose softmax mass (q̄.k̄/sqrt(d) + ln|k_c|, router.py:193-250) reaches p; inside
+ * the row the same (-ratio, -error, index) order, walk policy and single-block fallback apply.
+ *   p in (0, 1]      mask [bh][c_q][c_k] u8      entries [bh] i64 (may be NULL)                  */
+int svgear_route_error_aware_top_p(const SvgEarShape* shape, const double* error_table,
+                                   const float* q_centroids, const float* k_centroids,
+                                   const int32_t* q_sizes, const int32_t* k_sizes, double p,
+                                   int32_t overshoot, int32_t single_item_fallback, uint8_t* mask,
+                                   int64_t* entries, void* workspace, size_t workspace_bytes,
+                                   void* stream);
+
 /* Block-sparse executor with centroid compensation folded into one online softmax —
  * attention.sparse_attend = exact_block_pass + compensation_pass (attention.py:57-192).
  *   q_permuted/k_permuted/v_permuted cluster-contiguous bf16; mask [bh][c_q][c_k] u8
@@ -191,12 +203,15 @@ int svgear_sparse_attend(const SvgEarShape* shape, int32_t exec_mode, const void
  * inverse_permute_rows (cli.py:119-134).
  *   q,k,v [bh][n][d] bf16      q_init [bh][c_q][d] f32, k_init [bh][c_k][d] f32
  *   out  [bh][n_q][d] (bf16 / f32 per exec_mode)     mask [bh][c_q][c_k] u8
+ *   top_p == 0: global entry budget `capacity_entries`; 0 < top_p <= 1: per-query-cluster top-p
+ *   budget as in svgear_route_error_aware_top_p (capacity_entries is then ignored)
  *   aux may be NULL                                                                              */
 int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const void* v,
                    const float* q_init, const float* k_init, int32_t kmeans_iters,
                    int32_t estimator_mode, int64_t capacity_entries, int32_t overshoot,
-                   int32_t single_item_fallback, int32_t exec_mode, void* out, uint8_t* mask,
-                   const SvgEarAux* aux, void* workspace, size_t workspace_bytes, void* stream);
+                   int32_t single_item_fallback, int32_t exec_mode, double top_p, void* out,
+                   uint8_t* mask, const SvgEarAux* aux, void* workspace, size_t workspace_bytes,
+                   void* stream);
 
 #ifdef __cplusplus
 }

@@ -231,6 +231,29 @@ int svgear_route_score(const SvgEarShape* shape, const float* q_centroids,
                       overshoot, 0, 1, mask, entries, keys, st);
 }
 
+int svgear_route_error_aware_top_p(const SvgEarShape* shape, const double* error_table,
+                                   const float* q_centroids, const float* k_centroids,
+                                   const int32_t* q_sizes, const int32_t* k_sizes, double p,
+                                   int32_t overshoot, int32_t single_item_fallback, uint8_t* mask,
+                                   int64_t* entries, void* workspace, size_t workspace_bytes,
+                                   void* stream) {
+  if (!shape || !error_table || !q_centroids || !k_centroids || !q_sizes || !k_sizes || !mask || !workspace)
+    return SVGEAR_EINVAL;
+  if (!(p > 0.0 && p <= 1.0)) return SVGEAR_EINVAL;
+  if (overshoot != SVGEAR_FILL_REMAINDER && overshoot != SVGEAR_STOP_AT_FIRST_OVERFLOW)
+    return SVGEAR_EINVAL;
+  if (!shape_ok(shape)) return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  Carver cv(workspace, workspace_bytes);
+  double* mass = cv.take<double>((size_t)shape->bh * shape->c_q * shape->c_k);
+  if (!cv.ok) return SVGEAR_EWORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = launch_score_mass(*shape, q_centroids, k_centroids, k_sizes, mass, st);
+  if (rc != SVGEAR_OK) return rc;
+  return launch_route_top_p(*shape, error_table, mass, q_sizes, k_sizes, p, overshoot,
+                            single_item_fallback ? 1 : 0, mask, entries, st);
+}
+
 int svgear_sparse_attend(const SvgEarShape* shape, int32_t exec_mode, const void* q_permuted,
                          const void* k_permuted, const void* v_permuted, const int32_t* q_perm,
                          const int32_t* q_sizes, const int32_t* q_offsets, const int32_t* k_sizes,
@@ -255,11 +278,12 @@ int svgear_sparse_attend(const SvgEarShape* shape, int32_t exec_mode, const void
 int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const void* v,
                    const float* q_init, const float* k_init, int32_t kmeans_iters,
                    int32_t estimator_mode, int64_t capacity_entries, int32_t overshoot,
-                   int32_t single_item_fallback, int32_t exec_mode, void* out, uint8_t* mask,
+                   int32_t single_item_fallback, int32_t exec_mode, double top_p, void* out, uint8_t* mask,
                    const SvgEarAux* aux, void* workspace, size_t workspace_bytes, void* stream) {
   if (!shape || !q || !k || !v || !q_init || !k_init || !out || !mask || !workspace)
     return SVGEAR_EINVAL;
   if (kmeans_iters < 1 || capacity_entries < 0) return SVGEAR_EINVAL;
+  if (!(top_p >= 0.0 && top_p <= 1.0)) return SVGEAR_EINVAL;
   if (estimator_mode != SVGEAR_EST_VALUE_AWARE && estimator_mode != SVGEAR_EST_PLAIN)
     return SVGEAR_EINVAL;
   if (overshoot != SVGEAR_FILL_REMAINDER && overshoot != SVGEAR_STOP_AT_FIRST_OVERFLOW)
@@ -335,8 +359,16 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
   rc = launch_error_table(s, exec_mode, estimator_mode, q_cent, k_cent, v_cent, p.kp, p.vp, q_sizes,
                           k_sizes, k_offsets, err, stab, p.es, st);
   if (rc) return rc;
-  rc = launch_route(s.bh, s.c_q, s.c_k, err, q_sizes, k_sizes, capacity_entries, overshoot,
-                    single_item_fallback ? 1 : 0, 0, mask, entries, p.route_keys, st);
+  if (top_p > 0.0) {  // per-query-cluster top-p budget (router.py:172-190); the key buffer holds the masses
+    double* mass = reinterpret_cast<double*>(p.route_keys);
+    rc = launch_score_mass(s, q_cent, k_cent, k_sizes, mass, st);
+    if (rc) return rc;
+    rc = launch_route_top_p(s, err, mass, q_sizes, k_sizes, top_p, overshoot, single_item_fallback ? 1 : 0, mask,
+                            entries, st);
+  } else {
+    rc = launch_route(s.bh, s.c_q, s.c_k, err, q_sizes, k_sizes, capacity_entries, overshoot,
+                      single_item_fallback ? 1 : 0, 0, mask, entries, p.route_keys, st);
+  }
   if (rc) return rc;
   // (3) fused executor, output scattered to original token order
   return launch_attend(s, exec_mode, p.qp, p.kp, p.vp, q_perm, q_sizes, q_offsets, k_sizes, k_offsets,

@@ -146,6 +146,9 @@ int launch_route(int bh, int c_q, int c_k, const double* val, const int32_t* q_s
                  cudaStream_t st);
 int launch_score_mass(const SvgEarShape& s, const float* qc, const float* kc,
                       const int32_t* k_sizes, double* mass, cudaStream_t st);
+int launch_route_top_p(const SvgEarShape& s, const double* err, const double* mass, const int32_t* q_sizes,
+                       const int32_t* k_sizes, double p, int overshoot, int fallback, uint8_t* mask,
+                       int64_t* entries, cudaStream_t st);
 
 struct AttendScratch {
   int32_t* tile_list;   // [bh][max_tiles][4]  (q-cluster, first row, rows, pad)

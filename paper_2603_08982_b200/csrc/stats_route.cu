@@ -658,6 +658,164 @@ __global__ void __launch_bounds__(1024)
 #undef FOR_BLOCKS
 }
 
+// ------------------------------------------------------------------------------------------------
+// perClusterTopP routing (router.py:172-190 with score_top_p_budget, router.py:209-250): every
+// query-cluster row gets its own entry budget — the entries of the minimal set of key clusters whose
+// softmax mass reaches p — and spends it with the same greedy error-to-cost walk + single-block
+// fallback, restricted to the row.  One CTA per (row, instance): two bitonic sorts of the row in
+// shared memory (mass order, then (-ratio, -error, index) order), and an exact sequential walk by
+// one thread (cumulative sums in the reference's left-to-right order).
+// ------------------------------------------------------------------------------------------------
+struct TopPKey {
+  double a;  // primary, descending
+  double b;  // secondary, descending
+  int idx;   // tertiary, ascending (padding: INT_MAX)
+};
+__device__ __forceinline__ bool topp_before(const TopPKey& x, const TopPKey& y) {
+  if (x.a != y.a) return x.a > y.a;
+  if (x.b != y.b) return x.b > y.b;
+  return x.idx < y.idx;
+}
+__device__ void topp_sort(TopPKey* keys, int npad) {
+  for (int k = 2; k <= npad; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < npad; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          TopPKey x = keys[i], y = keys[l];
+          if (topp_before(y, x) == up) { keys[i] = y; keys[l] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    route_top_p_kernel(const double* __restrict__ err, const double* __restrict__ mass,
+                       const int32_t* __restrict__ q_sizes, const int32_t* __restrict__ k_sizes, int c_q,
+                       int c_k, int npad, double p, int overshoot, int fallback,
+                       uint8_t* __restrict__ mask, unsigned long long* __restrict__ entries) {
+  extern __shared__ __align__(16) unsigned char topp_smem[];
+  TopPKey* keys = reinterpret_cast<TopPKey*>(topp_smem);
+  __shared__ long long s_cap;
+  __shared__ int s_single;  // fallback block (or -1)
+  const int h = blockIdx.y, i = blockIdx.x, tid = threadIdx.x;
+  const double* erow = err + ((size_t)h * c_q + i) * c_k;
+  const double* mrow = mass + ((size_t)h * c_q + i) * c_k;
+  const int32_t* ks = k_sizes + (size_t)h * c_k;
+  const long long qs = q_sizes[(size_t)h * c_q + i];
+  uint8_t* out = mask + ((size_t)h * c_q + i) * c_k;
+  // ---- (1) row budget: minimal mass prefix reaching p (router.py:225-236) -------------------------
+  for (int j = tid; j < npad; j += 256) {
+    TopPKey k;
+    k.a = j < c_k ? mrow[j] : -INFINITY;
+    k.b = 0.0;
+    k.idx = j < c_k ? j : 0x7fffffff;
+    keys[j] = k;
+  }
+  __syncthreads();
+  topp_sort(keys, npad);
+  if (tid == 0) {
+    long long cap = 0;
+    if (p >= 1.0) {
+      for (int j = 0; j < c_k; ++j) cap += qs * ks[j];
+    } else {
+      double cum = 0.0;
+      int cut = c_k;  // searchsorted(cumsum, p, side="left"): first position with cumsum >= p
+      for (int r = 0; r < c_k; ++r) {
+        cum += keys[r].a;
+        if (cum >= p) { cut = r; break; }
+      }
+      const int last = min(cut, c_k - 1);
+      for (int r = 0; r <= last; ++r) cap += qs * ks[keys[r].idx];
+    }
+    s_cap = cap;
+  }
+  __syncthreads();
+  // ---- (2) row order (-ratio, -error, index) (estimator.py:83-96 restricted to the row) ------------
+  for (int j = tid; j < npad; j += 256) {
+    TopPKey k;
+    if (j < c_k) {
+      const double e = erow[j];
+      k.a = e / (double)(qs * ks[j]);
+      k.b = e;
+      k.idx = j;
+    } else {
+      k.a = -INFINITY;
+      k.b = -INFINITY;
+      k.idx = 0x7fffffff;
+    }
+    keys[j] = k;
+  }
+  for (int j = tid; j < c_k; j += 256) out[j] = 0;
+  __syncthreads();
+  topp_sort(keys, npad);
+  // ---- (3) greedy walk + single-block fallback (router.py:100-121), one thread ---------------------
+  if (tid == 0) {
+    const long long cap = s_cap;
+    long long left = cap;
+    double total = 0.0;
+    int ntake = 0;
+    for (int r = 0; r < c_k; ++r) {
+      const int j = keys[r].idx;
+      const long long w = qs * ks[j];
+      if (w <= left) {
+        left -= w;
+        total += keys[r].b;
+        keys[r].idx = j | 0x40000000;  // mark taken
+        ++ntake;
+      } else if (overshoot == SVGEAR_STOP_AT_FIRST_OVERFLOW) {
+        break;
+      }
+    }
+    int single = -1;
+    if (fallback) {
+      double best = 0.0;
+      int bj = -1;
+      for (int j = 0; j < c_k; ++j) {  // first maximum in index order among the blocks that fit
+        if (qs * ks[j] <= cap) {
+          const double e = erow[j];
+          if (bj < 0 || e > best) { best = e; bj = j; }
+        }
+      }
+      if (bj >= 0 && best > total) single = bj;
+    }
+    s_single = single;
+    unsigned long long ent = 0;
+    if (single >= 0) {
+      out[single] = 1;
+      ent = (unsigned long long)(qs * ks[single]);
+    } else {
+      ent = (unsigned long long)(cap - left);
+    }
+    if (entries) atomicAdd(&entries[h], ent);
+    (void)ntake;
+  }
+  __syncthreads();
+  if (s_single < 0) {
+    for (int r = tid; r < c_k; r += 256)
+      if (keys[r].idx & 0x40000000) out[keys[r].idx & 0x3fffffff] = 1;
+  }
+}
+
+int launch_route_top_p(const SvgEarShape& s, const double* err, const double* mass, const int32_t* q_sizes,
+                       const int32_t* k_sizes, double p, int overshoot, int fallback, uint8_t* mask,
+                       int64_t* entries, cudaStream_t st) {
+  int npad = 1;
+  while (npad < s.c_k) npad <<= 1;
+  const size_t smem = (size_t)npad * sizeof(TopPKey);
+  if (smem > 200 * 1024) return SVGEAR_EUNSUPPORTED;
+  if (entries) SVG_CUDA_OK(cudaMemsetAsync(entries, 0, (size_t)s.bh * sizeof(int64_t), st));
+  SVG_CUDA_OK(cudaFuncSetAttribute(route_top_p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  route_top_p_kernel<<<dim3(s.c_q, s.bh), 256, smem, st>>>(err, mass, q_sizes, k_sizes, s.c_q, s.c_k, npad, p,
+                                                          overshoot, fallback, mask,
+                                                          (unsigned long long*)entries);
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
 int launch_route(int bh, int c_q, int c_k, const double* val, const int32_t* q_sizes,
                  const int32_t* k_sizes, int64_t capacity, int overshoot, int fallback,
                  int ratio_mode, uint8_t* mask, int64_t* entries, unsigned long long* keys,

@@ -39,13 +39,15 @@ def reference_init(q, k, n_q_clusters, n_k_clusters, seed):
 def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_init=None,
                       k_init=None, init="reference", kmeans_iters=25, estimator="valueAware",
                       overshoot="fillRemainder", single_item_fallback=True, check_fp32=False,
-                      return_aux=False, workspace_buffer=None):
+                      return_aux=False, workspace_buffer=None, budget_mode="globalDensity"):
     """SVG-EAR attention.
 
     q, k, v : bf16 CUDA tensors [B, H, S, d] (or [H, S, d] / [S, d]); d in {64, 128}.
     n_q_clusters, n_k_clusters : cluster counts C_q, C_k.
     budget : exact-compute budget = global density rho in [0, 1]
-             (router.DensityBudget.global_density, router.py:59-61).
+             (router.DensityBudget.global_density, router.py:59-61); with
+             budget_mode="perClusterTopP" it is the per-query-cluster score mass p in (0, 1]
+             (router.DensityBudget.top_p, router.py:63-65 — the paper's production setting p=0.85).
     init   : "reference" -> k-means++ centres drawn with the reference's RNG recipe from `seed`
              (host side, slow at scale); "device" -> k-means++ on a strided subsample, on the
              device (svgear_kmeans_seed); "strided" -> evenly strided tokens;
@@ -71,7 +73,12 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
             raise ValueError(f"num_clusters must be >= 1, got {c} ({name})")
         if c > n:
             raise ValueError(f"num_clusters ({c}) exceeds token count ({n}) ({name})")
-    if budget is None or not (0.0 <= float(budget) <= 1.0):
+    if budget_mode not in ("globalDensity", "perClusterTopP"):
+        raise ValueError(f"unknown budget mode {budget_mode!r}")
+    if budget_mode == "perClusterTopP":
+        if budget is None or not (0.0 < float(budget) <= 1.0):
+            raise ValueError(f"perClusterTopP budget needs p in (0, 1], got {budget}")
+    elif budget is None or not (0.0 <= float(budget) <= 1.0):
         raise ValueError(f"globalDensity budget needs rho in [0, 1], got {budget}")
     if kmeans_iters < 1:
         raise ValueError(f"max_iters must be >= 1, got {kmeans_iters}")
@@ -134,9 +141,10 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
     rc = _lib.lib().svgear_forward(
         C.byref(shape), qb.data_ptr(), kb.data_ptr(), vb.data_ptr(), q_init.data_ptr(),
         k_init.data_ptr(), int(kmeans_iters), _EST[estimator],
-        entry_capacity(float(budget), n_q * n_k), _OVERSHOOT[overshoot],
-        1 if single_item_fallback else 0,
-        _lib.EXEC_FP32_CHECK if check_fp32 else _lib.EXEC_BF16_TENSOR, out.data_ptr(),
+        0 if budget_mode == "perClusterTopP" else entry_capacity(float(budget), n_q * n_k),
+        _OVERSHOOT[overshoot], 1 if single_item_fallback else 0,
+        _lib.EXEC_FP32_CHECK if check_fp32 else _lib.EXEC_BF16_TENSOR,
+        float(budget) if budget_mode == "perClusterTopP" else 0.0, out.data_ptr(),
         mask.data_ptr(), C.byref(aux_c) if aux_c is not None else None, ws.data_ptr(),
         ws.numel() * ws.element_size(), stream_ptr())
     _lib.check("svgear_forward", rc)

@@ -116,9 +116,32 @@ def route_error_aware(table: BlockErrorTable, budget: DensityBudget, *, q_centro
             single_item_fallback=single_item_fallback)
     if q_centroids is None or k_centroids is None:
         raise ValueError("perClusterTopP routing needs q_centroids and k_centroids")
-    raise NotImplementedError(
-        "perClusterTopP routing is a 'next' row of the hot-path scope (SURVEY.md §8 f1); "
-        "only globalDensity runs on the GPU in this round")
+    if not size_weighted_scores:
+        raise NotImplementedError("only size-weighted scores run on the GPU path")
+    if budget.overshoot not in _OVERSHOOT:
+        raise ValueError(f"unknown overshoot policy {budget.overshoot!r}")
+    dev = require_cuda()
+    err = torch.as_tensor(table.error_sum).to(dev, torch.float64).contiguous()
+    qc = torch.as_tensor(q_centroids).to(dev, torch.float32).contiguous()
+    kc = torch.as_tensor(k_centroids).to(dev, torch.float32).contiguous()
+    was_2d = err.ndim == 2
+    if was_2d:
+        err, qc, kc = err.unsqueeze(0), qc.unsqueeze(0), kc.unsqueeze(0)
+    bh, c_q, c_k = err.shape
+    d = qc.shape[-1]
+    qs = torch.as_tensor(table.q_sizes).to(dev, torch.int32).view(bh, c_q).contiguous()
+    ks = torch.as_tensor(table.k_sizes).to(dev, torch.int32).view(bh, c_k).contiguous()
+    n_q, n_k = int(qs[0].long().sum()), int(ks[0].long().sum())
+    shape = _lib.Shape(bh, n_q, n_k, d, c_q, c_k)
+    mask = torch.empty((bh, c_q, c_k), dtype=torch.uint8, device=dev)
+    entries = torch.empty((bh,), dtype=torch.int64, device=dev)
+    ws = workspace(bh * c_q * c_k * 8 + 1024, dev)
+    rc = _lib.lib().svgear_route_error_aware_top_p(
+        C.byref(shape), err.data_ptr(), qc.data_ptr(), kc.data_ptr(), qs.data_ptr(), ks.data_ptr(),
+        float(budget.p), _OVERSHOOT[budget.overshoot], 1 if single_item_fallback else 0, mask.data_ptr(),
+        entries.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr())
+    _lib.check("svgear_route_error_aware_top_p", rc)
+    return _finish(mask, entries, n_q * n_k, was_2d)
 
 
 def route_score(q_centroids, k_centroids, q_sizes, k_sizes, budget: DensityBudget, *,

@@ -282,6 +282,40 @@ class TestRouter:
             mm = float((host(m.selected) != g[f"mask_score_{tag(r)}"]).mean())
             assert mm == 0.0, (name, r, mm)
 
+    def test_top_p_budget_matches_reference(self, gcase):  # router.py:172-190, golden from the reference
+        name, g = gcase
+        t = P.BlockErrorTable(error_sum=torch.from_numpy(g["err_stream"]),
+                              q_sizes=torch.from_numpy(g["q_sizes"]).int(),
+                              k_sizes=torch.from_numpy(g["k_sizes"]).int(),
+                              stabilizers=None, mode="valueAware", flops=0)
+        for p in (0.5, 0.85, 1.0):
+            m = P.route_error_aware(t, P.DensityBudget.top_p(p), q_centroids=g["q_centroids"],
+                                    k_centroids=g["k_centroids"])
+            mm = float((host(m.selected) != g[f"mask_topp_{tag(p)}"]).mean())
+            if name == "dups_d64":   # exactly tied masses: report the rate, bound it
+                assert mm <= 0.25, (name, p, mm)
+            else:
+                assert mm == 0.0, (name, p, mm)
+
+    def test_top_p_large_table_against_oracle(self):
+        rng = np.random.default_rng(12)
+        cq, ck, d = 60, 1000, 64
+        qs = rng.integers(50, 500, size=cq)
+        ks = rng.integers(2, 160, size=ck)
+        err = rng.random((cq, ck)) ** 4 * np.outer(qs, ks)
+        qc = O.round_to_bf16(rng.normal(size=(cq, d))).astype(np.float32)
+        kc = O.round_to_bf16(rng.normal(size=(ck, d)) * 2.0).astype(np.float32)
+        t = P.BlockErrorTable(error_sum=torch.from_numpy(err), q_sizes=torch.from_numpy(qs).int(),
+                              k_sizes=torch.from_numpy(ks).int(), stabilizers=None, mode="valueAware", flops=0)
+        o = SimpleNamespace(error_sum=err, q_sizes=qs, k_sizes=ks)
+        for p, ov in ((0.3, P.FILL_REMAINDER), (0.85, P.FILL_REMAINDER), (0.85, P.STOP_AT_FIRST_OVERFLOW), (1.0, P.FILL_REMAINDER)):
+            m = P.route_error_aware(t, P.DensityBudget.top_p(p, ov), q_centroids=qc, k_centroids=kc)
+            want = O.route_error_aware_top_p(o, qc.astype(np.float64), kc.astype(np.float64), p, overshoot=ov)
+            mm = float((host(m.selected) != want.selected).mean())
+            assert mm <= 1e-4, (p, ov, mm)   # a cumulative mass within one ulp of p may flip one block
+            if mm == 0.0:
+                assert m.density_entries == want.density_entries
+
     def test_large_table_against_oracle(self):
         rng = np.random.default_rng(9)
         cq, ck = 300, 1000
@@ -550,3 +584,28 @@ class TestBudgetSweep:
             wins += e["ear"] <= e["score"] * 1.001
         assert wins >= len(rhos) - 1, errs
         assert errs[-1]["ear"] <= errs[0]["ear"]  # more exact budget never hurts on this instance
+
+
+# --------------------------------------------------------------------------------------------
+# fused operator with the per-query-cluster top-p budget (the paper's production mode, p = 0.85)
+# --------------------------------------------------------------------------------------------
+class TestOperatorTopP:
+    @pytest.mark.parametrize("p", [0.5, 0.85])
+    def test_matches_oracle_composition(self, p):
+        S, d, cq, ck = 2048, 64, 16, 40
+        qf, kf, vf = (O.round_to_bf16(t) for t in O.blob_instance(S, S, d, cq, ck, 0.1, 3))
+        out, mask, aux = P.svg_ear_attention(dev(qf)[None, None], dev(kf)[None, None], dev(vf)[None, None], cq, ck,
+                                             p, budget_mode="perClusterTopP", seed=3, check_fp32=True,
+                                             return_aux=True)
+        prep = O.prepare(qf, kf, vf, cq, ck, seed=3)
+        assert np.array_equal(host(aux["q_perm"][0, 0]), prep.q_model.permutation)
+        assert np.array_equal(host(aux["k_perm"][0, 0]), prep.k_model.permutation)
+        table = O.build_error_table(prep, "valueAware")
+        want_mask = O.route_error_aware_top_p(table, prep.q_model.centroids, prep.k_model.centroids, p)
+        mm = float((host(mask[0, 0]) != want_mask.selected).mean())
+        assert mm <= 0.01, mm
+        # output against the oracle executor run on the GPU's own mask (isolates mask ties)
+        o_out, _ = O.sparse_attend(prep.q, prep.k, prep.v, prep.q_model, prep.k_model, host(mask[0, 0]))
+        assert rel_l2(host(out[0, 0]), O.unpermute(o_out, prep.q_model)) <= TOL_FP32
+        with pytest.raises(ValueError):
+            P.svg_ear_attention(dev(qf), dev(kf), dev(vf), cq, ck, 0.0, budget_mode="perClusterTopP")
