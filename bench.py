@@ -313,8 +313,16 @@ def run_ours(args):
         t_att = stages["attend"] * 1e-3
         achieved = attend_flops / t_att / 1e12
         # the attend kernel is timed alone between events -> burst peak
+        # DRAM bytes of the attention launch from the committed ncu --set full capture
+        # (profiles/r01_ncu_full_summary.txt: 523.6 MB read + 141.0 MB written for 8 Wan2.2 heads);
+        # reported only for the workload and executor that capture was taken on
+        traffic = None
+        if args.workload == "wan2.2-720p" and not args.fp32_check and abs(args.rho - 0.25) < 1e-9:
+            traffic = (523.577344e6 + 141.025024e6) / 8.0 * hl
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk["tf_burst"], "unit": "TFLOP/s",
-                "frac": achieved / pk["tf_burst"], "traffic": None,
+                "frac": achieved / pk["tf_burst"], "traffic": traffic,
+                "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum, 8-head capture scaled by heads"
+                                  if traffic else None,
                 "kernel": "attend_fp32_kernel" if args.fp32_check else "attend_tc_kernel",
                 "algorithmic_flops_per_launch": attend_flops, "peak_source": pk["source"] + " (burst)"}
 

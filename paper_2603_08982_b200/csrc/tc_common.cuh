@@ -24,16 +24,6 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-// TMA tile::gather4: rows r0..r3 (dim 1) x the tensor map's box columns starting at `col` -> smem
-// (4 x 128 B, SWIZZLE_128B applied by the hardware); completes `bytes` on the mbarrier.
-__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* tm, int col, int r0, int r1, int r2,
-                                            int r3, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-      "l"(tm), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
-      : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t"
@@ -225,9 +215,5 @@ __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 12
 
 
 }  // namespace tc
-
-// Host: 2-D bf16 row-major tensor map [rows][cols], box = 64 columns x 1 row, SWIZZLE_128B — the
-// shape tile::gather4 wants (each instruction then names 4 rows).  Returns false on failure.
-bool make_row_gather_map(CUtensorMap* tm, const void* base, uint64_t rows, uint32_t cols);
 
 }  // namespace svg
