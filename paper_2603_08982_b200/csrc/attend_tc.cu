@@ -321,25 +321,39 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       TMEM_LD32(tS + 32, sb);       // columns 32-63 load under the arithmetic on sa
       auto block = [&](uint32_t(&v)[32], int col0, int pk0) {
         if (kind == 0) {
-          // half of the exponentials go to the MUFU, half to the FMA pipe (packed polynomial): the
-          // MUFU alone (16/clk/SM) would need as long as the tile's MMAs
+          // three of four column pairs take their exponential on the MUFU, the fourth on the FMA pipe
+          // (packed polynomial): the mix that minimises the block time with two softmax warps per SM
+          // sub-partition (tools/micro/softmax_block.cu; the MUFU alone, 16/clk/SM, would need as long
+          // as the tile's MMAs)
           const uint64_t sc2 = pack2(scale_log2e, scale_log2e), nm2 = pack2(-mu, -mu);
           uint64_t acc01 = pack2(0.f, 0.f), acc23 = pack2(0.f, 0.f);
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float v0 = __uint_as_float(v[j]), v1 = __uint_as_float(v[j + 1]);
-            const float v2 = __uint_as_float(v[j + 2]), v3 = __uint_as_float(v[j + 3]);
-            x0 = fmaxf(x0, fmaxf(v0, v1));
-            x1 = fmaxf(x1, fmaxf(v2, v3));
-            float a0, a1, p0, p1, p2, p3;
-            unpack2(ffma2(pack2(v0, v1), sc2, nm2), a0, a1);
-            p0 = ex2(a0);
-            p1 = ex2(a1);
-            exp2_poly2(ffma2(pack2(v2, v3), sc2, nm2), p2, p3);
-            acc01 = fadd2(acc01, pack2(p0, p1));
-            acc23 = fadd2(acc23, pack2(p2, p3));
-            pk[pk0 + j / 2] = pack_bf16x2(p0, p1);
-            pk[pk0 + j / 2 + 1] = pack_bf16x2(p2, p3);
+          for (int j = 0; j < 32; j += 8) {
+            float vv[8], p[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) vv[e] = __uint_as_float(v[j + e]);
+            x0 = fmaxf(x0, fmaxf(vv[0], vv[1]));
+            x1 = fmaxf(x1, fmaxf(vv[2], vv[3]));
+            x0 = fmaxf(x0, fmaxf(vv[4], vv[5]));
+            x1 = fmaxf(x1, fmaxf(vv[6], vv[7]));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint64_t xx = ffma2(pack2(vv[2 * q], vv[2 * q + 1]), sc2, nm2);
+              if (q == 3) {
+                exp2_poly2(xx, p[6], p[7]);
+              } else {
+                float a0, a1;
+                unpack2(xx, a0, a1);
+                p[2 * q] = ex2(a0);
+                p[2 * q + 1] = ex2(a1);
+              }
+            }
+            acc01 = fadd2(acc01, pack2(p[0], p[1]));
+            acc23 = fadd2(acc23, pack2(p[2], p[3]));
+            acc01 = fadd2(acc01, pack2(p[4], p[5]));
+            acc23 = fadd2(acc23, pack2(p[6], p[7]));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pk[pk0 + j / 2 + q] = pack_bf16x2(p[2 * q], p[2 * q + 1]);
           }
           float s0, s1, s2, s3;
           unpack2(acc01, s0, s1);
