@@ -10,7 +10,43 @@ using namespace svg;
 
 namespace svg {
 long long g_launches = 0;
+
+namespace {
+constexpr int kHelperSlots = 2;
+std::mutex g_helper_mu[kHelperSlots];
+cudaStream_t g_helper_stream[kHelperSlots] = {nullptr, nullptr};
+cudaEvent_t g_helper_fork[kHelperSlots] = {nullptr, nullptr}, g_helper_join[kHelperSlots] = {nullptr, nullptr};
+}  // namespace
+
+HelperFork::HelperFork(cudaStream_t main, int slot) : main_(main), side_(nullptr), slot_(slot), ok_(false), joined_(false) {
+  g_helper_mu[slot_].lock();
+  if (!g_helper_stream[slot_]) {
+    if (cudaStreamCreateWithFlags(&g_helper_stream[slot_], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_helper_fork[slot_], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_helper_join[slot_], cudaEventDisableTiming) != cudaSuccess) {
+      g_helper_stream[slot_] = nullptr;
+      (void)cudaGetLastError();
+      return;
+    }
+  }
+  side_ = g_helper_stream[slot_];
+  ok_ = cudaEventRecord(g_helper_fork[slot_], main_) == cudaSuccess &&
+        cudaStreamWaitEvent(side_, g_helper_fork[slot_], 0) == cudaSuccess;
 }
+
+int HelperFork::join() {
+  if (joined_) return SVGEAR_OK;
+  joined_ = true;
+  int rc = SVGEAR_OK;
+  if (ok_ && (cudaEventRecord(g_helper_join[slot_], side_) != cudaSuccess ||
+              cudaStreamWaitEvent(main_, g_helper_join[slot_], 0) != cudaSuccess))
+    rc = SVGEAR_ECUDA;
+  g_helper_mu[slot_].unlock();
+  return rc;
+}
+
+HelperFork::~HelperFork() { (void)join(); }
+}  // namespace svg
 
 namespace {
 
@@ -320,38 +356,25 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
   int rc;
   // (1) cluster Q and K independently; V follows K (analysis.py:228-238).  The two sides share
   // nothing, and the late Lloyd iterations are short latency-bound launches, so the key side is
-  // forked onto a helper stream; the join below makes the caller's stream the only one anything
-  // downstream depends on.  The helper stream and its two events are created once per process
-  // (stream creation can serialise with running work, so it is kept out of the per-call path).
-  static std::mutex fork_mu;
-  static cudaStream_t side = nullptr;
-  static cudaEvent_t fork = nullptr, join = nullptr;
+  // forked onto a helper stream (HelperFork, common.cuh); the join makes the caller's stream the
+  // only one anything downstream depends on.
   int rc_k = SVGEAR_ECUDA;
   rc = SVGEAR_ECUDA;
   {
-    std::lock_guard<std::mutex> lock(fork_mu);
-    if (!side) {
-      if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess) {
-        side = nullptr;
-        return SVGEAR_ECUDA;
-      }
-    }
-    if (cudaEventRecord(fork, st) == cudaSuccess && cudaStreamWaitEvent(side, fork, 0) == cudaSuccess) {
-      rc_k = launch_kmeans(exec_mode, s.bh, s.n_k, s.d, s.c_k, (const bf16*)k, k_init, kmeans_iters, k_assign,
-                           k_perm, k_sizes, k_offsets, k_cent, k_iters, nullptr, p.km2, side);
-      if (!rc_k) rc_k = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)k, k_perm, p.kp, side);
-      if (!rc_k) rc_k = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)v, k_perm, p.vp, side);
-      if (!rc_k)
-        rc_k = launch_segment_means(s.bh, s.n_k, s.d, s.c_k, p.vp, k_sizes, k_offsets, v_cent, nullptr, side);
-      rc = launch_kmeans(exec_mode, s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign,
-                         q_perm, q_sizes, q_offsets, q_cent, q_iters, nullptr, p.km, st);
-      if (!rc) rc = launch_gather_rows(s.bh, s.n_q, s.d, (const bf16*)q, q_perm, p.qp, st);
-      // join unconditionally so that the helper stream never outlives the caller's ordering
-      if (cudaEventRecord(join, side) != cudaSuccess || cudaStreamWaitEvent(st, join, 0) != cudaSuccess)
-        rc = SVGEAR_ECUDA;
-    }
+    HelperFork fk(st, 0);
+    if (!fk.ok()) return SVGEAR_ECUDA;
+    cudaStream_t side = fk.side();
+    rc_k = launch_kmeans(exec_mode, s.bh, s.n_k, s.d, s.c_k, (const bf16*)k, k_init, kmeans_iters, k_assign,
+                         k_perm, k_sizes, k_offsets, k_cent, k_iters, nullptr, p.km2, side);
+    if (!rc_k) rc_k = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)k, k_perm, p.kp, side);
+    if (!rc_k) rc_k = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)v, k_perm, p.vp, side);
+    if (!rc_k)
+      rc_k = launch_segment_means(s.bh, s.n_k, s.d, s.c_k, p.vp, k_sizes, k_offsets, v_cent, nullptr, side);
+    rc = launch_kmeans(exec_mode, s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign,
+                       q_perm, q_sizes, q_offsets, q_cent, q_iters, nullptr, p.km, st);
+    if (!rc) rc = launch_gather_rows(s.bh, s.n_q, s.d, (const bf16*)q, q_perm, p.qp, st);
+    // join unconditionally so that the helper stream never outlives the caller's ordering
+    if (fk.join() != SVGEAR_OK) rc = SVGEAR_ECUDA;
   }
   if (rc) return rc;
   if (rc_k) return rc_k;

@@ -19,14 +19,14 @@ namespace {
 
 constexpr int BM = 256;      // query rows per CTA: two M=128 halves that share every K/V tile
 constexpr int BN = 64;       // keys per tile
-constexpr int NTHREADS = 384;
+constexpr int threads_for(int halves) { return (4 * halves + 2 + halves) * 32; }  // softmax + 2 producers + issuers
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
-template <int D, int NS>
+template <int D, int NS, int HALVES>
 struct Smem {
-  static constexpr int kQBytes = BM * D * 2;
+  static constexpr int kQBytes = HALVES * 128 * D * 2;
   static constexpr int kTileBytes = BN * D * 2;
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kQBytes;             // NS stages
@@ -86,8 +86,8 @@ __device__ __forceinline__ void tma_box(uint32_t dst, const CUtensorMap* tm, int
 // and is the A operand of P.V straight from TMEM), O[half] at 256 + half*D.  S is double buffered
 // per half, so QK^T of tile t+1 runs under the softmax of tile t; the two halves interleave on the
 // tensor pipe.  The running maximum is only raised when it grows by more than 2^8 (lazy rescale).
-template <int D, int NS>
-__global__ void __launch_bounds__(NTHREADS, 1)
+template <int D, int NS, int HALVES>
+__global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
     attend_tc_kernel(const __grid_constant__ TmaSet tm, int oob_row,
                      const float* __restrict__ lnw, const int32_t* __restrict__ q_perm,
                      const int32_t* __restrict__ k_sizes, const int32_t* __restrict__ k_offsets,
@@ -95,13 +95,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                      const int32_t* __restrict__ tile_count, int max_tiles, int n_q, int n_k, int c_q,
                      int c_k, int ckpad, float scale_log2e, bf16* __restrict__ out,
                      float* __restrict__ lse) {
-  using L = Smem<D, NS>;
+  using L = Smem<D, NS, HALVES>;
+  constexpr int halves = HALVES;
+  constexpr int kSoftWarps = 4 * HALVES, kWarpK = kSoftWarps, kWarpV = kSoftWarps + 1, kWarpMma = kSoftWarps + 2;
+  constexpr int kTmemCols = 256 * HALVES, kOBase = 128 * HALVES;
   using B = Bars<NS>;
   const int h = blockIdx.y;
   if ((int)blockIdx.x >= tile_count[h]) return;
   const int32_t* te = tile_list + ((size_t)h * max_tiles + blockIdx.x) * 4;
   const int qcl = te[0], row0 = te[1], nrows = te[2];
-  const int halves = nrows > 128 ? 2 : 1;
+  if ((nrows > 128) != (HALVES == 2)) return;  // the other instantiation owns this tile
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -134,7 +137,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_init(bar(B::ODONE + 1), 1);
     fence_barrier_init();
   }
-  if (warp == 10) tmem_alloc(smem_u32(tmem_slot), 512);
+  if (warp == kWarpMma) tmem_alloc(smem_u32(tmem_slot), kTmemCols);
   const uint8_t* mrow = mask + ((size_t)h * c_q + qcl) * c_k;
   if (warp == 0) {
     // compact the selected key clusters of this query cluster: (first row, key-count prefix)
@@ -163,8 +166,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       s_total[0] = total;
       s_total[1] = nsel;
     }
-  } else if (warp >= 1 && warp <= 7) {
-    for (int j = tid - 32; j < ckpad; j += 224)
+  } else if (warp >= 1 && warp < kSoftWarps) {
+    for (int j = tid - 32; j < ckpad; j += (kSoftWarps - 1) * 32)
       s_bias[j] = (j < c_k && mrow[j] == 0) ? lnw[(size_t)h * c_k + j] * kLog2e : -INFINITY;
   }
   tc_fence_before();
@@ -176,9 +179,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int n_cent = ckpad / BN;
   const int T = n_exact + n_cent;
 
-  if (warp == 8 || warp == 9) {
+  if (warp == kWarpK || warp == kWarpV) {
     // =========================== producers: K (warp 8) / Q then V (warp 9), one elected thread ===
-    const bool is_k = warp == 8;
+    const bool is_k = warp == kWarpK;
     if (elect_one()) {
       const CUtensorMap* maps = is_k ? tm.k : tm.v;
       const CUtensorMap* cmap = is_k ? &tm.kbar : &tm.vbar;
@@ -239,17 +242,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= 10) {
+  } else if (warp >= kWarpMma) {
     // =========================== MMA issuers: warp 10 -> half 0, warp 11 -> half 1 =============
     // One elected thread per half runs its own QK^T / P.V sequence, so a barrier round trip of one
     // half never stalls the other half's MMAs; K/V stages are released by both (count = halves).
-    const int hf = warp - 10;
+    const int hf = warp - kWarpMma;
     if (hf < halves && elect_one()) {
       constexpr uint32_t idesc_qk = make_idesc(128, BN, 0);
       constexpr uint32_t idesc_pv = make_idesc(128, D, 1);
       const uint32_t qb = sQ + (uint32_t)(hf * (128 * D * 2));
       const uint32_t tSb = tmem + (uint32_t)(hf * 128);
-      const uint32_t tO = tmem + (uint32_t)(256 + hf * D);
+      const uint32_t tO = tmem + (uint32_t)(kOBase + hf * D);
       auto issue_qk = [&](int t) {
         const int st = t % NS;
         mbar_wait(bar(B::KFULL + st), (t / NS) & 1);
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int hf = warp >> 2;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t tSb = tmem + lane_base + (uint32_t)(hf * 128);
-    const uint32_t tO = tmem + lane_base + (uint32_t)(256 + hf * D);
+    const uint32_t tO = tmem + lane_base + (uint32_t)(kOBase + hf * D);
     const int b_sfull = B::SFULL + hf * 2, b_pfull = B::PFULL + hf * 2, b_odone = B::ODONE + hf;
     float m = -INFINITY, l = 0.f;
     // The S tile is consumed as two 32-column blocks; the TMEM load of the next block is always in
@@ -481,9 +484,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_before();
   }
   __syncthreads();
-  if (warp == 10) {
+  if (warp == kWarpMma) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, kTmemCols);
   }
 }
 
@@ -512,18 +515,31 @@ static bool encode_rows_map(CUtensorMap* tm, const void* base, uint64_t rows, in
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int D, int NS>
+template <int D, int NS2, int NS1>
 static int launch_attend_tc_ns(const SvgEarShape& s, const TmaSet& tm, const int32_t* q_perm,
                                const int32_t* k_sizes, const int32_t* k_offsets, const uint8_t* mask, bf16* out,
                                float* lse, AttendScratch& sc, int ckpad, int mt, float scale_log2e,
                                cudaStream_t st) {
-  const size_t smem = Smem<D, NS>::bytes(ckpad);
-  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  attend_tc_kernel<D, NS><<<dim3(mt, s.bh), NTHREADS, smem, st>>>(
+  HelperFork fk(st, 1);
+  if (!fk.ok()) return SVGEAR_ECUDA;
+  cudaStream_t side = fk.side();
+  // tiles with more than 128 live rows: one CTA per SM, two halves sharing every K/V tile
+  const size_t smem2 = Smem<D, NS2, 2>::bytes(ckpad);
+  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  attend_tc_kernel<D, NS2, 2><<<dim3(mt, s.bh), threads_for(2), smem2, st>>>(
       tm, s.bh * s.n_k, sc.lnw, q_perm, k_sizes, k_offsets, mask, sc.tile_list, sc.tile_count, mt, s.n_q, s.n_k,
       s.c_q, s.c_k, ckpad, scale_log2e, out, lse);
   SVG_LAUNCH_OK();
-  return SVGEAR_OK;
+  // remainder tiles (<= 128 live rows): one half per CTA, two CTAs co-resident per SM so that one
+  // CTA's softmax runs under the other's MMAs.  The two kernels write disjoint rows; the second is
+  // forked onto a helper stream so that its CTAs fill the tail of the first instead of following it.
+  const size_t smem1 = Smem<D, NS1, 1>::bytes(ckpad);
+  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+  attend_tc_kernel<D, NS1, 1><<<dim3(mt, s.bh), threads_for(1), smem1, side>>>(
+      tm, s.bh * s.n_k, sc.lnw, q_perm, k_sizes, k_offsets, mask, sc.tile_list, sc.tile_count, mt, s.n_q, s.n_k,
+      s.c_q, s.c_k, ckpad, scale_log2e, out, lse);
+  SVG_LAUNCH_OK();
+  return fk.join();
 }
 
 int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const bf16* vp,
@@ -545,15 +561,15 @@ int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const
   ok = ok && encode_rows_map(&tm.q, qp, (uint64_t)s.bh * s.n_q, s.d, 64);
   if (!ok) return SVGEAR_ECUDA;
   const size_t cap = 227 * 1024;
-#define SVG_TRY(DD, NSS)                                                                                 \
-  if (s.d == DD && Smem<DD, NSS>::bytes(ckpad) <= cap)                                                   \
-    return launch_attend_tc_ns<DD, NSS>(s, tm, q_perm, k_sizes, k_offsets, mask, out, lse, sc, ckpad, mt, \
-                                        scale_log2e, st);
-  SVG_TRY(128, 4)
-  SVG_TRY(128, 3)
-  SVG_TRY(128, 2)
-  SVG_TRY(64, 4)
-  SVG_TRY(64, 2)
+#define SVG_TRY(DD, N2, N1)                                                                               \
+  if (s.d == DD && Smem<DD, N2, 2>::bytes(ckpad) <= cap && 2 * Smem<DD, N1, 1>::bytes(ckpad) <= cap)      \
+    return launch_attend_tc_ns<DD, N2, N1>(s, tm, q_perm, k_sizes, k_offsets, mask, out, lse, sc, ckpad, mt, \
+                                           scale_log2e, st);
+  SVG_TRY(128, 4, 2)
+  SVG_TRY(128, 3, 2)
+  SVG_TRY(128, 2, 2)
+  SVG_TRY(64, 4, 4)
+  SVG_TRY(64, 2, 2)
 #undef SVG_TRY
   return SVGEAR_EUNSUPPORTED;
 }

@@ -87,6 +87,25 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Fork/join onto a process-wide helper stream (api.cu).  Independent pieces of one call (the two
+// k-means sides; the two attention kernels) run concurrently: the constructor makes helper stream
+// `slot` wait for everything enqueued on `main` so far, join() makes `main` wait for the helper.
+// The helper streams and events are created once (stream creation can serialise with running
+// work); a per-slot mutex keeps concurrent host threads from interleaving their fork/join pairs.
+// Event based, so the pattern is capturable in a CUDA graph.
+class HelperFork {
+ public:
+  HelperFork(cudaStream_t main, int slot);
+  ~HelperFork();
+  bool ok() const { return ok_; }
+  cudaStream_t side() const { return side_; }
+  int join();  // SVGEAR_OK or SVGEAR_ECUDA; idempotent
+ private:
+  cudaStream_t main_, side_;
+  int slot_;
+  bool ok_, joined_;
+};
+
 // ---- stage launchers (defined in the per-stage .cu files) -------------------------------------
 
 struct KmeansScratch {
