@@ -130,6 +130,8 @@ struct KmeansScratch {
   int32_t* ticket;        // [bh]     block ticket counter of sizes_hist_kernel
   int32_t* has_empty;     // [bh]     some cluster is empty after this iteration's assignment
   int32_t* resid_nz;      // [bh]     the second bf16 piece of some centre is non-zero
+  float* dmin;            // [bh][c]  distance from each centre to the nearest big mover (movers_kernel)
+  float2* movers;         // [bh]     {number of big movers (0: none), max movement of the other centres}
   bool carve(Carver& cv, int bh, int n, int c, int d);
 };
 

@@ -640,6 +640,8 @@ bool KmeansScratch::carve(Carver& cv, int bh, int n, int c, int d) {
   ticket = cv.take<int32_t>(bh);
   has_empty = cv.take<int32_t>(bh);
   resid_nz = cv.take<int32_t>(bh);
+  dmin = cv.take<float>((size_t)bh * c);
+  movers = cv.take<float2>(bh);
   return cv.ok;
 }
 

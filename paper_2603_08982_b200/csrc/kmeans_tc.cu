@@ -113,10 +113,100 @@ __global__ void token_norm_kernel(const bf16* __restrict__ x, int d, long long t
 // Block 0 of each instance also resets the per-iteration counters (sizes, changed, dirty).
 // ------------------------------------------------------------------------------------------------
 constexpr int kFilterTokens = 2048;  // tokens per CTA
+constexpr int kMaxMovers = 64;
+
+// A few centres that moved far — typically clusters refilled by the empty-cluster repair, whose centre
+// jumps onto the donor token — would push EVERY token's lower bound below its upper bound through
+// the global max-movement term.  Per instance this kernel separates the big movers
+// L = {j : move[j] > max_move / 4} (used only when |L| <= kMaxMovers) and gives every cluster a the
+// distance from its (new) centre to the nearest big mover e != a.  For a token x of cluster a,
+//     dist(x, c_e) >= dist(c_a, c_e) - dist(x, c_a) >= dmin[a] - ub(x)      (triangle inequality)
+// so the filter may charge only the movement of the REMAINING centres to the lower bound:
+//     lb <- min(lb - max_{j not in L} move[j],  dmin[a] - ub).
+// info[h] = {|L| (0 = plain Hamerly), max movement outside L}.
+__global__ void __launch_bounds__(256)
+    movers_kernel(int c, int d, const float* __restrict__ cent, const float* __restrict__ move,
+                  float* __restrict__ dmin, float2* __restrict__ info, const int32_t* __restrict__ done) {
+  const int h = blockIdx.y;
+  if (done[h]) return;
+  extern __shared__ float s_mc[];  // [kMaxMovers][d] centres of the big movers
+  __shared__ int s_list[kMaxMovers];
+  __shared__ int s_n;
+  __shared__ float s_red[8];
+  __shared__ float s_m1, s_rest;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // every block of the instance derives the same mover set (32 clusters per block below)
+  const float* mv = move + (size_t)h * c;
+  float m = 0.f;
+  for (int j = tid; j < c; j += 256) m = fmaxf(m, mv[j]);
+  m = warp_max(m);
+  if (lane == 0) s_red[warp] = m;
+  if (tid == 0) s_n = 0;
+  __syncthreads();
+  if (tid == 0) {
+    float v = s_red[0];
+    for (int w = 1; w < 8; ++w) v = fmaxf(v, s_red[w]);
+    s_m1 = v;
+  }
+  __syncthreads();
+  const float thr = s_m1 * 0.25f;
+  float rest = 0.f;
+  for (int j = tid; j < c; j += 256) {
+    const float v = mv[j];
+    if (v > thr && s_m1 > 0.f) {
+      const int pos = atomicAdd(&s_n, 1);
+      if (pos < kMaxMovers) s_list[pos] = j;
+    } else {
+      rest = fmaxf(rest, v);
+    }
+  }
+  rest = warp_max(rest);
+  __syncthreads();
+  if (lane == 0) s_red[warp] = rest;
+  __syncthreads();
+  if (tid == 0) {
+    float v = s_red[0];
+    for (int w = 1; w < 8; ++w) v = fmaxf(v, s_red[w]);
+    s_rest = v;
+  }
+  __syncthreads();
+  const int nl = s_n;
+  if (nl == 0 || nl > kMaxMovers || c <= nl) {  // no outliers (or too many): plain Hamerly
+    if (tid == 0 && blockIdx.x == 0) info[h] = make_float2(0.f, 0.f);
+    return;
+  }
+  for (int i = tid; i < nl * d; i += 256) s_mc[i] = cent[((size_t)h * c + s_list[i / d]) * d + i % d];
+  __syncthreads();
+  // 8 lanes per cluster (d/8 consecutive elements each), 4 clusters per warp, 32 per block
+  const int a = blockIdx.x * 32 + warp * 4 + (lane >> 3), sub = lane & 7, epl = d / 8;
+  const int aa = min(a, c - 1);
+  float ca[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) ca[k] = k < epl ? cent[((size_t)h * c + aa) * d + sub * epl + k] : 0.f;
+  float best = INFINITY;
+  for (int q = 0; q < nl; ++q) {
+    const float* mc = s_mc + q * d + sub * epl;
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (k < epl) {
+        const float df = ca[k] - mc[k];
+        acc = fmaf(df, df, acc);
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    if (s_list[q] != aa) best = fminf(best, acc);
+  }
+  if (a < c && sub == 0) dmin[(size_t)h * c + a] = sqrtf(best) * (1.0f - 1.0f / 65536.0f);
+  if (tid == 0 && blockIdx.x == 0) info[h] = make_float2((float)nl, s_rest);
+}
 
 __global__ void __launch_bounds__(256)
     bound_filter_kernel(int n, int c, int all_active, const int32_t* __restrict__ assign,
-                        const float* __restrict__ move, const float* __restrict__ cnorm,
+                        const float* __restrict__ move, const float* __restrict__ dmin,
+                        const float2* __restrict__ info, const float* __restrict__ cnorm,
                         const float* __restrict__ xnorm, float* __restrict__ ub, float* __restrict__ lb,
                         int32_t* __restrict__ active, int32_t* __restrict__ nactive,
                         int32_t* __restrict__ sizes, int32_t* __restrict__ changed,
@@ -166,6 +256,9 @@ __global__ void __launch_bounds__(256)
   // movements are rounded fp32 norms: inflate them slightly so the bounds stay bounds
   constexpr float kInfl = 1.0f + 1.0f / 65536.0f;
   m1 *= kInfl; m2 *= kInfl;
+  const float2 inf = info[h];
+  const bool movers = inf.x > 0.f;  // big movers handled through the inter-centre bound (movers_kernel)
+  const float mrest = inf.y * kInfl;
   for (int t0 = lo; t0 < hi; t0 += 256) {
     const int t = t0 + tid;
     bool act = false;
@@ -173,7 +266,7 @@ __global__ void __launch_bounds__(256)
       const size_t g = (size_t)h * n + t;
       const int a = assign[g];
       const float u = ub[g] + move[(size_t)h * c + a] * kInfl;
-      const float l = lb[g] - (a == a1 ? m2 : m1);
+      const float l = movers ? fminf(lb[g] - mrest, dmin[(size_t)h * c + a] - u) : lb[g] - (a == a1 ? m2 : m1);
       ub[g] = u;
       lb[g] = l;
       // squared-space margin: the evaluated distances carry an absolute error of a few
@@ -459,8 +552,13 @@ int launch_kmeans_assign_tc(int bh, int n, int d, int c, int iter, bool full_eva
                                                                            sc.cnorm_pad, sc.resid_nz, sc.done);
   SVG_LAUNCH_OK();
   const int all_active = (iter == 0 || full_eval) ? 1 : 0;
+  if (!all_active) {
+    movers_kernel<<<dim3(ceil_div(c, 32), bh), 256, (size_t)kMaxMovers * d * sizeof(float), st>>>(c, d, cent, sc.move, sc.dmin, sc.movers,
+                                                                         sc.done);
+    SVG_LAUNCH_OK();
+  }
   bound_filter_kernel<<<dim3(ceil_div(n, kFilterTokens), bh), 256, 0, st>>>(
-      n, c, all_active, assign, sc.move, cnorm, sc.xnorm, sc.ub, sc.lb, sc.active, sc.nactive, sizes,
+      n, c, all_active, assign, sc.move, sc.dmin, sc.movers, cnorm, sc.xnorm, sc.ub, sc.lb, sc.active, sc.nactive, sizes,
       sc.changed, sc.dirty, sc.done);
   SVG_LAUNCH_OK();
   static int num_sms = 0;
