@@ -407,13 +407,17 @@ def stage_times(torch, P, _lib, q, k, v, cq, ck, args, reps):
         vc = P.segment_means(vp, km); mark("segment_means")
         table = P.estimate_errors_streaming(qm, km, kp, vp); mark("error_table")
         mask = R.route_error_aware(table, R.DensityBudget.global_density(args.rho)); mark("route")
+        # keep the GPU busy for ~2 ms while the host enqueues the executor (tile list, tensor maps,
+        # launches), so that the event pair below brackets device time only, not host latency
+        torch.cuda._sleep(4_000_000); mark("_spin")
         res = P.sparse_attend(qp, kp, vp, qm, km, mask, v_centroids=vc, unpermute=True,
                               dtype=torch.float32 if args.fp32_check else torch.bfloat16); mark("attend")
         torch.cuda.synchronize()
         if rep == 0:
             continue  # warm-up
         for (_, a), (name, b) in zip(marks, marks[1:]):
-            acc[name] = acc.get(name, 0.0) + a.elapsed_time(b) / reps
+            if not name.startswith("_"):
+                acc[name] = acc.get(name, 0.0) + a.elapsed_time(b) / reps
         flops = float(res.flops.exact_block + res.flops.compensation)
         density = float(mask.density.double().mean())
         iters = {"q_max": int(rq["iters"].max()), "k_max": int(rk["iters"].max())}
