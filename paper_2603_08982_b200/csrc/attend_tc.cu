@@ -562,7 +562,7 @@ int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const
   if (!ok) return SVGEAR_ECUDA;
   const size_t cap = 227 * 1024;
 #define SVG_TRY(DD, N2, N1)                                                                               \
-  if (s.d == DD && Smem<DD, N2, 2>::bytes(ckpad) <= cap && 2 * Smem<DD, N1, 1>::bytes(ckpad) <= cap)      \
+  if (s.d == DD && Smem<DD, N2, 2>::bytes(ckpad) <= cap && Smem<DD, N1, 1>::bytes(ckpad) <= cap)          \
     return launch_attend_tc_ns<DD, N2, N1>(s, tm, q_perm, k_sizes, k_offsets, mask, out, lse, sc, ckpad, mt, \
                                            scale_log2e, st);
   SVG_TRY(128, 4, 2)

@@ -391,6 +391,19 @@ class TestExecutor:
             _, o_lse = O.sparse_attend(qp, kp, vp, qm, km, sel)
             assert np.abs(host(res.lse) - o_lse).max() <= (1e-4 if dtype == torch.float32 else 2e-2)
 
+    def test_many_key_clusters(self):
+        # c_k = 2500 (> 1024): longer selection lists in shared memory, fewer pipeline stages
+        rng = np.random.default_rng(21)
+        n_q, n_k, d, c_q, c_k = 600, 6000, 64, 3, 2500
+        q, k, v = (O.round_to_bf16(rng.normal(size=s)) for s in ((n_q, d), (n_k, d), (n_k, d)))
+        prep = P.prepare(dev(q), dev(k), dev(v), c_q, c_k, seed=1, max_iters=3)
+        qm, km = np_model(prep.q_model), np_model(prep.k_model)
+        sel = rng.random((c_q, c_k)) < 0.3
+        mask = P.mask_from_selected(torch.from_numpy(sel).cuda(), self._sizes(prep))
+        res = P.sparse_attend(prep.q, prep.k, prep.v, prep.q_model, prep.k_model, mask, dtype=torch.bfloat16)
+        want = O.mixed_logit_output(q[qm.permutation], k[km.permutation], v[km.permutation], qm, km, sel)
+        assert rel_l2(host(res.output.float()), want) <= TOL_BF16
+
     def test_unpermute_scatters_rows(self):
         prep, qm, km, qp, kp, vp = self._instance(9)
         mask = P.mask_from_selected((torch.rand(4, 6) < 0.5).cuda(), self._sizes(prep))
