@@ -62,14 +62,6 @@ struct TmaSet {
   CUtensorMap q;      // [bh*n_q][D] bf16, box {64, 64}
 };
 
-// 2-D tiled bulk tensor load: box at (col, row) -> shared memory, completes tx bytes on `bar`
-__device__ __forceinline__ void tma_box(uint32_t dst, const CUtensorMap* tm, int col, int row, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(tm), "r"(col), "r"(row), "r"(bar)
-      : "memory");
-}
-
 }  // namespace
 
 // One CTA = up to 256 consecutive rows of one query cluster (tile list built by build_tiles_kernel),
@@ -495,7 +487,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 // [rows][d] bf16 row-major, box = 64 columns x box_rows rows, SWIZZLE_128B, zero fill out of bounds
-static bool encode_rows_map(CUtensorMap* tm, const void* base, uint64_t rows, int d, int box_rows) {
+bool encode_rows_map(CUtensorMap* tm, const void* base, uint64_t rows, int d, int box_rows) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     void* p = nullptr;

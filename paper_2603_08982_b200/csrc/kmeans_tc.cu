@@ -292,8 +292,8 @@ __global__ void __launch_bounds__(256)
 //   warp 10   : token-tile producer
 template <int D>
 __global__ void __launch_bounds__(KTHREADS, 1)
-    assign_tc_kernel(const bf16* __restrict__ x, const bf16* __restrict__ pieces,
-                     const float* __restrict__ cnorm_pad, const float* __restrict__ xnorm, int bh, int n,
+    assign_tc_kernel(const __grid_constant__ CUtensorMap pieces_map, const bf16* __restrict__ x,
+                     const float* __restrict__ cnorm_pad, const float* __restrict__ xnorm, int bh, int head0, int n,
                      int c, int cpad, int cpad16, int first_iter, int32_t* __restrict__ assign,
                      float* __restrict__ own_d2, float* __restrict__ ub, float* __restrict__ lb,
                      const int32_t* __restrict__ active, const int32_t* __restrict__ nactive,
@@ -362,41 +362,31 @@ __global__ void __launch_bounds__(KTHREADS, 1)
   };
 
   if (warp == 8) {
-    // =========================== centroid-piece producer ========================================
-    constexpr int CPR = D / 8, RPI = 32 / CPR;
-    const int sub = lane / CPR, chunk = lane % CPR;
-    int u = 0;  // running unit counter across items
-    for (int it = 0; it < my_items; ++it) {
-      int tile_unused;
-      const int h = locate(it, tile_unused);
-      const int np = resid_nz[h] ? kPieces : 1;  // pieces that are not identically zero
-      const int U = NT * np;                      // pipeline units of this item
-      for (int uu = 0; uu < U; ++uu, ++u) {
-        const int st = u % KSTAGES;
-        if (u >= KSTAGES) mbar_wait(bar(KB_BEMPTY + st), ((u / KSTAGES) - 1) & 1);
-        const int nt = uu / np, p = uu % np;
-        const int nn = min(KN, cpad16 - nt * KN);
-        const bf16* bsrc = pieces + (((size_t)h * kPieces + p) * cpad + (size_t)nt * KN) * D;
-        const uint32_t dst = sB + (uint32_t)st * L::kBBytes;
-        for (int r0 = 0; r0 < nn; r0 += RPI) {
-          const int r = r0 + sub;
-          cp_async16(dst + (uint32_t)((chunk >> 3) * (KN * 128)) + swz(r, chunk & 7),
-                     bsrc + (size_t)r * D + chunk * 8);
-        }
-        cp_async_commit();
-        // keep one group in flight: unit u-1 has landed after this wait
-        asm volatile("cp.async.wait_group %0;" ::"n"(KSTAGES - 2) : "memory");
-        if (u >= 1) {
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar(KB_BFULL + (u - 1) % KSTAGES));
+    // =========================== centroid-piece producer (TMA, one elected thread) ==============
+    // pieces are a plain [instance][piece][cpad][D] bf16 matrix: one 128-row x 64-column box per
+    // slab lands in the canonical SWIZZLE_128B layout (the previous 2048 16-byte cp.async per unit
+    // cost ~2000 clk of issue time per unit — twice the unit's MMA time)
+    if (elect_one()) {
+      int u = 0;  // running unit counter across items
+      for (int it = 0; it < my_items; ++it) {
+        int tile_unused;
+        const int h = locate(it, tile_unused);
+        const int np = resid_nz[h] ? kPieces : 1;  // pieces that are not identically zero
+        const int U = NT * np;                      // pipeline units of this item
+        for (int uu = 0; uu < U; ++uu, ++u) {
+          const int st = u % KSTAGES;
+          if (u >= KSTAGES) mbar_wait(bar(KB_BEMPTY + st), ((u / KSTAGES) - 1) & 1);
+          const int nt = uu / np, p = uu % np;
+          const uint32_t dst = sB + (uint32_t)st * L::kBBytes;
+          const uint32_t fb = bar(KB_BFULL + st);
+          mbar_expect_tx(fb, (uint32_t)L::kBBytes);
+          const int row = ((head0 + h) * kPieces + p) * cpad + nt * KN;
+#pragma unroll
+          for (int sl = 0; sl < D / 64; ++sl) tma_box(dst + (uint32_t)(sl * (KN * 128)), &pieces_map, sl * 64, row, fb);
         }
       }
     }
-    cp_async_wait_all();
-    fence_proxy_async();
     __syncwarp();
-    if (lane == 0 && u >= 1) mbar_arrive(bar(KB_BFULL + (u - 1) % KSTAGES));
   } else if (warp == 10) {
     // =========================== token-tile producer (A operand, double buffered) ===============
     constexpr int CPR = D / 8, RPI = 32 / CPR;
@@ -475,36 +465,62 @@ __global__ void __launch_bounds__(KTHREADS, 1)
       const int t = __ldg(active + (size_t)h * n + min(ti, na - 1));
       const float xn = xnorm[(size_t)h * n + t];
       const float* cn = cnorm_pad + (size_t)h * cpad;
-      float best = INFINITY, second = INFINITY;
-      int bi = 0;
+      // Two independent (min, first index, runner-up) chains over the even / odd columns halve the
+      // serial compare-select dependency; they are merged once per token below.  |x|^2 is a
+      // per-token constant of the arg-min, so the loop ranks w = |c|^2 - 2 x.c and the clip at zero
+      // is applied once to the winner.  (The reference clips every entry, clustering.py:62; that
+      // only matters when two DIFFERENT centroids are both within rounding of the token, and
+      // identical centroids still tie exactly here.)
+      float best0 = INFINITY, best1 = INFINITY, sec0 = INFINITY, sec1 = INFINITY;
+      int bi0 = 0, bi1 = 1;
+      auto rank32 = [&](const uint32_t(&a)[32], int cb) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const float w0 = fmaf(-2.0f, __uint_as_float(a[j]), __ldg(cn + cb + j));
+          const float w1 = fmaf(-2.0f, __uint_as_float(a[j + 1]), __ldg(cn + cb + j + 1));
+          sec0 = fminf(sec0, fmaxf(w0, best0));  // runner-up distance (lower bound for skipping)
+          sec1 = fminf(sec1, fmaxf(w1, best1));
+          // strict: ties keep the lowest cluster index (NaN from stale columns never wins)
+          if (w0 < best0) { best0 = w0; bi0 = cb + j; }
+          if (w1 < best1) { best1 = w1; bi1 = cb + j + 1; }
+        }
+      };
       for (int nt = 0; nt < NT; ++nt, ++g) {
         const int buf = g & 1;
         mbar_wait(bar(KB_ACCFULL + buf), (g >> 1) & 1);
         tc_fence_after();
         const uint32_t tcol = tmem + lane_base + (uint32_t)(buf * 256 + m * 128);
         const int nn = min(KN, cpad16 - nt * KN);
-        for (int c4 = 0; c4 < nn; c4 += 32) {  // a narrow last tile leaves stale columns: norm = +inf there
-          uint32_t a[32];
-          TMEM_LD32(tcol + c4, a);
+        const int cb = nt * KN;
+        // 32-column chunks, the TMEM load of the next chunk in flight under the ranking of the
+        // current one (a narrow last tile leaves stale columns: their norm is +inf)
+        uint32_t a0[32], a1[32];
+        TMEM_LD32(tcol, a0);
+        tc_wait_ld();
+        if (nn > 32) TMEM_LD32(tcol + 32, a1);
+        rank32(a0, cb);
+        if (nn > 32) {
           tc_wait_ld();
-          const int cb = nt * KN + c4;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            // |x|^2 is a per-token constant of the arg-min, so the loop ranks w = |c|^2 - 2 x.c and
-            // the clip at zero is applied once to the winner below.  (The reference clips every
-            // entry, clustering.py:62; that only matters when two DIFFERENT centroids are both
-            // within rounding of the token, and identical centroids still tie exactly here.)
-            const float w = fmaf(-2.0f, __uint_as_float(a[j]), __ldg(cn + cb + j));
-            second = fminf(second, fmaxf(w, best));  // runner-up distance (lower bound for skipping)
-            if (w < best) {  // strict: ties keep the lowest cluster index (NaN from stale columns never wins)
-              best = w;
-              bi = cb + j;
+          if (nn > 64) TMEM_LD32(tcol + 64, a0);
+          rank32(a1, cb + 32);
+          if (nn > 64) {
+            tc_wait_ld();
+            if (nn > 96) TMEM_LD32(tcol + 96, a1);
+            rank32(a0, cb + 64);
+            if (nn > 96) {
+              tc_wait_ld();
+              rank32(a1, cb + 96);
             }
           }
         }
         tc_fence_before();
         mbar_arrive(bar(KB_ACCEMPTY + buf));
       }
+      // merge the chains: lower value wins, equal values keep the lower index
+      const bool odd = best1 < best0 || (best1 == best0 && bi1 < bi0);
+      const float best = odd ? best1 : best0;
+      const int bi = odd ? bi1 : bi0;
+      const float second = fminf(fminf(sec0, sec1), odd ? best0 : best1);
       if (ti < na) {
         const size_t gi = (size_t)h * n + t;
         const float d2 = fmaxf(xn + best, 0.f);
@@ -567,12 +583,13 @@ int launch_kmeans_assign_tc(int bh, int n, int d, int c, int iter, bool full_eva
     SVG_CUDA_OK(cudaGetDevice(&dev));
     SVG_CUDA_OK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  CUtensorMap pieces_map;
+  if (!encode_rows_map(&pieces_map, sc.pieces, (uint64_t)bh * kPieces * cpad, d, KN)) return SVGEAR_ECUDA;
   for (int h0 = 0; h0 < bh; h0 += kMaxHeads) {
     const int nb = bh - h0 < kMaxHeads ? bh - h0 : kMaxHeads;
     const int items = nb * ceil_div(n, KM);  // upper bound; the kernel reads the real counts
     const int grid = items < num_sms ? items : num_sms;
     const bf16* xs = x + (size_t)h0 * n * d;
-    const bf16* ps = sc.pieces + (size_t)h0 * kPieces * cpad * d;
     const float* cs = sc.cnorm_pad + (size_t)h0 * cpad;
     const float* xns = sc.xnorm + (size_t)h0 * n;
     int32_t* as = assign + (size_t)h0 * n;
@@ -584,12 +601,12 @@ int launch_kmeans_assign_tc(int bh, int n, int d, int c, int iter, bool full_eva
     if (d == 128) {
       const size_t smem = KSmem<128>::bytes();
       SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      assign_tc_kernel<128><<<grid, KTHREADS, smem, st>>>(xs, ps, cs, xns, nb, n, c, cpad, cpad16, iter == 0, as, os,
+      assign_tc_kernel<128><<<grid, KTHREADS, smem, st>>>(pieces_map, xs, cs, xns, nb, h0, n, c, cpad, cpad16, iter == 0, as, os,
                                                           us, ls, al, sc.nactive + h0, dt, sc.resid_nz + h0, sc.done + h0);
     } else {
       const size_t smem = KSmem<64>::bytes();
       SVG_CUDA_OK(cudaFuncSetAttribute(assign_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      assign_tc_kernel<64><<<grid, KTHREADS, smem, st>>>(xs, ps, cs, xns, nb, n, c, cpad, cpad16, iter == 0, as, os,
+      assign_tc_kernel<64><<<grid, KTHREADS, smem, st>>>(pieces_map, xs, cs, xns, nb, h0, n, c, cpad, cpad16, iter == 0, as, os,
                                                          us, ls, al, sc.nactive + h0, dt, sc.resid_nz + h0, sc.done + h0);
     }
     SVG_LAUNCH_OK();

@@ -36,6 +36,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "}" ::"r"(bar), "r"(parity)
       : "memory");
 }
+// 2-D tiled bulk tensor load: box at (col, row) -> shared memory, completes tx bytes on `bar`
+__device__ __forceinline__ void tma_box(uint32_t dst, const CUtensorMap* tm, int col, int row, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(tm), "r"(col), "r"(row), "r"(bar)
+      : "memory");
+}
+
 // non-blocking phase test
 __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
   uint32_t ok;
@@ -215,5 +223,9 @@ __device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * 12
 
 
 }  // namespace tc
+
+// Host: tensor map of a [rows][d] bf16 row-major matrix, box = 64 columns x box_rows rows,
+// SWIZZLE_128B, zero fill out of bounds (attend_tc.cu).  Returns false on failure.
+bool encode_rows_map(CUtensorMap* tm, const void* base, uint64_t rows, int d, int box_rows);
 
 }  // namespace svg
