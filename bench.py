@@ -236,7 +236,14 @@ def run_ours(args):
     # copy stream (heads are independent instances, so the grouping does not change any result of
     # a head except the device-side seeding draw, which is keyed by the instance index).
     n_groups = 4 if (hl >= 8 and world == 1) else 1
-    bounds = [hl * g // n_groups for g in range(n_groups + 1)]
+    if n_groups == 1:
+        bounds = [0, hl]
+    else:
+        # a small first group lets compute start early; the rest is split evenly (big groups run the
+        # latency-bound stages more efficiently)
+        first = max(1, hl // 10)
+        rest = hl - first
+        bounds = [0] + [first + rest * g // (n_groups - 1) for g in range(n_groups)]
     copy_stream = torch.cuda.Stream(device=dev)   # host -> device
     back_stream = torch.cuda.Stream(device=dev)   # device -> host (PCIe is full duplex)
     gmax = max(bounds[g + 1] - bounds[g] for g in range(n_groups))
