@@ -321,11 +321,12 @@ def run_ours(args):
         achieved = attend_flops / t_att / 1e12
         # the attend kernel is timed alone between events -> burst peak
         # DRAM bytes of the attention launch from the committed ncu --set full capture
-        # (profiles/r01_ncu_full_summary.txt: 523.6 MB read + 141.0 MB written for 8 Wan2.2 heads);
+        # (profiles/r01_ncu_full_summary.txt, 8 Wan2.2 heads: two-half kernel 522.4 MB read + 138.6 MB
+        # written, remainder-tile kernel 402.0 MB read + 4.8 MB written (cold L2 under ncu));
         # reported only for the workload and executor that capture was taken on
         traffic = None
         if args.workload == "wan2.2-720p" and not args.fp32_check and abs(args.rho - 0.25) < 1e-9:
-            traffic = (523.577344e6 + 141.025024e6) / 8.0 * hl
+            traffic = (522.377472e6 + 138.584832e6 + 402.021376e6 + 4.755200e6) / 8.0 * hl
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk["tf_burst"], "unit": "TFLOP/s",
                 "frac": achieved / pk["tf_burst"], "traffic": traffic,
                 "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum, 8-head capture scaled by heads"
