@@ -46,8 +46,9 @@ struct Bars {
   static constexpr int VEMPTY = VFULL + NS;    // [NS]
   static constexpr int SFULL = VEMPTY + NS;    // [half][buffer]
   static constexpr int PFULL = SFULL + 4;      // [half][buffer]
-  static constexpr int ODONE = PFULL + 4;      // [half]
-  static constexpr int COUNT = ODONE + 2;
+  static constexpr int ODONE = PFULL + 4;      // [half]  one phase per tile (O rescale inside the loop)
+  static constexpr int OFINAL = ODONE + 2;     // [half]  single phase: every P.V of the CTA has landed
+  static constexpr int COUNT = OFINAL + 2;
 };
 
 // Tensor maps of one launch (passed as a __grid_constant__ kernel parameter).  K and V (permuted,
@@ -127,6 +128,8 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
     }
     mbar_init(bar(B::ODONE), 1);
     mbar_init(bar(B::ODONE + 1), 1);
+    mbar_init(bar(B::OFINAL), 1);
+    mbar_init(bar(B::OFINAL + 1), 1);
     fence_barrier_init();
   }
   if (warp == kWarpMma) tmem_alloc(smem_u32(tmem_slot), kTmemCols);
@@ -283,6 +286,7 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
         umma_commit(bar(B::ODONE + hf));
         umma_commit(bar(B::VEMPTY + st));
       }
+      umma_commit(bar(B::OFINAL + hf));
     }
     __syncwarp();
   } else if ((warp >> 2) < halves) {
@@ -447,7 +451,12 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
       }
     }
     // ---- epilogue: O / l -> bf16 -> global, scattered to original token order -----------------
-    mbar_wait(bar(b_odone), (T - 1) & 1);
+    // The per-tile ODONE barrier cannot be used here: a parity wait only tells the current phase
+    // from the one before it, and right after the last P hand-off P.V(T-2) may still be in flight
+    // (inside the loop a thread holding S(t) knows P.V(t-2) has completed; nothing bounds the lag
+    // here), so a wait for phase T-1 could be satisfied by phase T-3 and O read two tiles early.
+    // OFINAL has a single phase, committed after the last P.V.
+    mbar_wait(bar(B::OFINAL + hf), 0);
     tc_fence_after();
     const int r = tid;  // row within the CTA tile (warps 0-7 <-> rows 0-255)
     const bool live = r < nrows;

@@ -622,3 +622,34 @@ class TestOperatorTopP:
         assert rel_l2(host(out[0, 0]), O.unpermute(o_out, prep.q_model)) <= TOL_FP32
         with pytest.raises(ValueError):
             P.svg_ear_attention(dev(qf), dev(kf), dev(vf), cq, ck, 0.0, budget_mode="perClusterTopP")
+
+
+# --------------------------------------------------------------------------------------------
+# randomized shapes: ragged sizes, tiny instances, cluster counts up to the token count
+# --------------------------------------------------------------------------------------------
+class TestRandomShapes:
+    @pytest.mark.parametrize("seed", list(range(12)))
+    def test_executor_and_lloyd_on_random_shapes(self, seed):
+        rng = np.random.default_rng(1000 + seed)
+        d = int(rng.choice([64, 128]))
+        n_q, n_k = int(rng.integers(3, 700)), int(rng.integers(3, 900))
+        c_q, c_k = int(rng.integers(1, min(n_q, 12) + 1)), int(rng.integers(1, min(n_k, 40) + 1))
+        q, k, v = (O.round_to_bf16(rng.normal(size=s) * rng.uniform(0.3, 2.0)) for s in ((n_q, d), (n_k, d), (n_k, d)))
+        prep = P.prepare(dev(q), dev(k), dev(v), c_q, c_k, seed=seed)
+        qm, km = np_model(prep.q_model), np_model(prep.k_model)
+        # clustering invariants + agreement with the float64 oracle from the same seed
+        for mdl, n, c in ((qm, n_q, c_q), (km, n_k, c_k)):
+            assert sorted(mdl.permutation.tolist()) == list(range(n))
+            assert mdl.sizes.sum() == n and (mdl.sizes >= 1).all()
+            assert np.array_equal(mdl.permutation, np.argsort(mdl.assignments, kind="stable"))
+        ref = O.prepare(q, k, v, c_q, c_k, seed=seed)
+        mism = float((qm.assignments != ref.q_model.assignments).mean()) + float((km.assignments != ref.k_model.assignments).mean())
+        assert mism == 0.0, (n_q, n_k, c_q, c_k, d, mism)
+        # executor, both modes, arbitrary mask
+        sel = rng.random((c_q, c_k)) < rng.uniform(0.0, 1.0)
+        sizes = prep.q_model.sizes.long().unsqueeze(1) * prep.k_model.sizes.long().unsqueeze(0)
+        mask = P.mask_from_selected(torch.from_numpy(sel).cuda(), sizes)
+        want = O.mixed_logit_output(q[qm.permutation], k[km.permutation], v[km.permutation], qm, km, sel)
+        for dtype, tol in ((torch.float32, TOL_FP32), (torch.bfloat16, TOL_BF16)):
+            res = P.sparse_attend(prep.q, prep.k, prep.v, prep.q_model, prep.k_model, mask, dtype=dtype)
+            assert rel_l2(host(res.output.float()), want) <= tol, (n_q, n_k, c_q, c_k, d, str(dtype))
