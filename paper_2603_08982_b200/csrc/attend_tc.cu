@@ -264,9 +264,6 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
         umma_commit(bar(B::KEMPTY + st));
       };
       mbar_wait(bar(B::QFULL), 0);
-      // stagger the halves by one softmax pass so that the two softmax warps of an SM sub-partition
-      // are not in their exponential phase (or in their hand-off gap) at the same time
-      if (hf == 1) mbar_wait(bar(B::PFULL + 0), 0);
       issue_qk(0);
       for (int t = 0; t < T; ++t) {
         const int st = t % NS;
