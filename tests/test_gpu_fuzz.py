@@ -126,3 +126,58 @@ def test_operator_end_to_end(seed):
         assert ent == int(aux["mask_entries"][0, h]), info
         if mode == "globalDensity":
             assert ent <= P.entry_capacity(budget, len(q) * len(k)), info
+
+
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_error_table_and_routing_random_shapes(seed):
+    """Error table against the oracle ON THE GPU'S OWN clustering (so only the estimator is compared),
+    then both routing modes bit-exact against the oracle's router run on the GPU's table."""
+    rng = np.random.default_rng(9500 + seed)
+    q, k, v, c_q, c_k, d, kind = random_instance(rng, max_q=1500, max_k=2500, max_cq=40, max_ck=120)
+    prep = P.prepare(dev(q), dev(k), dev(v), c_q, c_k, seed=seed, max_iters=5)
+    qm, km = np_model(prep.q_model), np_model(prep.k_model)
+    ref_prep = SimpleNamespace(q_model=qm, k_model=km, q=q[qm.permutation].astype(np.float64),
+                               k=k[km.permutation].astype(np.float64), v=v[km.permutation].astype(np.float64))
+    info = (len(q), len(k), c_q, c_k, d, kind)
+    for mode in ("valueAware", "plain"):
+        got = host(P.build_error_table(prep, mode).error_sum)
+        want = O.build_error_table(ref_prep, mode).error_sum
+        assert np.isfinite(got).all() and (got >= 0).all(), info
+        assert np.abs(got - want).max() <= 5e-4 * max(want.max(), 1e-30), info + (mode,)
+    table = P.build_error_table(prep, "valueAware")
+    mine = SimpleNamespace(error_sum=host(table.error_sum), q_sizes=qm.sizes, k_sizes=km.sizes)
+    rho = float(rng.uniform(0.0, 1.0))
+    m = P.route_error_aware(table, P.DensityBudget.global_density(rho))
+    want = O.route_error_aware(mine, rho)
+    assert np.array_equal(host(m.selected), want.selected), info + (rho,)
+    assert m.density_entries == want.density_entries
+    p = float(rng.uniform(0.1, 1.0))
+    m = P.route_error_aware(table, P.DensityBudget.top_p(p), q_centroids=prep.q_model.centroids,
+                            k_centroids=prep.k_model.centroids)
+    want = O.route_error_aware_top_p(mine, qm.centroids, km.centroids, p)
+    mism = float((host(m.selected) != want.selected).mean())
+    assert mism <= (0.05 if kind == 2 else 2e-3), info + (p, mism)   # duplicates: exactly tied masses
+
+
+@pytest.mark.parametrize("seed", list(range(4)))
+def test_executor_medium_multi_tile(seed):
+    """Query clusters of several hundred to a few thousand rows: 256-row two-half CTA tiles plus the
+    one-half remainder kernel, several heads per launch."""
+    rng = np.random.default_rng(9900 + seed)
+    d = int(rng.choice([64, 128]))
+    n_q, n_k = int(rng.integers(1500, 5000)), int(rng.integers(1500, 5000))
+    c_q, c_k = int(rng.integers(2, 9)), int(rng.integers(8, 60))
+    H = 3
+    qs, ks, vs = (O.round_to_bf16(rng.normal(size=(H, n, d))) for n in (n_q, n_k, n_k))
+    prep = P.prepare(dev(qs), dev(ks), dev(vs), c_q, c_k, seed=seed, max_iters=4)
+    sel = rng.random((H, c_q, c_k)) < rng.uniform(0.1, 0.6)
+    sizes = prep.q_model.sizes.long().unsqueeze(-1) * prep.k_model.sizes.long().unsqueeze(-2)
+    mask = P.mask_from_selected(torch.from_numpy(sel).cuda(), sizes)
+    res = P.sparse_attend(prep.q, prep.k, prep.v, prep.q_model, prep.k_model, mask, dtype=torch.bfloat16)
+    for h in range(H):
+        qm = SimpleNamespace(**{f: host(getattr(prep.q_model, f)[h]).astype(np.int64 if f != "centroids" else np.float64)
+                                for f in ("assignments", "centroids", "sizes", "permutation", "offsets")}, num_clusters=c_q)
+        km = SimpleNamespace(**{f: host(getattr(prep.k_model, f)[h]).astype(np.int64 if f != "centroids" else np.float64)
+                                for f in ("assignments", "centroids", "sizes", "permutation", "offsets")}, num_clusters=c_k)
+        want = O.mixed_logit_output(qs[h][qm.permutation], ks[h][km.permutation], vs[h][km.permutation], qm, km, sel[h])
+        assert rel_l2(host(res.output[h].float()), want) <= 1e-2, (n_q, n_k, c_q, c_k, d, h)
