@@ -181,3 +181,18 @@ def test_executor_medium_multi_tile(seed):
                                 for f in ("assignments", "centroids", "sizes", "permutation", "offsets")}, num_clusters=c_k)
         want = O.mixed_logit_output(qs[h][qm.permutation], ks[h][km.permutation], vs[h][km.permutation], qm, km, sel[h])
         assert rel_l2(host(res.output[h].float()), want) <= 1e-2, (n_q, n_k, c_q, c_k, d, h)
+
+
+def test_run_to_run_determinism():
+    """No floating-point atomics, fixed-order reductions: repeated calls are bit-identical even
+    though the two k-means sides and the two attention kernels run concurrently."""
+    torch.manual_seed(5)
+    q, k, v = (torch.randn(1, 4, 7000, 128, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    ref = None
+    for rep in range(3):
+        out, mask, aux = P.svg_ear_attention(q, k, v, 24, 80, 0.3, init="device", return_aux=True)
+        cur = [out, mask, aux["q_perm"], aux["k_perm"], aux["k_centroids"], aux["error_table"], aux["lse"]]
+        if ref is None:
+            ref = [t.clone() for t in cur]
+        else:
+            assert all(torch.equal(a, b) for a, b in zip(cur, ref)), rep
