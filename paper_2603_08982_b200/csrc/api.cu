@@ -360,6 +360,7 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
   // only one anything downstream depends on.
   int rc_k = SVGEAR_ECUDA;
   rc = SVGEAR_ECUDA;
+  const bool keys_early = exec_mode == SVGEAR_EXEC_BF16_TENSOR;
   {
     HelperFork fk(st, 0);
     if (!fk.ok()) return SVGEAR_ECUDA;
@@ -370,6 +371,10 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
     if (!rc_k) rc_k = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)v, k_perm, p.vp, side);
     if (!rc_k)
       rc_k = launch_segment_means(s.bh, s.n_k, s.d, s.c_k, p.vp, k_sizes, k_offsets, v_cent, nullptr, side);
+    // the key-side half of the estimator needs nothing from the query side: keep it on the helper
+    // stream, under the (usually longer) query-side Lloyd loop
+    if (!rc_k && keys_early)
+      rc_k = launch_error_table_keys(s, estimator_mode, k_cent, v_cent, p.kp, p.vp, k_sizes, k_offsets, p.es, side);
     rc = launch_kmeans(exec_mode, s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign,
                        q_perm, q_sizes, q_offsets, q_cent, q_iters, nullptr, p.km, st);
     if (!rc) rc = launch_gather_rows(s.bh, s.n_q, s.d, (const bf16*)q, q_perm, p.qp, st);
@@ -380,7 +385,7 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
   if (rc_k) return rc_k;
   // (2) error table + routing
   rc = launch_error_table(s, exec_mode, estimator_mode, q_cent, k_cent, v_cent, p.kp, p.vp, q_sizes,
-                          k_sizes, k_offsets, err, stab, p.es, st);
+                          k_sizes, k_offsets, err, stab, p.es, st, keys_early);
   if (rc) return rc;
   if (top_p > 0.0) {  // per-query-cluster top-p budget (router.py:172-190); the key buffer holds the masses
     double* mass = reinterpret_cast<double*>(p.route_keys);

@@ -159,7 +159,10 @@ struct ErrScratch {
 int launch_error_table(const SvgEarShape& s, int exec_mode, int mode, const float* qc, const float* kc,
                        const float* vc, const bf16* kp, const bf16* vp, const int32_t* q_sizes,
                        const int32_t* k_sizes, const int32_t* k_offsets, double* err,
-                       float* stabilizers, ErrScratch& sc, cudaStream_t st);
+                       float* stabilizers, ErrScratch& sc, cudaStream_t st, bool key_stats_done = false);
+int launch_error_table_keys(const SvgEarShape& s, int mode, const float* kc, const float* vc, const bf16* kp,
+                            const bf16* vp, const int32_t* k_sizes, const int32_t* k_offsets, ErrScratch& sc,
+                            cudaStream_t st);
 
 int launch_route(int bh, int c_q, int c_k, const double* val, const int32_t* q_sizes,
                  const int32_t* k_sizes, int64_t capacity, int overshoot, int fallback,

@@ -348,28 +348,41 @@ size_t errtab_tc_scratch_bytes(const SvgEarShape& s) {
          align_up((size_t)s.bh * 2 * cqpad * s.d * 2, 256) + 1024;
 }
 
+// key-side half of the estimator (needs only the key clustering): k - k̄ split + per-key scalars
+int launch_key_stats(const SvgEarShape& s, int mode, const float* kc, const float* vc, const bf16* kp,
+                     const bf16* vp, const int32_t* k_sizes, const int32_t* k_offsets, bf16* kd_hi, bf16* kd_lo,
+                     float4* kstat, cudaStream_t st) {
+  if (s.d == 128)
+    key_stats_kernel<128><<<dim3(s.c_k, s.bh), 128, 0, st>>>(mode, kc, vc, kp, vp, k_sizes, k_offsets, s.n_k,
+                                                            s.c_k, kd_hi, kd_lo, kstat);
+  else
+    key_stats_kernel<64><<<dim3(s.c_k, s.bh), 128, 0, st>>>(mode, kc, vc, kp, vp, k_sizes, k_offsets, s.n_k,
+                                                           s.c_k, kd_hi, kd_lo, kstat);
+  SVG_LAUNCH_OK();
+  return SVGEAR_OK;
+}
+
 int launch_error_table_tc(const SvgEarShape& s, int mode, const float* qc, const float* kc, const float* vc,
                           const bf16* kp, const bf16* vp, const int32_t* q_sizes, const int32_t* k_sizes,
                           const int32_t* k_offsets, const float* sbar, const float* mref, bf16* kd_hi,
-                          bf16* kd_lo, float4* kstat, bf16* qsplit, double* err, cudaStream_t st) {
+                          bf16* kd_lo, float4* kstat, bf16* qsplit, double* err, bool key_stats_done,
+                          cudaStream_t st) {
   const int cqpad = ceil_div(s.c_q, EM) * EM;
   const float scale = 1.0f / sqrtf((float)s.d);
   split_q_kernel<<<dim3(ceil_div(cqpad * s.d, 256), s.bh), 256, 0, st>>>(qc, s.d, s.c_q, cqpad, qsplit);
   SVG_LAUNCH_OK();
+  if (!key_stats_done) {
+    const int rc = launch_key_stats(s, mode, kc, vc, kp, vp, k_sizes, k_offsets, kd_hi, kd_lo, kstat, st);
+    if (rc) return rc;
+  }
   dim3 grid(ceil_div(s.c_k, ERANGE), cqpad / EM, s.bh);
   if (s.d == 128) {
-    key_stats_kernel<128><<<dim3(s.c_k, s.bh), 128, 0, st>>>(mode, kc, vc, kp, vp, k_sizes, k_offsets, s.n_k,
-                                                            s.c_k, kd_hi, kd_lo, kstat);
-    SVG_LAUNCH_OK();
     const size_t smem = ESmem<128>::bytes();
     SVG_CUDA_OK(cudaFuncSetAttribute(error_table_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     error_table_tc_kernel<128><<<grid, ETHREADS, smem, st>>>(qsplit, kd_hi, kd_lo, kstat, q_sizes, k_sizes,
                                                              k_offsets, sbar, mref, s.n_k, s.c_q, s.c_k, cqpad,
                                                              scale, err);
   } else {
-    key_stats_kernel<64><<<dim3(s.c_k, s.bh), 128, 0, st>>>(mode, kc, vc, kp, vp, k_sizes, k_offsets, s.n_k,
-                                                           s.c_k, kd_hi, kd_lo, kstat);
-    SVG_LAUNCH_OK();
     const size_t smem = ESmem<64>::bytes();
     SVG_CUDA_OK(cudaFuncSetAttribute(error_table_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     error_table_tc_kernel<64><<<grid, ETHREADS, smem, st>>>(qsplit, kd_hi, kd_lo, kstat, q_sizes, k_sizes,

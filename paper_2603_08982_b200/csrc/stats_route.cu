@@ -201,7 +201,18 @@ __global__ void __launch_bounds__(256, 1)
 int launch_error_table_tc(const SvgEarShape& s, int mode, const float* qc, const float* kc, const float* vc,
                           const bf16* kp, const bf16* vp, const int32_t* q_sizes, const int32_t* k_sizes,
                           const int32_t* k_offsets, const float* sbar, const float* mref, bf16* kd_hi,
-                          bf16* kd_lo, float4* kstat, bf16* qsplit, double* err, cudaStream_t st);
+                          bf16* kd_lo, float4* kstat, bf16* qsplit, double* err, bool key_stats_done,
+                          cudaStream_t st);
+int launch_key_stats(const SvgEarShape& s, int mode, const float* kc, const float* vc, const bf16* kp,
+                     const bf16* vp, const int32_t* k_sizes, const int32_t* k_offsets, bf16* kd_hi, bf16* kd_lo,
+                     float4* kstat, cudaStream_t st);
+
+// key-side half of the tensor-core estimator, for callers that overlap it with the query side
+int launch_error_table_keys(const SvgEarShape& s, int mode, const float* kc, const float* vc, const bf16* kp,
+                            const bf16* vp, const int32_t* k_sizes, const int32_t* k_offsets, ErrScratch& sc,
+                            cudaStream_t st) {
+  return launch_key_stats(s, mode, kc, vc, kp, vp, k_sizes, k_offsets, sc.kd_hi, sc.kd_lo, sc.kstat, st);
+}
 
 bool ErrScratch::carve(Carver& cv, const SvgEarShape& s) {
   const int cqpad = ceil_div(s.c_q, 128) * 128;
@@ -216,7 +227,7 @@ bool ErrScratch::carve(Carver& cv, const SvgEarShape& s) {
 int launch_error_table(const SvgEarShape& s, int exec_mode, int mode, const float* qc, const float* kc,
                        const float* vc, const bf16* kp, const bf16* vp, const int32_t* q_sizes,
                        const int32_t* k_sizes, const int32_t* k_offsets, double* err,
-                       float* stabilizers, ErrScratch& sc, cudaStream_t st) {
+                       float* stabilizers, ErrScratch& sc, cudaStream_t st, bool key_stats_done) {
   const float scale = 1.0f / sqrtf((float)s.d);
   float* sbar = sc.sbar;
   centroid_logits_kernel<<<dim3(ceil_div(s.c_q, kLogitRows), s.bh), 256, 0, st>>>(qc, kc, s.d, s.c_q, s.c_k, scale, sbar,
@@ -224,7 +235,7 @@ int launch_error_table(const SvgEarShape& s, int exec_mode, int mode, const floa
   SVG_LAUNCH_OK();
   if (exec_mode == SVGEAR_EXEC_BF16_TENSOR)
     return launch_error_table_tc(s, mode, qc, kc, vc, kp, vp, q_sizes, k_sizes, k_offsets, sbar, stabilizers,
-                                 sc.kd_hi, sc.kd_lo, sc.kstat, sc.qsplit, err, st);
+                                 sc.kd_hi, sc.kd_lo, sc.kstat, sc.qsplit, err, key_stats_done, st);
   const int passes = ceil_div(s.c_q, 256);
   const int thr = min(256, max(128, ceil_div(ceil_div(s.c_q, passes), 32) * 32));
   if (s.d == 128)
