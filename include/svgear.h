@@ -11,8 +11,11 @@
  *
  * Conventions
  *  - plain pointers and sizes only; every pointer is a CUDA DEVICE pointer unless named `host_*`;
- *  - the caller owns every buffer including the workspace; the library allocates nothing that
- *    outlives a call and keeps no global state; outputs are written exactly once;
+ *  - the caller owns every buffer including the workspace; the library allocates no device memory
+ *    and outputs are written exactly once.  The only process-wide state is two helper streams (with
+ *    their fork/join events) created on first use: svgear_forward runs the key-side k-means, and
+ *    the attention executor its remainder-tile kernel, concurrently with the caller's stream and
+ *    joins them back before returning, so every result is ordered on `stream` alone;
  *  - all work is enqueued on `stream` (a cudaStream_t passed as void*), nothing synchronises the
  *    host; results are deterministic run to run (no floating-point atomics);
  *  - token matrices are row-major bf16 `[bh][n][d]`, d in {64,128}, d_v == d;
