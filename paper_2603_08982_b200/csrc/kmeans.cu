@@ -611,7 +611,6 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ x, const int32_t* _
 // ------------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------------
-size_t kmeans_tc_scratch_bytes(int bh, int n, int c, int d);
 int launch_token_norms(int bh, int n, int d, const bf16* x, float* xnorm, cudaStream_t st);
 int launch_kmeans_assign_tc(int bh, int n, int d, int c, int iter, bool full_eval, const bf16* x,
                             const float* cent, const float* cnorm, KmeansScratch& sc, int32_t* assign,
@@ -627,7 +626,7 @@ bool KmeansScratch::carve(Carver& cv, int bh, int n, int c, int d) {
   done = cv.take<int32_t>(bh);
   changed = cv.take<int32_t>(bh);
   const int cpad = ceil_div(c, 128) * 128;
-  pieces = cv.take<bf16>((size_t)bh * 3 * cpad * d);
+  pieces = cv.take<bf16>((size_t)bh * 2 * cpad * d);  // kPieces = 2 (kmeans_tc.cu)
   cnorm_pad = cv.take<float>((size_t)bh * cpad);
   xnorm = cv.take<float>((size_t)bh * n);
   ub = cv.take<float>((size_t)bh * n);

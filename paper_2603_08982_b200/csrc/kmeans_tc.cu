@@ -3,19 +3,19 @@
 // Reference step: clustering._sq_dists + argmin (clustering.py:55-62, 113):
 //     d2[t,c] = max(|x_t|^2 - 2 x_t.c_c + |c_c|^2, 0),  assign[t] = first argmin_c d2[t,c].
 // The x.c^T contraction is ~99.5 % of a Lloyd iteration.  Tokens are bf16 (exact); each fp32
-// centroid is split into kPieces bf16 pieces c = c0 + c1 (+ c2) so that sum_p x.c_p reproduces
-// the fp32 product to ~2^-24 with fp32 accumulation in TMEM — the pieces simply extend the K
-// dimension of one GEMM.  The epilogue (one thread per token) turns accumulator columns into
-// distances and keeps the running (min, first index), so the [n x C] distance matrix never
-// exists in memory.
+// centroid is split into kPieces = 2 bf16 pieces c = c0 + c1 so that sum_p x.c_p reproduces
+// the fp32 product to ~2^-17 relative with fp32 accumulation in TMEM — the pieces simply extend the
+// K dimension of one GEMM (one piece when the centres are bf16-exact).  The epilogue (one thread per
+// token) turns accumulator columns into distances and keeps the running (min, first index,
+// runner-up), so the [n x C] distance matrix never exists in memory.
 //
-// CTA = 256 tokens (two M=128 tiles) x all centroids, N tiles of 128.  Centroid-piece tiles
-// (32 KB at d=128) stream through a 4-stage cp.async pipeline; each piece tile is reused by both
-// M tiles, which keeps L2 traffic at 32 B/cycle/SM.  TMEM: 2 buffers x (2 M tiles x 128 columns)
-// = 512 columns, so the epilogue of N tile n overlaps the MMAs of N tile n+1.
+// Persistent kernel, work item = 256 ACTIVE tokens (two M=128 tiles, gathered through the active
+// list) x all centroids, N tiles of 128.  Centroid-piece tiles (32 KB at d=128) stream through a
+// 3-stage TMA ring; each piece tile is reused by both M tiles.  TMEM: 2 buffers x (2 M tiles x 128
+// columns) = 512 columns, so the epilogue of N tile n overlaps the MMAs of N tile n+1.
 //   warps 0-7 : epilogue (warp w -> M tile w/4, TMEM lanes 32*(w%4)..)
-//   warp  8   : producer (A token tiles once, then the centroid-piece tiles)
-//   warp  9   : TMEM allocator + single-thread MMA issuer
+//   warp  8   : centroid-piece producer (TMA)      warp 9 : TMEM allocator + MMA issuer
+//   warp 10   : token-tile producer (cp.async row gather)
 #include "tc_common.cuh"
 
 namespace svg {
@@ -554,12 +554,6 @@ __global__ void __launch_bounds__(KTHREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
-}
-
-size_t kmeans_tc_scratch_bytes(int bh, int n, int c, int d) {
-  const int cpad = ceil_div(c, KN) * KN;
-  return align_up((size_t)bh * kPieces * cpad * d * 2, 256) + align_up((size_t)bh * cpad * 4, 256) +
-         align_up((size_t)bh * n * 4, 256) + 1024;
 }
 
 int launch_token_norms(int bh, int n, int d, const bf16* x, float* xnorm, cudaStream_t st) {
