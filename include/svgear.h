@@ -216,6 +216,28 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
                    uint8_t* mask, const SvgEarAux* aux, void* workspace, size_t workspace_bytes,
                    void* stream);
 
+/* ---- the callers either side of the operator in a DiT attention block ----
+ * The reference stops at single (Q,K,V) matrices; the paper's deployment feeds
+ * the operator from a fused QKV projection with q/k RMSNorm and rotary embedding, and feeds its
+ * output to the output projection.  The projections are the caller's (library GEMMs); these two
+ * entries are the HBM-bound layout/normalisation steps between them and svgear_forward.          */
+enum { SVGEAR_NORM_NONE = 0, SVGEAR_NORM_HEAD = 1 /* RMS over d */, SVGEAR_NORM_TOKEN = 2 /* RMS over h*d */ };
+enum { SVGEAR_ROPE_NONE = 0, SVGEAR_ROPE_INTERLEAVED = 1 /* pairs (2i,2i+1) */, SVGEAR_ROPE_HALF_SPLIT = 2 /* pairs (i,i+d/2) */ };
+
+/* qkv [b][s][3][h][d] bf16 (the projection output) -> q, k, v [b][h][s][d] bf16.
+ *   q, k: y = x * rsqrt(mean(x^2) + eps) * weight (weights f32 [h*d]; mean over d or over h*d),
+ *   then tokens with index < rope_len are rotated by rope_cos/rope_sin f32 [rope_len][d/2]
+ *   (tokens >= rope_len, e.g. appended text tokens, are not rotated); fp32 arithmetic, one rounding.
+ *   h*d <= 8192.                                                                                 */
+int svgear_qkv_prologue(int32_t b, int32_t s, int32_t h, int32_t d, const void* qkv,
+                        int32_t norm_mode, const float* q_norm_weight, const float* k_norm_weight,
+                        float eps, int32_t rope_mode, int32_t rope_len, const float* rope_cos,
+                        const float* rope_sin, void* q, void* k, void* v, void* stream);
+
+/* x [b][h][s][d] bf16 (the operator's output) -> out [b][s][h][d] bf16 (the output projection's input) */
+int svgear_heads_to_tokens(int32_t b, int32_t s, int32_t h, int32_t d, const void* x, void* out,
+                           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,7 +15,7 @@ import threading
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_PATH = os.path.join(PKG_DIR, "libsvgear.so")
-SOURCES = ("api.cu", "kmeans.cu", "kmeans_tc.cu", "stats_route.cu", "errtab_tc.cu", "attend_ref.cu", "attend_tc.cu")
+SOURCES = ("api.cu", "kmeans.cu", "kmeans_tc.cu", "stats_route.cu", "errtab_tc.cu", "attend_ref.cu", "attend_tc.cu", "dit.cu")
 NVCC_FLAGS = (
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-shared", "-Xcompiler", "-fPIC",
@@ -26,6 +26,8 @@ EST_VALUE_AWARE, EST_PLAIN = 0, 1
 FILL_REMAINDER, STOP_AT_FIRST_OVERFLOW = 0, 1
 EXEC_BF16_TENSOR, EXEC_FP32_CHECK = 0, 1
 KMEANS_FULL_EVAL = 0x100
+NORM_NONE, NORM_HEAD, NORM_TOKEN = 0, 1, 2
+ROPE_NONE, ROPE_INTERLEAVED, ROPE_HALF_SPLIT = 0, 1, 2
 
 
 class SvgEarError(RuntimeError):
@@ -64,6 +66,8 @@ SIGNATURES = {
     "svgear_route_score": ([C.POINTER(Shape), _P, _P, _P, _P, _I64, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_route_error_aware_top_p": ([C.POINTER(Shape), _P, _P, _P, _P, _P, C.c_double, _I32, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_sparse_attend": ([C.POINTER(Shape), _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "svgear_qkv_prologue": ([_I32, _I32, _I32, _I32, _P, _I32, _P, _P, C.c_float, _I32, _I32, _P, _P, _P, _P, _P, _P], C.c_int),
+    "svgear_heads_to_tokens": ([_I32, _I32, _I32, _I32, _P, _P, _P], C.c_int),
     "svgear_forward": ([C.POINTER(Shape), _P, _P, _P, _P, _P, _I32, _I32, _I64, _I32, _I32, _I32, C.c_double, _P, _P, C.POINTER(Aux), _P, _SZ, _P], C.c_int),
 }
 
