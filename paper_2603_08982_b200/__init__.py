@@ -3,7 +3,10 @@ centroid compensation, as hand-written CUDA behind a C ABI (include/svgear.h).
 
 Public surface mirrors the hot-path part of the reference package `routedattn`:
     prepare, build_error_table, route_error_aware, sparse_attend  (the four-call composition)
-and adds the fused operator `svg_ear_attention` and head-parallel sharding helpers.
+and adds the fused operator `svg_ear_attention`, head-parallel sharding helpers, and the callers
+either side of the path (SURVEY §8 "next" rows): `schedule` (dense warm-up + warm-started k-means
+across denoising steps), `dit` (QKV prologue / attention block), `tensorio` + `config` + `cli`
+(QKVT container and the run / sweep / verify harness).
 """
 
 from ._lib import SvgEarError, build_library, lib as load_library
@@ -20,5 +23,9 @@ from .router import (FILL_REMAINDER, STOP_AT_FIRST_OVERFLOW, BlockMask, DensityB
                      entry_capacity, mask_from_selected, relaxed_objective, route_error_aware,
                      route_error_aware_entries, route_score)
 from .sharding import gather_heads, head_range, sharded_svg_ear_attention
+from .schedule import SvgEarStack, WarmupSchedule
+from .dit import SvgEarSelfAttention, heads_to_tokens, qkv_prologue, rope_table_3d
+from .tensorio import TensorFormatError, read_tensor_file, write_tensor_file
+from .config import ConfigError, RunConfig, apply_preset
 
 __version__ = "0.1.0"
