@@ -17,7 +17,11 @@
 // small residuals of tight clusters; a running maximum M of g (the reference's m_loc - s̄_ij)
 // keeps every exponential <= 1, and the final rescale exp(2(s̄_ij - m_ref + M)) is applied in
 // float64, the type of the reference's table.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace svg {
 
@@ -325,7 +329,10 @@ int launch_score_mass(const SvgEarShape& s, const float* qc, const float* kc,
 //   phase 2  fillRemainder: repeatedly take the highest-priority block after the cursor whose
 //            weight still fits (block-wide lexicographic arg-max), until none fits;
 //   phase 3  best-single-fitting-block fallback.
-// One CTA per instance; integer atomics only.
+// One thread-block CLUSTER per instance (the scans are issue bound, so a single CTA per instance left
+// the kernel at ~1 SM per head): every CTA scans its slice of the blocks into a local histogram, the
+// non-empty bins are merged into rank 0's totals through distributed shared memory, rank 0 picks the
+// digit and broadcasts it.  Integer atomics only.
 // ------------------------------------------------------------------------------------------------
 struct Prio {
   unsigned long long a;  // ord64(primary key)
@@ -339,6 +346,7 @@ __device__ __forceinline__ unsigned long long ord64(double v) {
 // 11-bit digits: a -> 6 passes, b -> 6 passes, c -> 3 passes.
 constexpr int kRouteBins = 2048;
 constexpr int kRoutePasses = 15;
+constexpr int kRouteMaxCluster = 8;
 __device__ __forceinline__ void pass_geom(int pass, int& field, int& shift, int& width) {
   if (pass < 12) {
     field = pass / 6;
@@ -375,7 +383,10 @@ __global__ void __launch_bounds__(1024)
                  const int32_t* __restrict__ k_sizes_all, long long capacity, int overshoot, int fallback,
                  uint8_t* __restrict__ mask_all, long long* __restrict__ entries_all, int pieces,
                  int piece_bits) {
-  const int h = blockIdx.x;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int R = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int h = blockIdx.x / R;
   const int nb = c_q * c_k;
   const double* val = val_all + (size_t)h * nb;
   const unsigned long long* keys = keys_all + (size_t)h * nb;
@@ -388,9 +399,12 @@ __global__ void __launch_bounds__(1024)
   int32_t* s_ks = s_dyn;                                                        // [c_k]
   unsigned int* s_hc = reinterpret_cast<unsigned int*>(s_dyn + ((c_k + 3) & ~3));  // [bins]
   unsigned int* s_hp = s_hc + kRouteBins;                                         // [pieces][bins]
+  // cluster totals (live on rank 0; with one CTA per instance the local arrays are the totals)
+  unsigned int* s_tc = R > 1 ? s_hp + pieces * kRouteBins : s_hc;                 // [bins]
+  unsigned int* s_tp = s_tc + kRouteBins;                                         // [pieces][bins]
   auto bin_weight = [&](int dg) -> unsigned long long {
     unsigned long long t = 0;
-    for (int q = 0; q < pieces; ++q) t += (unsigned long long)s_hp[q * kRouteBins + dg] << (q * piece_bits);
+    for (int q = 0; q < pieces; ++q) t += (unsigned long long)s_tp[q * kRouteBins + dg] << (q * piece_bits);
     return t;
   };
   auto bin_add = [&](unsigned int dg, unsigned long long wsum, unsigned int cnt) {
@@ -408,8 +422,15 @@ __global__ void __launch_bounds__(1024)
   __shared__ double s_redd[32];
   __shared__ long long s_base;
   __shared__ int s_flag;
+  // per-CTA partial results collected on rank 0 (phase 2 double-buffered by iteration parity)
+  __shared__ Prio s_cbest[2][kRouteMaxCluster];
+  __shared__ long long s_cbw[2][kRouteMaxCluster];
+  __shared__ double s_csum[kRouteMaxCluster], s_cbv[kRouteMaxCluster];
+  __shared__ long long s_cent[kRouteMaxCluster];
+  __shared__ int s_cbi[kRouteMaxCluster];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x;
+  const int gtid = rank * nthr + tid, gthr = R * nthr;  // this thread's slot among the cluster's threads
   for (int j = tid; j < c_k; j += nthr) s_ks[j] = k_sizes_all[(size_t)h * c_k + j];
   if (tid == 0) { s_pa = 0; s_pb = 0; s_pc = 0; s_base = 0; s_flag = 0; }
   __syncthreads();
@@ -422,12 +443,12 @@ __global__ void __launch_bounds__(1024)
     if (xb != yb) return xb > yb;
     return x.c > y.c;
   };
-  // iterate this thread's blocks b = tid, tid + nthr, ... keeping (row, col) incrementally
+  // iterate this thread's blocks b = gtid, gtid + gthr, ... keeping (row, col) incrementally
 #define FOR_BLOCKS(BODY)                                             \
   {                                                                  \
-    int qi_ = tid / c_k, kj_ = tid % c_k;                            \
-    const int dq_ = nthr / c_k, dk_ = nthr % c_k;                    \
-    for (int b = tid; b < nb; b += nthr) {                           \
+    int qi_ = gtid / c_k, kj_ = gtid % c_k;                          \
+    const int dq_ = gthr / c_k, dk_ = gthr % c_k;                    \
+    for (int b = gtid; b < nb; b += gthr) {                          \
       const long long w = (long long)qs[qi_] * (long long)s_ks[kj_]; \
       BODY                                                           \
       qi_ += dq_; kj_ += dk_;                                        \
@@ -442,7 +463,9 @@ __global__ void __launch_bounds__(1024)
     int field, shift, width;
     pass_geom(pass, field, shift, width);
     for (int k = tid; k < kRouteBins * (pieces + 1); k += nthr) s_hc[k] = 0u;  // counts + all pieces
-    __syncthreads();
+    if (R > 1 && rank == 0)
+      for (int k = tid; k < kRouteBins * (pieces + 1); k += nthr) s_tc[k] = 0u;
+    cluster.sync();  // totals are zero before any CTA merges into them
     const unsigned long long pa = s_pa, pb = s_pb;
     const unsigned int pc = s_pc;
     const int hs = shift + width;
@@ -483,7 +506,15 @@ __global__ void __launch_bounds__(1024)
       if (rc) bin_add(rd, rw, rc);
     }
     __syncthreads();
-    if (warp == 0) {
+    if (R > 1) {  // merge the non-empty local bins into rank 0's totals
+      unsigned int* t0 = cluster.map_shared_rank(s_tc, 0);
+      for (int k = tid; k < kRouteBins * (pieces + 1); k += nthr) {
+        const unsigned int x = s_hc[k];
+        if (x) atomicAdd(t0 + k, x);
+      }
+      cluster.sync();
+    }
+    if (rank == 0 && warp == 0) {
       // first bin (from the top) where the running weight exceeds the capacity: each lane owns 64
       // consecutive bins, lane 0 the highest
       const int nbins = 1 << width;
@@ -514,7 +545,7 @@ __global__ void __launch_bounds__(1024)
           for (int q = 0; q < per; ++q) {
             const int dg = hi - q;
             if (dg < 0) break;
-            if (s_hc[dg] == 0) continue;
+            if (s_tc[dg] == 0) continue;
             const long long bwt = (long long)bin_weight(dg);
             if (run + bwt > capacity) { found = dg; break; }
             run += bwt;
@@ -523,11 +554,20 @@ __global__ void __launch_bounds__(1024)
           if (field == 0) s_pa |= (unsigned long long)found << shift;
           else if (field == 1) s_pb |= (unsigned long long)found << shift;
           else s_pc |= (unsigned int)found << shift;
-          s_flag = (s_hc[found] == 1) ? 2 : 0;  // unique candidate -> it is the boundary block
+          s_flag = (s_tc[found] == 1) ? 2 : 0;  // unique candidate -> it is the boundary block
         }
       }
+      __syncwarp();
+      if (lane == 0)
+        for (int r = 1; r < R; ++r) {  // broadcast the decision
+          *cluster.map_shared_rank(&s_pa, r) = s_pa;
+          *cluster.map_shared_rank(&s_pb, r) = s_pb;
+          *cluster.map_shared_rank(&s_pc, r) = s_pc;
+          *cluster.map_shared_rank(&s_base, r) = s_base;
+          *cluster.map_shared_rank(&s_flag, r) = s_flag;
+        }
     }
-    __syncthreads();
+    cluster.sync();
     last_field = field; last_shift = shift;
     if (s_flag == 1) { all_fit = true; break; }
     if (s_flag == 2) break;
@@ -550,10 +590,14 @@ __global__ void __launch_bounds__(1024)
         if (last_field == 1) hit = (kb >> last_shift) == (pb >> last_shift);
         else hit = kb == pb && ((~(unsigned int)b) >> last_shift) == (pc >> last_shift);
       }
-      if (hit) { s_red[0].a = ka; s_red[0].c = ~(unsigned int)b; }  // exactly one writer
+      if (hit)  // exactly one writer in the cluster
+        for (int r = 0; r < R; ++r) {
+          Prio* dst = cluster.map_shared_rank(&s_red[0], r);
+          dst->a = ka; dst->c = ~(unsigned int)b;
+        }
       (void)w;
     })
-    __syncthreads();
+    cluster.sync();
     bound = s_red[0];
   }
   __syncthreads();
@@ -566,7 +610,7 @@ __global__ void __launch_bounds__(1024)
   // ---- phase 2: fillRemainder tail ------------------------------------------------------------------
   if (!all_fit && overshoot == SVGEAR_FILL_REMAINDER) {
     Prio cur = bound;
-    while (true) {
+    for (int it = 0;; ++it) {
       Prio best;
       best.a = 0; best.c = 0;
       long long bw = 0;
@@ -600,19 +644,30 @@ __global__ void __launch_bounds__(1024)
           const long long rw = __shfl_xor_sync(0xffffffffu, qw, o);
           if (r.a != 0 && (q.a == 0 || pgt(r, q))) { q = r; qw = rw; }
         }
-        if (lane == 0) { s_red[0] = q; s_redw[0] = qw; }
+        if (lane == 0) {  // this CTA's candidate -> rank 0
+          *cluster.map_shared_rank(&s_cbest[it & 1][rank], 0) = q;
+          *cluster.map_shared_rank(&s_cbw[it & 1][rank], 0) = qw;
+        }
       }
-      __syncthreads();
-      best = s_red[0];
-      bw = s_redw[0];
+      cluster.sync();
+      {  // every thread reduces the R candidates in rank order (same result everywhere)
+        const Prio* cb = cluster.map_shared_rank(&s_cbest[it & 1][0], 0);
+        const long long* cw = cluster.map_shared_rank(&s_cbw[it & 1][0], 0);
+        best = cb[0];
+        bw = cw[0];
+        for (int r = 1; r < R; ++r) {
+          const Prio q = cb[r];
+          if (q.a != 0 && (best.a == 0 || pgt(q, best))) { best = q; bw = cw[r]; }
+        }
+      }
       if (best.a == 0) break;  // nothing fits any more
-      if (tid == 0) mask[~best.c] = 1;
+      if (gtid == 0) mask[~best.c] = 1;
       remaining -= bw;
       cur = best;
       __syncthreads();
     }
   }
-  __syncthreads();
+  cluster.sync();  // rank 0's tail writes to the mask are visible to the whole cluster
   // ---- phase 3: single-item fallback + entry count ----------------------------------------------
   double sum_sel = 0.0;
   long long ent = 0;
@@ -642,7 +697,7 @@ __global__ void __launch_bounds__(1024)
     s_red[warp].c = (unsigned int)besti;
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0) {  // this CTA's partial results -> rank 0
     const int nw = nthr >> 5;
     double s = 0.0;
     long long e = 0;
@@ -655,16 +710,34 @@ __global__ void __launch_bounds__(1024)
       int oi = (int)s_red[w2].c;
       if (ov > bv || (ov == bv && oi < bx)) { bv = ov; bx = oi; }
     }
+    *cluster.map_shared_rank(&s_csum[rank], 0) = s;
+    *cluster.map_shared_rank(&s_cent[rank], 0) = e;
+    *cluster.map_shared_rank(&s_cbv[rank], 0) = bv;
+    *cluster.map_shared_rank(&s_cbi[rank], 0) = bx;
+  }
+  cluster.sync();
+  if (rank == 0 && tid == 0) {
+    double s = 0.0;
+    long long e = 0;
+    double bv = -INFINITY;
+    int bx = 0x7fffffff;
+    for (int r = 0; r < R; ++r) {
+      s += s_csum[r];
+      e += s_cent[r];
+      if (s_cbv[r] > bv || (s_cbv[r] == bv && s_cbi[r] < bx)) { bv = s_cbv[r]; bx = s_cbi[r]; }
+    }
     int swap = (fallback && bx != 0x7fffffff && bv > s) ? 1 : 0;
-    s_flag = swap;
-    s_base = swap ? (long long)bx : -1;
     if (entries_all)
       entries_all[h] = swap ? (long long)qs[bx / c_k] * (long long)s_ks[bx % c_k] : e;
+    for (int r = 0; r < R; ++r) {
+      *cluster.map_shared_rank(&s_flag, r) = swap;
+      *cluster.map_shared_rank(&s_base, r) = swap ? (long long)bx : -1;
+    }
   }
-  __syncthreads();
+  cluster.sync();
   if (s_flag) {
     const int keep = (int)s_base;
-    for (int b = tid; b < nb; b += nthr) mask[b] = (b == keep) ? 1 : 0;
+    for (int b = gtid; b < nb; b += gthr) mask[b] = (b == keep) ? 1 : 0;
   }
 #undef FOR_BLOCKS
 }
@@ -842,11 +915,42 @@ int launch_route(int bh, int c_q, int c_k, const double* val, const int32_t* q_s
   if (piece_bits > 17) piece_bits = 17;
   if (piece_bits < 6) return SVGEAR_EUNSUPPORTED;
   const int pieces = (40 + piece_bits - 1) / piece_bits;  // run sums: 34-bit weights x 64 blocks
-  const size_t smem = ((size_t)((c_k + 3) & ~3) + (size_t)kRouteBins * (pieces + 1)) * sizeof(int32_t);
-  SVG_CUDA_OK(cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  route_kernel<<<bh, 1024, smem, st>>>(c_q, c_k, val, keys, q_sizes, k_sizes, (long long)capacity, overshoot,
-                                       fallback, mask, reinterpret_cast<long long*>(entries), pieces,
-                                       piece_bits);
+  // CTAs per instance: one for small tables, otherwise the largest cluster size for which every
+  // instance's cluster is co-resident (a 1024-thread CTA of this kernel owns an SM's registers, and
+  // clusters do not straddle GPCs, so the driver is asked rather than assuming 148 / bh)
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(1024);
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SVG_CUDA_OK(cudaFuncSetAttribute(
+      route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (int)(((size_t)((c_k + 3) & ~3) + (size_t)kRouteBins * (pieces + 1) * 2) * sizeof(int32_t))));
+  int cluster = 1;
+  if ((long long)c_q * c_k > 16384) {
+    for (int r = kRouteMaxCluster; r > 1; --r) {
+      cfg.gridDim = dim3(bh * r);
+      cfg.dynamicSmemBytes = ((size_t)((c_k + 3) & ~3) + (size_t)kRouteBins * (pieces + 1) * 2) * sizeof(int32_t);
+      attr[0].val.clusterDim.x = r;
+      int fit = 0;
+      if (cudaOccupancyMaxActiveClusters(&fit, route_kernel, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        continue;
+      }
+      if (fit >= bh) { cluster = r; break; }
+    }
+  }
+  const size_t smem = ((size_t)((c_k + 3) & ~3) + (size_t)kRouteBins * (pieces + 1) * (cluster > 1 ? 2 : 1)) * sizeof(int32_t);
+  cfg.gridDim = dim3(bh * cluster);
+  cfg.dynamicSmemBytes = smem;
+  attr[0].val.clusterDim.x = cluster;
+  SVG_CUDA_OK(cudaLaunchKernelEx(&cfg, route_kernel, c_q, c_k, val, (const unsigned long long*)keys, q_sizes, k_sizes,
+                                 (long long)capacity, overshoot, fallback, mask,
+                                 reinterpret_cast<long long*>(entries), pieces, piece_bits));
   SVG_LAUNCH_OK();
   return SVGEAR_OK;
 }

@@ -333,6 +333,46 @@ class TestRouter:
             assert m.density_entries == want.density_entries <= cap
 
 
+    @pytest.mark.parametrize("bh", [3, 40, 80])  # 8, 4 and 2 CTAs per instance (thread-block clusters)
+    def test_batched_large_tables_with_ties_against_oracle(self, bh):
+        rng = np.random.default_rng(21)
+        cq, ck = 150, 200
+        distinct = 3
+        qs = rng.integers(1, 60, size=(distinct, cq))
+        ks = rng.integers(1, 40, size=(distinct, ck))
+        err = np.stack([rng.random((cq, ck)) ** 4 * np.outer(qs[i], ks[i]) for i in range(distinct)])
+        # instance 1: heavy ties in ratio AND value (equal sizes, quantised errors) -> index order decides
+        qs[1], ks[1] = 7, 5
+        err[1] = rng.integers(0, 6, size=(cq, ck)).astype(np.float64)
+        # instance 2: ties in ratio only (error proportional to the block size times a few levels)
+        err[2] = rng.integers(1, 4, size=(cq, ck)) * np.outer(qs[2], ks[2]).astype(np.float64)
+        idx = np.arange(bh) % distinct
+        t = P.BlockErrorTable(error_sum=torch.from_numpy(err[idx]), q_sizes=torch.from_numpy(qs[idx]).int(),
+                              k_sizes=torch.from_numpy(ks[idx]).int(), stabilizers=None, mode="valueAware", flops=0)
+        for rho, ov, fb in ((0.1, P.FILL_REMAINDER, True), (0.37, P.STOP_AT_FIRST_OVERFLOW, True),
+                            (0.0004, P.FILL_REMAINDER, True), (1.0, P.FILL_REMAINDER, False)):
+            # all instances of a call share the token counts, hence one capacity: use the smallest
+            cap = min(P.entry_capacity(rho, int(qs[i].sum()) * int(ks[i].sum())) for i in range(distinct))
+            from paper_2603_08982_b200 import _lib
+            import ctypes as C
+            e = dev(err[idx], torch.float64)
+            q_s, k_s = dev(qs[idx], torch.int32), dev(ks[idx], torch.int32)
+            mask = torch.empty((bh, cq, ck), dtype=torch.uint8, device="cuda")
+            ent = torch.empty((bh,), dtype=torch.int64, device="cuda")
+            ws = torch.empty(bh * cq * ck * 8 + 1024, dtype=torch.uint8, device="cuda")
+            rc = _lib.lib().svgear_route_error_aware(bh, cq, ck, e.data_ptr(), q_s.data_ptr(), k_s.data_ptr(), cap,
+                                                     P.router._OVERSHOOT[ov], 1 if fb else 0, mask.data_ptr(),
+                                                     ent.data_ptr(), ws.data_ptr(), ws.numel(), None)
+            assert rc == 0
+            torch.cuda.synchronize()
+            for i in range(distinct):
+                want = O.route_error_aware_entries(SimpleNamespace(error_sum=err[i], q_sizes=qs[i], k_sizes=ks[i]),
+                                                   cap, overshoot=ov, fallback=fb)
+                for b in range(i, bh, distinct):
+                    assert np.array_equal(host(mask[b]).astype(bool), want.selected), (rho, ov, i, b)
+                    assert int(ent[b]) == want.density_entries
+
+
 class TestExecutor:
     def _instance(self, seed, n_q=150, n_k=190, d=64, c_q=4, c_k=6):
         rng = np.random.default_rng(seed)
