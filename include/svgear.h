@@ -216,6 +216,22 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
                    uint8_t* mask, const SvgEarAux* aux, void* workspace, size_t workspace_bytes,
                    void* stream);
 
+/* svgear_forward with the device-side k-means++ seeding folded in: equivalent to
+ * svgear_kmeans_seed_gram(q side, seed) + svgear_kmeans_seed_gram(k side, seed + 0x9E37) followed by
+ * svgear_forward, but each side's seeding kernel runs on the stream of that side's Lloyd loop, so
+ * the query side does not wait for the (longer) key-side seeding.  NOT the reference's numpy draw:
+ * for parity runs hand svgear_forward the reference's start centres.
+ *   q_gram [bh][m_q][m_q], k_gram [bh][m_k][m_k] bf16: Gram matrices of the strided subsamples
+ *   (token i*n/m, i < m), as for svgear_kmeans_seed_gram; c <= m <= min(n, 4096)
+ *   q_init [bh][c_q][d], k_init [bh][c_k][d] f32: OUT, the start centres that were drawn          */
+int svgear_forward_seeded(const SvgEarShape* shape, const void* q, const void* k, const void* v,
+                          const void* q_gram, const void* k_gram, int32_t m_q, int32_t m_k,
+                          uint32_t seed, float* q_init, float* k_init, int32_t kmeans_iters,
+                          int32_t estimator_mode, int64_t capacity_entries, int32_t overshoot,
+                          int32_t single_item_fallback, int32_t exec_mode, double top_p, void* out,
+                          uint8_t* mask, const SvgEarAux* aux, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
 /* ---- the callers either side of the operator in a DiT attention block ----
  * The reference stops at single (Q,K,V) matrices; the paper's deployment feeds
  * the operator from a fused QKV projection with q/k RMSNorm and rotary embedding, and feeds its

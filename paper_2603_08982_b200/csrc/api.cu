@@ -311,11 +311,24 @@ int svgear_sparse_attend(const SvgEarShape* shape, int32_t exec_mode, const void
                        k_centroids, v_centroids, mask, out, lse, sc, (cudaStream_t)stream);
 }
 
-int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const void* v,
-                   const float* q_init, const float* k_init, int32_t kmeans_iters,
-                   int32_t estimator_mode, int64_t capacity_entries, int32_t overshoot,
-                   int32_t single_item_fallback, int32_t exec_mode, double top_p, void* out, uint8_t* mask,
-                   const SvgEarAux* aux, void* workspace, size_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+// Device-side k-means++ seeding folded into the forward pass: each side's seeding kernel runs on the
+// stream of that side's Lloyd loop (svgear_forward_seeded), so the short query-side seeding does not
+// wait for the long key-side one.
+struct SeedPlan {
+  const bf16* q_gram;
+  const bf16* k_gram;
+  int m_q, m_k;
+  uint32_t seed;
+};
+
+int forward_impl(const SvgEarShape* shape, const void* q, const void* k, const void* v,
+                 float* q_init, float* k_init, const SeedPlan* sp, int32_t kmeans_iters,
+                 int32_t estimator_mode, int64_t capacity_entries, int32_t overshoot,
+                 int32_t single_item_fallback, int32_t exec_mode, double top_p, void* out, uint8_t* mask,
+                 const SvgEarAux* aux, void* workspace, size_t workspace_bytes, void* stream) {
   if (!shape || !q || !k || !v || !q_init || !k_init || !out || !mask || !workspace)
     return SVGEAR_EINVAL;
   if (kmeans_iters < 1 || capacity_entries < 0) return SVGEAR_EINVAL;
@@ -365,8 +378,12 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
     HelperFork fk(st, 0);
     if (!fk.ok()) return SVGEAR_ECUDA;
     cudaStream_t side = fk.side();
-    rc_k = launch_kmeans(exec_mode, s.bh, s.n_k, s.d, s.c_k, (const bf16*)k, k_init, kmeans_iters, k_assign,
-                         k_perm, k_sizes, k_offsets, k_cent, k_iters, nullptr, p.km2, side);
+    rc_k = sp ? launch_seed_gram(s.bh, s.n_k, s.d, s.c_k, sp->m_k, (const bf16*)k, sp->k_gram, sp->seed + 0x9E37u,
+                                 k_init, side)
+              : SVGEAR_OK;
+    if (!rc_k)
+      rc_k = launch_kmeans(exec_mode, s.bh, s.n_k, s.d, s.c_k, (const bf16*)k, k_init, kmeans_iters, k_assign,
+                           k_perm, k_sizes, k_offsets, k_cent, k_iters, nullptr, p.km2, side);
     if (!rc_k) rc_k = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)k, k_perm, p.kp, side);
     if (!rc_k) rc_k = launch_gather_rows(s.bh, s.n_k, s.d, (const bf16*)v, k_perm, p.vp, side);
     if (!rc_k)
@@ -375,8 +392,11 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
     // stream, under the (usually longer) query-side Lloyd loop
     if (!rc_k && keys_early)
       rc_k = launch_error_table_keys(s, estimator_mode, k_cent, v_cent, p.kp, p.vp, k_sizes, k_offsets, p.es, side);
-    rc = launch_kmeans(exec_mode, s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign,
-                       q_perm, q_sizes, q_offsets, q_cent, q_iters, nullptr, p.km, st);
+    rc = sp ? launch_seed_gram(s.bh, s.n_q, s.d, s.c_q, sp->m_q, (const bf16*)q, sp->q_gram, sp->seed, q_init, st)
+            : SVGEAR_OK;
+    if (!rc)
+      rc = launch_kmeans(exec_mode, s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign,
+                         q_perm, q_sizes, q_offsets, q_cent, q_iters, nullptr, p.km, st);
     if (!rc) rc = launch_gather_rows(s.bh, s.n_q, s.d, (const bf16*)q, q_perm, p.qp, st);
     // join unconditionally so that the helper stream never outlives the caller's ordering
     if (fk.join() != SVGEAR_OK) rc = SVGEAR_ECUDA;
@@ -401,6 +421,35 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
   // (3) fused executor, output scattered to original token order
   return launch_attend(s, exec_mode, p.qp, p.kp, p.vp, q_perm, q_sizes, q_offsets, k_sizes, k_offsets,
                        k_cent, v_cent, mask, out, a.lse, p.at, st);
+}
+}  // namespace
+
+extern "C" {
+
+int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const void* v,
+                   const float* q_init, const float* k_init, int32_t kmeans_iters,
+                   int32_t estimator_mode, int64_t capacity_entries, int32_t overshoot,
+                   int32_t single_item_fallback, int32_t exec_mode, double top_p, void* out, uint8_t* mask,
+                   const SvgEarAux* aux, void* workspace, size_t workspace_bytes, void* stream) {
+  return forward_impl(shape, q, k, v, const_cast<float*>(q_init), const_cast<float*>(k_init), nullptr,
+                      kmeans_iters, estimator_mode, capacity_entries, overshoot, single_item_fallback, exec_mode,
+                      top_p, out, mask, aux, workspace, workspace_bytes, stream);
+}
+
+int svgear_forward_seeded(const SvgEarShape* shape, const void* q, const void* k, const void* v,
+                          const void* q_gram, const void* k_gram, int32_t m_q, int32_t m_k, uint32_t seed,
+                          float* q_init, float* k_init, int32_t kmeans_iters, int32_t estimator_mode,
+                          int64_t capacity_entries, int32_t overshoot, int32_t single_item_fallback,
+                          int32_t exec_mode, double top_p, void* out, uint8_t* mask, const SvgEarAux* aux,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape || !q_gram || !k_gram) return SVGEAR_EINVAL;
+  if (!shape_ok(shape)) return SVGEAR_ESHAPE;
+  if (m_q < shape->c_q || m_q > shape->n_q || m_q > 4096 || m_k < shape->c_k || m_k > shape->n_k || m_k > 4096)
+    return SVGEAR_ESHAPE;
+  SeedPlan sp{(const bf16*)q_gram, (const bf16*)k_gram, m_q, m_k, seed};
+  return forward_impl(shape, q, k, v, q_init, k_init, &sp, kmeans_iters, estimator_mode, capacity_entries,
+                      overshoot, single_item_fallback, exec_mode, top_p, out, mask, aux, workspace,
+                      workspace_bytes, stream);
 }
 
 }  // extern "C"

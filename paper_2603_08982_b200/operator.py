@@ -16,7 +16,7 @@ import torch
 from . import _lib
 from ._tensors import ShapeError, require_cuda, stream_ptr, workspace
 from .analysis import side_seeds
-from .clustering import device_start, device_start_pair, seeded_start, strided_start
+from .clustering import _seed_inputs, device_start, device_start_pair, seeded_start, strided_start
 from .router import _OVERSHOOT, entry_capacity
 
 _EST = {"valueAware": _lib.EST_VALUE_AWARE, "plain": _lib.EST_PLAIN}
@@ -96,6 +96,14 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
     vb = v.to(dev, torch.bfloat16).reshape(bh, n_k, d).contiguous()
     c_q, c_k = int(n_q_clusters), int(n_k_clusters)
 
+    seeded = None  # (q_gram, m_q, k_gram, m_k): seed inside the forward call, each side on its own stream
+    if q_init is None and k_init is None and init == "device":
+        _, q_init, gq, mq = _seed_inputs(qb, c_q, 8)
+        _, k_init, gk, mk = _seed_inputs(kb, c_k, 8)
+        if gq is not None and gk is not None:
+            seeded = (gq, mq, gk, mk)
+        else:
+            q_init = k_init = None
     if q_init is None or k_init is None:
         if init == "reference":
             rq, rk = reference_init(qb, kb, c_q, c_k, seed)
@@ -138,16 +146,19 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
             lse=torch.empty((bh, n_q), dtype=f32, device=dev),
         )
         aux_c = _lib.Aux(**{name: aux_t[name].data_ptr() for name in _lib.Aux.FIELDS})
-    rc = _lib.lib().svgear_forward(
-        C.byref(shape), qb.data_ptr(), kb.data_ptr(), vb.data_ptr(), q_init.data_ptr(),
-        k_init.data_ptr(), int(kmeans_iters), _EST[estimator],
+    fn, head = "svgear_forward", (q_init.data_ptr(), k_init.data_ptr())
+    if seeded is not None:
+        fn = "svgear_forward_seeded"
+        head = (seeded[0].data_ptr(), seeded[2].data_ptr(), seeded[1], seeded[3], int(seed) & 0xFFFFFFFF) + head
+    rc = getattr(_lib.lib(), fn)(
+        C.byref(shape), qb.data_ptr(), kb.data_ptr(), vb.data_ptr(), *head, int(kmeans_iters), _EST[estimator],
         0 if budget_mode == "perClusterTopP" else entry_capacity(float(budget), n_q * n_k),
         _OVERSHOOT[overshoot], 1 if single_item_fallback else 0,
         _lib.EXEC_FP32_CHECK if check_fp32 else _lib.EXEC_BF16_TENSOR,
         float(budget) if budget_mode == "perClusterTopP" else 0.0, out.data_ptr(),
         mask.data_ptr(), C.byref(aux_c) if aux_c is not None else None, ws.data_ptr(),
         ws.numel() * ws.element_size(), stream_ptr())
-    _lib.check("svgear_forward", rc)
+    _lib.check(fn, rc)
     out = out.reshape(*lead, n_q, d)
     mask_b = mask.bool().reshape(*lead, c_q, c_k)
     if not return_aux:

@@ -693,3 +693,33 @@ class TestRandomShapes:
         for dtype, tol in ((torch.float32, TOL_FP32), (torch.bfloat16, TOL_BF16)):
             res = P.sparse_attend(prep.q, prep.k, prep.v, prep.q_model, prep.k_model, mask, dtype=dtype)
             assert rel_l2(host(res.output.float()), want) <= tol, (n_q, n_k, c_q, c_k, d, str(dtype))
+
+
+class TestSeededForward:
+    """svgear_forward_seeded = svgear_kmeans_seed_gram per side + svgear_forward, with each side's
+    seeding on the stream of its own Lloyd loop: results must be bit-identical to the two-step path."""
+
+    @pytest.mark.parametrize("d,H,S,cq,ck", [(64, 3, 1500, 16, 40), (128, 2, 2304, 20, 64)])
+    def test_bit_identical_to_seed_then_forward(self, d, H, S, cq, ck):
+        from paper_2603_08982_b200.clustering import device_start_pair
+        heads = [tuple(O.round_to_bf16(a) for a in O.blob_instance(S, S, d, cq, ck, 0.15, 50 + h)) for h in range(H)]
+        q, k, v = (dev(np.stack([hd[i] for hd in heads])).unsqueeze(0) for i in range(3))
+        for seed in (0, 7):
+            out1, mask1, aux1 = P.svg_ear_attention(q, k, v, cq, ck, 0.25, seed=seed, init="device", return_aux=True)
+            qi, ki = device_start_pair(q[0], cq, k[0], ck, seed)
+            out2, mask2, aux2 = P.svg_ear_attention(q, k, v, cq, ck, 0.25, q_init=qi, k_init=ki, return_aux=True)
+            assert torch.equal(aux1["q_init"][0], qi) and torch.equal(aux1["k_init"][0], ki)
+            assert torch.equal(aux1["q_perm"], aux2["q_perm"]) and torch.equal(aux1["k_perm"], aux2["k_perm"])
+            assert torch.equal(mask1, mask2) and torch.equal(out1, out2)
+
+    def test_c_abi_rejects_bad_subsample_sizes(self):
+        from paper_2603_08982_b200 import _lib
+        import ctypes as C
+        shape = _lib.Shape(1, 256, 256, 64, 8, 8)
+        buf = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+        p = buf.data_ptr()
+        call = lambda mq, mk, g=p: _lib.lib().svgear_forward_seeded(
+            C.byref(shape), p, p, p, g, p, mq, mk, 0, p, p, 5, 0, 100, 0, 1, 0, 0.0, p, p, None, p, buf.numel(), None)
+        assert call(4, 64) == _lib.ESHAPE      # fewer subsample tokens than centres
+        assert call(64, 512) == _lib.ESHAPE    # more than the instance has
+        assert call(64, 64, None) == _lib.EINVAL
