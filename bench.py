@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--sigma", type=float, default=0.1)
     ap.add_argument("--init", default="device", choices=["device", "strided"])
+    ap.add_argument("--head-groups", type=int, default=None,
+                    help="head groups run on concurrent streams inside the operator (default: its own choice)")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the resident-input step eagerly instead of replaying a captured CUDA graph")
     return ap.parse_args()
@@ -211,9 +213,10 @@ def run_ours(args):
 
     q, k, v = make_heads(torch, lo, hi, S, d, cq, ck, args.sigma, dev)
     shape = _lib.Shape(max(hl, 1), S, S, d, cq, ck)
-    ws = torch.empty(_lib.workspace_bytes(shape), dtype=torch.uint8, device=dev)
+    ws = torch.empty(P.operator_workspace_bytes(max(hl, 1), S, S, d, cq, ck, args.head_groups), dtype=torch.uint8,
+                     device=dev)
     kw = dict(init=args.init, kmeans_iters=args.kmeans_iters, check_fp32=args.fp32_check,
-              workspace_buffer=ws)
+              workspace_buffer=ws, head_groups=args.head_groups)
 
     def layer(qq, kk, vv, aux=False):
         if hl == 0:
@@ -237,22 +240,44 @@ def run_ours(args):
     # computed, the host->device copy of group g+1 and the device->host copy of group g-1 run on a
     # copy stream (heads are independent instances, so the grouping does not change any result of
     # a head except the device-side seeding draw, which is keyed by the instance index).
-    n_groups = 4 if (hl >= 8 and world == 1) else 1
+    n_groups = 5 if (hl >= 16 and world == 1) else (4 if (hl >= 8 and world == 1) else 1)
     if n_groups == 1:
         bounds = [0, hl]
-    else:
+    elif n_groups == 4:
         # a small first group lets compute start early; the rest is split evenly (big groups run the
         # latency-bound stages more efficiently)
         first = max(1, hl // 10)
         rest = hl - first
         bounds = [0] + [first + rest * g // (n_groups - 1) for g in range(n_groups)]
+    else:
+        # every group computes on its own stream as soon as its inputs have landed, so the groups'
+        # latency-bound stages overlap; a small first group starts compute early and a small last
+        # group keeps the tail after the final host->device copy short
+        edge = max(1, hl // 10)
+        mid = hl - 2 * edge
+        bounds = [0] + [edge + mid * g // (n_groups - 2) for g in range(n_groups - 1)] + [hl]
     copy_stream = torch.cuda.Stream(device=dev)   # host -> device
     back_stream = torch.cuda.Stream(device=dev)   # device -> host (PCIe is full duplex)
     gmax = max(bounds[g + 1] - bounds[g] for g in range(n_groups))
-    ws_g = ws if n_groups == 1 else torch.empty(
-        _lib.workspace_bytes(_lib.Shape(max(gmax, 1), S, S, d, cq, ck)), dtype=torch.uint8, device=dev)
+    ws_g = [ws] if n_groups == 1 else [torch.empty(
+        P.operator_workspace_bytes(max(gmax, 1), S, S, d, cq, ck, args.head_groups), dtype=torch.uint8, device=dev)
+        for _ in range(n_groups)]
+    group_streams = [torch.cuda.Stream(device=dev) for _ in range(n_groups)]
     do = torch.empty((1, hl, S, d), dtype=out_dtype, device=dev)
     dm = torch.empty((1, hl, cq, ck), dtype=torch.bool, device=dev)
+
+    def group_compute(g):
+        """The public operator on head group g of the device staging buffers -> do/dm slices."""
+        a, b = bounds[g], bounds[g + 1]
+        o, m = P.svg_ear_attention(dq[:, a:b], dk[:, a:b], dv[:, a:b], cq, ck, args.rho, seed=a,
+                                   init=args.init, kmeans_iters=args.kmeans_iters,
+                                   check_fp32=args.fp32_check, workspace_buffer=ws_g[g],
+                                   head_groups=args.head_groups)
+        do[:, a:b].copy_(o); dm[:, a:b].copy_(m)
+
+    # per-group CUDA graphs of the operator call (filled in after the warm-up below): a group's ~3000
+    # eager launches cost more host time than its kernels take, so the e2e leg was host bound
+    group_graphs = [None] * n_groups
 
     def step_e2e():
         if n_groups == 1:
@@ -274,16 +299,21 @@ def run_ours(args):
                 ev = torch.cuda.Event(); ev.record(copy_stream); h2d.append(ev)
         for g in range(n_groups):
             a, b = bounds[g], bounds[g + 1]
-            cur.wait_event(h2d[g])
-            o, m = P.svg_ear_attention(dq[:, a:b], dk[:, a:b], dv[:, a:b], cq, ck, args.rho, seed=a,
-                                       init=args.init, kmeans_iters=args.kmeans_iters,
-                                       check_fp32=args.fp32_check, workspace_buffer=ws_g)
-            do[:, a:b].copy_(o); dm[:, a:b].copy_(m)
-            ev = torch.cuda.Event(); ev.record(cur); done.append(ev)
+            gs = group_streams[g]
+            gs.wait_stream(cur)
+            gs.wait_event(h2d[g])
+            with torch.cuda.stream(gs):
+                if group_graphs[g] is not None:
+                    group_graphs[g].replay()
+                else:
+                    group_compute(g)
+                ev = torch.cuda.Event(); ev.record(gs); done.append(ev)
             with torch.cuda.stream(back_stream):
                 back_stream.wait_event(ev)
                 ho[:, a:b].copy_(do[:, a:b], non_blocking=True)
                 hm[:, a:b].copy_(dm[:, a:b], non_blocking=True)
+        for gs in group_streams:
+            cur.wait_stream(gs)
         cur.wait_stream(back_stream)
         cur.wait_stream(copy_stream)
 
@@ -340,6 +370,27 @@ def run_ours(args):
     launches = (lib.svgear_launch_count() - l0) if graph is None else launches_per_step * args.steps
     clocks = sampler.stop()
     step_e2e()
+    e2e_graphs = False
+    if graph is not None and n_groups > 1:
+        try:
+            torch.cuda.synchronize()
+            eager_o, eager_m = do.clone(), dm.clone()
+            caps = []
+            for g in range(n_groups):
+                cg = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(cg, stream=group_streams[g]):
+                    group_compute(g)
+                caps.append(cg)
+            group_graphs[:] = caps
+            step_e2e()
+            torch.cuda.synchronize()
+            if not (torch.equal(do, eager_o) and torch.equal(dm, eager_m)):
+                raise RuntimeError("e2e graph replay differs from the eager result")
+            e2e_graphs = True
+        except Exception as exc:  # noqa: BLE001
+            print(f"[bench] e2e group graphs unavailable, launching eagerly: {exc}", file=sys.stderr)
+            group_graphs[:] = [None] * n_groups
+            torch.cuda.synchronize()
     ms_e2e = timed(step_e2e, args.steps)
 
     # ---- stage timings (CUDA events on the launching stream) for the roofline -------------------
@@ -399,8 +450,10 @@ def run_ours(args):
                        "executor": "fp32-check" if args.fp32_check else "bf16-tcgen05",
                        "density_achieved": density, "parallelism": f"head-parallel x{world}",
                        "l2": "inputs (%.0f MB/rank) exceed the 126 MB L2; no explicit flush" % (in_bytes / 1e6),
-                       "e2e_pipeline": f"{n_groups} head groups, H2D and D2H on their own streams",
-                       "cuda_graph": graph is not None},
+                       "e2e_pipeline": f"{n_groups} head groups, each computed on its own stream as soon as its inputs land (H2D and D2H on their own streams)",
+                       "cuda_graph": graph is not None, "e2e_cuda_graphs": e2e_graphs,
+                       "head_groups": ("operator default (2 concurrent head groups at >= 16 heads)"
+                                       if args.head_groups is None else args.head_groups)},
             "clocks": clocks,
             "e2e": {"value": fl / (ms_e2e * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms_e2e,
                     "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": out_bytes},

@@ -223,10 +223,14 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
  * for parity runs hand svgear_forward the reference's start centres.
  *   q_gram [bh][m_q][m_q], k_gram [bh][m_k][m_k] bf16: Gram matrices of the strided subsamples
  *   (token i*n/m, i < m), as for svgear_kmeans_seed_gram; c <= m <= min(n, 4096)
+ *   first_instance: instance b of this call draws as instance first_instance + b of the whole batch,
+ *   so a caller that splits a batch into groups (one call per group, e.g. on concurrent streams)
+ *   gets the centres of the unsplit call
  *   q_init [bh][c_q][d], k_init [bh][c_k][d] f32: OUT, the start centres that were drawn          */
 int svgear_forward_seeded(const SvgEarShape* shape, const void* q, const void* k, const void* v,
                           const void* q_gram, const void* k_gram, int32_t m_q, int32_t m_k,
-                          uint32_t seed, float* q_init, float* k_init, int32_t kmeans_iters,
+                          uint32_t seed, int32_t first_instance, float* q_init, float* k_init,
+                          int32_t kmeans_iters,
                           int32_t estimator_mode, int64_t capacity_entries, int32_t overshoot,
                           int32_t single_item_fallback, int32_t exec_mode, double top_p, void* out,
                           uint8_t* mask, const SvgEarAux* aux, void* workspace,

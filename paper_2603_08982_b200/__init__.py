@@ -18,7 +18,7 @@ from .clustering import (ClusterModel, cluster_means, device_start, inverse_perm
                          permute_rows, segment_means, strided_start)
 from .estimator import (BlockErrorTable, estimate_errors, estimate_errors_streaming,
                         estimate_errors_value_aware)
-from .operator import reference_init, svg_ear_attention
+from .operator import operator_workspace_bytes, reference_init, svg_ear_attention
 from .router import (FILL_REMAINDER, STOP_AT_FIRST_OVERFLOW, BlockMask, DensityBudget,
                      entry_capacity, mask_from_selected, relaxed_objective, route_error_aware,
                      route_error_aware_entries, route_score)

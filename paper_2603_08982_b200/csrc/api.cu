@@ -12,36 +12,58 @@ namespace svg {
 long long g_launches = 0;
 
 namespace {
+// Helper streams are keyed by (lane, slot): a lane belongs to one caller stream, so that calls issued
+// on different streams (head groups running concurrently) do not serialise on a shared helper.
 constexpr int kHelperSlots = 2;
-std::mutex g_helper_mu[kHelperSlots];
-cudaStream_t g_helper_stream[kHelperSlots] = {nullptr, nullptr};
-cudaEvent_t g_helper_fork[kHelperSlots] = {nullptr, nullptr}, g_helper_join[kHelperSlots] = {nullptr, nullptr};
+constexpr int kHelperLanes = 16;
+std::mutex g_lane_mu;
+cudaStream_t g_lane_owner[kHelperLanes];
+int g_lanes_used = 0;
+std::mutex g_helper_mu[kHelperLanes][kHelperSlots];
+cudaStream_t g_helper_stream[kHelperLanes][kHelperSlots];
+cudaEvent_t g_helper_fork[kHelperLanes][kHelperSlots], g_helper_join[kHelperLanes][kHelperSlots];
+
+int lane_of(cudaStream_t main) {
+  std::lock_guard<std::mutex> lk(g_lane_mu);
+  for (int i = 0; i < g_lanes_used; ++i)
+    if (g_lane_owner[i] == main) return i;
+  if (g_lanes_used < kHelperLanes) {
+    g_lane_owner[g_lanes_used] = main;
+    return g_lanes_used++;
+  }
+  // more caller streams than lanes: share (correct, only less concurrent)
+  return (int)(((uintptr_t)main >> 4) % kHelperLanes);
+}
 }  // namespace
 
-HelperFork::HelperFork(cudaStream_t main, int slot) : main_(main), side_(nullptr), slot_(slot), ok_(false), joined_(false) {
-  g_helper_mu[slot_].lock();
-  if (!g_helper_stream[slot_]) {
-    if (cudaStreamCreateWithFlags(&g_helper_stream[slot_], cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_helper_fork[slot_], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_helper_join[slot_], cudaEventDisableTiming) != cudaSuccess) {
-      g_helper_stream[slot_] = nullptr;
+HelperFork::HelperFork(cudaStream_t main, int slot)
+    : main_(main), side_(nullptr), slot_(lane_of(main) * kHelperSlots + slot), ok_(false), joined_(false) {
+  std::mutex& mu = (&g_helper_mu[0][0])[slot_];
+  cudaStream_t& hs = (&g_helper_stream[0][0])[slot_];
+  cudaEvent_t& ef = (&g_helper_fork[0][0])[slot_];
+  cudaEvent_t& ej = (&g_helper_join[0][0])[slot_];
+  mu.lock();
+  if (!hs) {
+    if (cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ef, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ej, cudaEventDisableTiming) != cudaSuccess) {
+      hs = nullptr;
       (void)cudaGetLastError();
       return;
     }
   }
-  side_ = g_helper_stream[slot_];
-  ok_ = cudaEventRecord(g_helper_fork[slot_], main_) == cudaSuccess &&
-        cudaStreamWaitEvent(side_, g_helper_fork[slot_], 0) == cudaSuccess;
+  side_ = hs;
+  ok_ = cudaEventRecord(ef, main_) == cudaSuccess && cudaStreamWaitEvent(side_, ef, 0) == cudaSuccess;
 }
 
 int HelperFork::join() {
   if (joined_) return SVGEAR_OK;
   joined_ = true;
   int rc = SVGEAR_OK;
-  if (ok_ && (cudaEventRecord(g_helper_join[slot_], side_) != cudaSuccess ||
-              cudaStreamWaitEvent(main_, g_helper_join[slot_], 0) != cudaSuccess))
+  cudaEvent_t ej = (&g_helper_join[0][0])[slot_];
+  if (ok_ && (cudaEventRecord(ej, side_) != cudaSuccess || cudaStreamWaitEvent(main_, ej, 0) != cudaSuccess))
     rc = SVGEAR_ECUDA;
-  g_helper_mu[slot_].unlock();
+  (&g_helper_mu[0][0])[slot_].unlock();
   return rc;
 }
 
@@ -322,6 +344,7 @@ struct SeedPlan {
   const bf16* k_gram;
   int m_q, m_k;
   uint32_t seed;
+  int first;  // index of this call's first instance in the caller's whole batch
 };
 
 int forward_impl(const SvgEarShape* shape, const void* q, const void* k, const void* v,
@@ -379,7 +402,7 @@ int forward_impl(const SvgEarShape* shape, const void* q, const void* k, const v
     if (!fk.ok()) return SVGEAR_ECUDA;
     cudaStream_t side = fk.side();
     rc_k = sp ? launch_seed_gram(s.bh, s.n_k, s.d, s.c_k, sp->m_k, (const bf16*)k, sp->k_gram, sp->seed + 0x9E37u,
-                                 k_init, side)
+                                 k_init, side, sp->first)
               : SVGEAR_OK;
     if (!rc_k)
       rc_k = launch_kmeans(exec_mode, s.bh, s.n_k, s.d, s.c_k, (const bf16*)k, k_init, kmeans_iters, k_assign,
@@ -392,7 +415,7 @@ int forward_impl(const SvgEarShape* shape, const void* q, const void* k, const v
     // stream, under the (usually longer) query-side Lloyd loop
     if (!rc_k && keys_early)
       rc_k = launch_error_table_keys(s, estimator_mode, k_cent, v_cent, p.kp, p.vp, k_sizes, k_offsets, p.es, side);
-    rc = sp ? launch_seed_gram(s.bh, s.n_q, s.d, s.c_q, sp->m_q, (const bf16*)q, sp->q_gram, sp->seed, q_init, st)
+    rc = sp ? launch_seed_gram(s.bh, s.n_q, s.d, s.c_q, sp->m_q, (const bf16*)q, sp->q_gram, sp->seed, q_init, st, sp->first)
             : SVGEAR_OK;
     if (!rc)
       rc = launch_kmeans(exec_mode, s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign,
@@ -438,15 +461,15 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
 
 int svgear_forward_seeded(const SvgEarShape* shape, const void* q, const void* k, const void* v,
                           const void* q_gram, const void* k_gram, int32_t m_q, int32_t m_k, uint32_t seed,
-                          float* q_init, float* k_init, int32_t kmeans_iters, int32_t estimator_mode,
+                          int32_t first_instance, float* q_init, float* k_init, int32_t kmeans_iters, int32_t estimator_mode,
                           int64_t capacity_entries, int32_t overshoot, int32_t single_item_fallback,
                           int32_t exec_mode, double top_p, void* out, uint8_t* mask, const SvgEarAux* aux,
                           void* workspace, size_t workspace_bytes, void* stream) {
-  if (!shape || !q_gram || !k_gram) return SVGEAR_EINVAL;
+  if (!shape || !q_gram || !k_gram || first_instance < 0) return SVGEAR_EINVAL;
   if (!shape_ok(shape)) return SVGEAR_ESHAPE;
   if (m_q < shape->c_q || m_q > shape->n_q || m_q > 4096 || m_k < shape->c_k || m_k > shape->n_k || m_k > 4096)
     return SVGEAR_ESHAPE;
-  SeedPlan sp{(const bf16*)q_gram, (const bf16*)k_gram, m_q, m_k, seed};
+  SeedPlan sp{(const bf16*)q_gram, (const bf16*)k_gram, m_q, m_k, seed, first_instance};
   return forward_impl(shape, q, k, v, q_init, k_init, &sp, kmeans_iters, estimator_mode, capacity_entries,
                       overshoot, single_item_fallback, exec_mode, top_p, out, mask, aux, workspace,
                       workspace_bytes, stream);

@@ -142,7 +142,7 @@ int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, con
 int launch_seed_pp(int bh, int n, int d, int c, const bf16* x, int oversample, uint32_t seed, float* cent,
                    cudaStream_t st);
 int launch_seed_gram(int bh, int n, int d, int c, int m, const bf16* x, const bf16* gram, uint32_t seed,
-                     float* cent, cudaStream_t st);
+                     float* cent, cudaStream_t st, int first_instance = 0);
 int launch_gather_rows(int bh, int n, int d, const bf16* x, const int32_t* perm, bf16* out,
                        cudaStream_t st);
 int launch_segment_means(int bh, int n, int d, int c, const bf16* xp, const int32_t* sizes,

@@ -932,7 +932,7 @@ constexpr int kGramPer = 4;  // samples per thread (m <= 4096)
 
 __global__ void __launch_bounds__(1024)
     seed_gram_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gram, int n, int d, int c, int m,
-                     uint32_t seed, float* __restrict__ cent) {
+                     uint32_t seed, int first, float* __restrict__ cent) {
   const int h = blockIdx.x;
   __shared__ float s_warp[32];
   __shared__ float s_total;
@@ -951,7 +951,7 @@ __global__ void __launch_bounds__(1024)
     mind[e] = s < m ? INFINITY : 0.f;
   }
   int picks[kSeedBatch];
-  picks[0] = (int)(hash_u32(seed, (uint32_t)h, 0u) % (uint32_t)m);
+  picks[0] = (int)(hash_u32(seed, (uint32_t)(first + h), 0u) % (uint32_t)m);
   int cnt = 1, npicked = 0;
   while (true) {
     for (int e = tid; e < cnt * d; e += 1024) {
@@ -1009,7 +1009,7 @@ __global__ void __launch_bounds__(1024)
     if (total > 0.f && mine > 0.f) {
       const float lo = s_warp[warp] + inc - mine;
       for (int i = 0; i < next; ++i) {
-        const float u = ((float)(hash_u32(seed, (uint32_t)h, (uint32_t)(npicked + i) + 1u) >> 8) + 0.5f) *
+        const float u = ((float)(hash_u32(seed, (uint32_t)(first + h), (uint32_t)(npicked + i) + 1u) >> 8) + 0.5f) *
                         (1.0f / 16777216.0f);
         const float target = u * total;
         if (target >= lo && target < lo + mine) {
@@ -1033,7 +1033,7 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
     for (int i = 0; i < next; ++i) {
       int pk = s_pick[i];
-      if (pk < 0 || pk >= m) pk = (int)(hash_u32(seed, (uint32_t)h, (uint32_t)(npicked + i) + 77777u) % (uint32_t)m);
+      if (pk < 0 || pk >= m) pk = (int)(hash_u32(seed, (uint32_t)(first + h), (uint32_t)(npicked + i) + 77777u) % (uint32_t)m);
       for (int j = 0; j < i; ++j)
         if (picks[j] == pk) pk = (pk + 1 + i) % m;
       picks[i] = pk;
@@ -1043,9 +1043,9 @@ __global__ void __launch_bounds__(1024)
 }
 
 int launch_seed_gram(int bh, int n, int d, int c, int m, const bf16* x, const bf16* gram, uint32_t seed,
-                     float* cent, cudaStream_t st) {
+                     float* cent, cudaStream_t st, int first_instance) {
   if (m > 1024 * kGramPer || m < c) return SVGEAR_ESHAPE;
-  seed_gram_kernel<<<bh, 1024, 0, st>>>(x, gram, n, d, c, m, seed, cent);
+  seed_gram_kernel<<<bh, 1024, 0, st>>>(x, gram, n, d, c, m, seed, first_instance, cent);
   SVG_LAUNCH_OK();
   return SVGEAR_OK;
 }

@@ -22,6 +22,39 @@ from .router import _OVERSHOOT, entry_capacity
 _EST = {"valueAware": _lib.EST_VALUE_AWARE, "plain": _lib.EST_PLAIN}
 
 
+_GROUP_STREAMS = {}
+
+
+def _group_streams(dev, n):
+    """Per-device compute streams of the head groups (created once; every tensor they touch is
+    allocated on the caller's stream and the groups are joined before the operator returns)."""
+    have = _GROUP_STREAMS.setdefault(dev.index, [])
+    while len(have) < n:
+        have.append(torch.cuda.Stream(device=dev))
+    return have[:n]
+
+
+def _auto_groups(bh, n_q, n_k):
+    return 2 if (bh >= 16 and min(n_q, n_k) >= 16384) else 1
+
+
+def _group_layout(bh, n_q, n_k, d, c_q, c_k, groups):
+    """(instance bounds, per-group workspace bytes, total bytes) of a head-group split."""
+    bnd = [bh * g // groups for g in range(groups + 1)]
+    nds = [_lib.workspace_bytes(_lib.Shape(bnd[g + 1] - bnd[g], n_q, n_k, d, c_q, c_k)) for g in range(groups)]
+    if groups > 1:  # every group's slice starts 256-byte aligned
+        nds = [(x + 255) // 256 * 256 for x in nds]
+    return bnd, nds, sum(nds) + (256 if groups > 1 else 0)
+
+
+def operator_workspace_bytes(bh, n_q, n_k, d, n_q_clusters, n_k_clusters, head_groups=None):
+    """Bytes of `workspace_buffer` that let svg_ear_attention run with the given head_groups
+    (None = the operator's own choice) on bh instances."""
+    groups = _auto_groups(bh, n_q, n_k) if head_groups is None else int(head_groups)
+    groups = max(1, min(groups, bh))
+    return _group_layout(bh, n_q, n_k, d, int(n_q_clusters), int(n_k_clusters), groups)[2]
+
+
 def reference_init(q, k, n_q_clusters, n_k_clusters, seed):
     """k-means++ start centres the reference would draw for `prepare(seed=...)`, for every
     instance of a [.., S, d] batch (instance index b uses seed + b).  Host-side numpy; meant for
@@ -39,7 +72,8 @@ def reference_init(q, k, n_q_clusters, n_k_clusters, seed):
 def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_init=None,
                       k_init=None, init="reference", kmeans_iters=25, estimator="valueAware",
                       overshoot="fillRemainder", single_item_fallback=True, check_fp32=False,
-                      return_aux=False, workspace_buffer=None, budget_mode="globalDensity"):
+                      return_aux=False, workspace_buffer=None, budget_mode="globalDensity",
+                      head_groups=None):
     """SVG-EAR attention.
 
     q, k, v : bf16 CUDA tensors [B, H, S, d] (or [H, S, d] / [S, d]); d in {64, 128}.
@@ -53,6 +87,11 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
              device (svgear_kmeans_seed); "strided" -> evenly strided tokens;
              ignored for a side whose q_init / k_init ([.., C, d] float32 centres) is given.
     check_fp32 : run the executor in fp32 on CUDA cores and return a float32 output.
+    head_groups : split the B*H instances into this many contiguous groups and run one
+             svgear_forward per group on its own CUDA stream (joined before returning): the
+             latency-bound phases of one group (late Lloyd iterations, routing) overlap the
+             throughput-bound phases of another.  Results are bit-identical for every value.
+             None -> 2 groups for large batches (>= 16 instances of >= 16k tokens), else 1.
     Returns (out, mask) — out [.., S, d] in ORIGINAL token order, mask [.., C_q, C_k] bool
     (True = block computed exactly) — plus a dict of intermediates when return_aux=True.
     """
@@ -116,11 +155,18 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
     q_init = q_init.to(dev, torch.float32).reshape(bh, c_q, d).contiguous()
     k_init = k_init.to(dev, torch.float32).reshape(bh, c_k, d).contiguous()
 
-    shape = _lib.Shape(bh, n_q, n_k, d, c_q, c_k)
-    need = _lib.workspace_bytes(shape)
+    if head_groups is None:
+        head_groups = _auto_groups(bh, n_q, n_k)
+    groups = max(1, min(int(head_groups), bh))
+    layout = lambda g_count: _group_layout(bh, n_q, n_k, d, c_q, c_k, g_count)
+    bounds, needs, need = layout(groups)
+    if workspace_buffer is not None and groups > 1 and workspace_buffer.numel() * workspace_buffer.element_size() < need:
+        groups = 1  # a caller-sized buffer for the unsplit call: run unsplit rather than fail
+        bounds, needs, need = layout(1)
     ws = workspace_buffer if workspace_buffer is not None else workspace(need, dev)
     if ws.numel() * ws.element_size() < need:
         raise ValueError(f"workspace_buffer too small: need {need} bytes")
+    ws_base = (ws.data_ptr() + 255) // 256 * 256 if groups > 1 else ws.data_ptr()
     out = torch.empty((bh, n_q, d), dtype=torch.float32 if check_fp32 else torch.bfloat16, device=dev)
     mask = torch.empty((bh, c_q, c_k), dtype=torch.uint8, device=dev)
     aux_t, aux_c = {}, None
@@ -145,20 +191,40 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
             mask_entries=torch.zeros((bh,), dtype=torch.int64, device=dev),
             lse=torch.empty((bh, n_q), dtype=f32, device=dev),
         )
-        aux_c = _lib.Aux(**{name: aux_t[name].data_ptr() for name in _lib.Aux.FIELDS})
-    fn, head = "svgear_forward", (q_init.data_ptr(), k_init.data_ptr())
-    if seeded is not None:
-        fn = "svgear_forward_seeded"
-        head = (seeded[0].data_ptr(), seeded[2].data_ptr(), seeded[1], seeded[3], int(seed) & 0xFFFFFFFF) + head
-    rc = getattr(_lib.lib(), fn)(
-        C.byref(shape), qb.data_ptr(), kb.data_ptr(), vb.data_ptr(), *head, int(kmeans_iters), _EST[estimator],
-        0 if budget_mode == "perClusterTopP" else entry_capacity(float(budget), n_q * n_k),
-        _OVERSHOOT[overshoot], 1 if single_item_fallback else 0,
-        _lib.EXEC_FP32_CHECK if check_fp32 else _lib.EXEC_BF16_TENSOR,
-        float(budget) if budget_mode == "perClusterTopP" else 0.0, out.data_ptr(),
-        mask.data_ptr(), C.byref(aux_c) if aux_c is not None else None, ws.data_ptr(),
-        ws.numel() * ws.element_size(), stream_ptr())
-    _lib.check(fn, rc)
+    fn = "svgear_forward_seeded" if seeded is not None else "svgear_forward"
+    capacity = 0 if budget_mode == "perClusterTopP" else entry_capacity(float(budget), n_q * n_k)
+
+    def launch(a, b, ws_ptr, ws_bytes):
+        """svgear_forward for instances [a, b) on the current stream."""
+        row = lambda t: t.data_ptr() + a * t.stride(0) * t.element_size()
+        aux_g = None
+        if return_aux:
+            aux_g = _lib.Aux(**{name: row(aux_t[name]) for name in _lib.Aux.FIELDS})
+        head = (row(q_init), row(k_init))
+        if seeded is not None:
+            head = (row(seeded[0]), row(seeded[2]), seeded[1], seeded[3], int(seed) & 0xFFFFFFFF, a) + head
+        shape_g = _lib.Shape(b - a, n_q, n_k, d, c_q, c_k)
+        rc = getattr(_lib.lib(), fn)(
+            C.byref(shape_g), row(qb), row(kb), row(vb), *head, int(kmeans_iters), _EST[estimator], capacity,
+            _OVERSHOOT[overshoot], 1 if single_item_fallback else 0,
+            _lib.EXEC_FP32_CHECK if check_fp32 else _lib.EXEC_BF16_TENSOR,
+            float(budget) if budget_mode == "perClusterTopP" else 0.0, row(out), row(mask),
+            C.byref(aux_g) if aux_g is not None else None, ws_ptr, ws_bytes, stream_ptr())
+        _lib.check(fn, rc)
+
+    if groups == 1:
+        launch(0, bh, ws.data_ptr(), ws.numel() * ws.element_size())
+    else:
+        cur = torch.cuda.current_stream(dev)
+        streams = _group_streams(dev, groups)
+        off = ws_base
+        for g in range(groups):
+            streams[g].wait_stream(cur)
+            with torch.cuda.stream(streams[g]):
+                launch(bounds[g], bounds[g + 1], off, needs[g])
+            off += needs[g]
+        for g in range(groups):
+            cur.wait_stream(streams[g])
     out = out.reshape(*lead, n_q, d)
     mask_b = mask.bool().reshape(*lead, c_q, c_k)
     if not return_aux:

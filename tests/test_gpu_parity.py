@@ -719,7 +719,35 @@ class TestSeededForward:
         buf = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
         p = buf.data_ptr()
         call = lambda mq, mk, g=p: _lib.lib().svgear_forward_seeded(
-            C.byref(shape), p, p, p, g, p, mq, mk, 0, p, p, 5, 0, 100, 0, 1, 0, 0.0, p, p, None, p, buf.numel(), None)
+            C.byref(shape), p, p, p, g, p, mq, mk, 0, 0, p, p, 5, 0, 100, 0, 1, 0, 0.0, p, p, None, p, buf.numel(), None)
         assert call(4, 64) == _lib.ESHAPE      # fewer subsample tokens than centres
         assert call(64, 512) == _lib.ESHAPE    # more than the instance has
         assert call(64, 64, None) == _lib.EINVAL
+        assert _lib.lib().svgear_forward_seeded(C.byref(shape), p, p, p, p, p, 64, 64, 0, -1, p, p, 5, 0, 100, 0, 1, 0, 0.0, p, p,
+                                                None, p, buf.numel(), None) == _lib.EINVAL
+
+
+class TestHeadGroups:
+    """head_groups only changes which stream an instance runs on: every result is bit-identical."""
+
+    @pytest.mark.parametrize("init", ["device", "reference"])
+    def test_groups_are_bit_identical(self, init):
+        d, H, S, cq, ck = 64, 5, 1200, 12, 30
+        heads = [tuple(O.round_to_bf16(a) for a in O.blob_instance(S, S, d, cq, ck, 0.15, 80 + h)) for h in range(H)]
+        q, k, v = (dev(np.stack([hd[i] for hd in heads])).unsqueeze(0) for i in range(3))
+        base = P.svg_ear_attention(q, k, v, cq, ck, 0.3, seed=3, init=init, return_aux=True, head_groups=1)
+        for g in (2, 3, 5, 9):
+            got = P.svg_ear_attention(q, k, v, cq, ck, 0.3, seed=3, init=init, return_aux=True, head_groups=g)
+            assert torch.equal(got[0], base[0]) and torch.equal(got[1], base[1])
+            for name in base[2]:
+                assert torch.equal(got[2][name], base[2][name]), (g, name)
+
+    def test_caller_workspace_sized_for_one_call_still_works(self):
+        from paper_2603_08982_b200 import _lib
+        d, H, S, cq, ck = 64, 4, 600, 6, 10
+        heads = [tuple(O.round_to_bf16(a) for a in O.blob_instance(S, S, d, cq, ck, 0.15, 90 + h)) for h in range(H)]
+        q, k, v = (dev(np.stack([hd[i] for hd in heads])).unsqueeze(0) for i in range(3))
+        ws = torch.empty(_lib.workspace_bytes(_lib.Shape(H, S, S, d, cq, ck)), dtype=torch.uint8, device="cuda")
+        a = P.svg_ear_attention(q, k, v, cq, ck, 0.3, init="device", workspace_buffer=ws, head_groups=2)
+        b = P.svg_ear_attention(q, k, v, cq, ck, 0.3, init="device", head_groups=1)
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
