@@ -63,6 +63,46 @@ class TestCAbi:
             P.svg_ear_attention(*(torch.zeros(8, 64, dtype=torch.bfloat16),) * 3, 2, 2, 0.25)
 
 
+class TestHeadGroupLayout:
+    """Host-side plan of the operator's head groups (operator._group_layout): groups partition the
+    instances contiguously and the workspace of a split call is the aligned sum of its groups'."""
+
+    def test_partition_and_workspace(self):
+        from paper_2603_08982_b200 import operator as op
+        for bh, groups in ((40, 2), (40, 3), (5, 5), (7, 4), (24, 1)):
+            bnd, needs, total = op._group_layout(bh, 4096, 4096, 64, 32, 64, groups)
+            assert bnd[0] == 0 and bnd[-1] == bh and len(bnd) == groups + 1
+            sizes = [b - a for a, b in zip(bnd, bnd[1:])]
+            assert all(s >= 1 for s in sizes) and max(sizes) - min(sizes) <= 1
+            for s, n in zip(sizes, needs):
+                assert n >= _lib.workspace_bytes(_lib.Shape(s, 4096, 4096, 64, 32, 64))
+                assert groups == 1 or n % 256 == 0
+            assert total == sum(needs) + (256 if groups > 1 else 0)
+
+    def test_operator_workspace_bytes(self):
+        one = P.operator_workspace_bytes(40, 75600, 75600, 128, 300, 1000, head_groups=1)
+        assert one == _lib.workspace_bytes(_lib.Shape(40, 75600, 75600, 128, 300, 1000))
+        auto = P.operator_workspace_bytes(40, 75600, 75600, 128, 300, 1000)
+        two = P.operator_workspace_bytes(40, 75600, 75600, 128, 300, 1000, head_groups=2)
+        assert auto == two  # >= 16 large instances -> two groups
+        assert abs(two - one) < 0.01 * one  # splitting costs alignment, not memory
+        assert P.operator_workspace_bytes(8, 75600, 75600, 128, 300, 1000) == \
+            _lib.workspace_bytes(_lib.Shape(8, 75600, 75600, 128, 300, 1000))
+        assert P.operator_workspace_bytes(3, 512, 512, 64, 4, 4, head_groups=9) == \
+            P.operator_workspace_bytes(3, 512, 512, 64, 4, 4, head_groups=3)
+
+    def test_seeded_forward_argument_errors(self):
+        lib = P.load_library()
+        buf = (C.c_char * 4096)()
+        p = C.addressof(buf)
+        shape = _lib.Shape(1, 256, 256, 64, 8, 8)
+        tail = (5, 0, 100, 0, 1, 0, 0.0, p, p, None, p, 4096, None)
+        assert lib.svgear_forward_seeded(C.byref(shape), p, p, p, None, p, 64, 64, 0, 0, p, p, *tail) == _lib.EINVAL
+        assert lib.svgear_forward_seeded(C.byref(shape), p, p, p, p, p, 64, 64, 0, -1, p, p, *tail) == _lib.EINVAL
+        assert lib.svgear_forward_seeded(C.byref(shape), p, p, p, p, p, 4, 64, 0, 0, p, p, *tail) == _lib.ESHAPE
+        assert lib.svgear_forward_seeded(C.byref(shape), p, p, p, p, p, 64, 8192, 0, 0, p, p, *tail) == _lib.ESHAPE
+
+
 class TestValidationMirrorsReference:
     def test_budget(self):  # tests/test_router.py:52-73
         assert P.DensityBudget.global_density(0.25).rho == 0.25

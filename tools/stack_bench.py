@@ -2,11 +2,14 @@
 attention at a workload shape, on synthetic latents that drift slowly from step to step (per layer a
 fixed blob mixture whose centres random-walk by `--drift` per step, fresh token noise every step).
 
-Two schedules are timed (CUDA events around the whole run, inputs resident):
+Three schedules are timed (CUDA events around the whole run, inputs resident), all through the
+product scheduler `schedule.SvgEarStack`:
   cold : every (layer, step) seeds its k-means on the device (svgear_kmeans_seed_gram);
   warm : step t of a layer starts Lloyd from the centroids of step t-1 of the same layer
          (the reference's warm start, clustering.py:158-163) with the iteration
-         cap --warm-iters (the first step of a layer is cold).
+         cap --warm-iters (the first step of a layer is cold);
+  warm_paper_schedule : as warm, plus the paper's dense warm-up (first 20 % of the steps and layer 0
+         run dense attention).
 With --gpus N (torchrun) the heads are sharded as in bench.py.
 
     python tools/stack_bench.py --layers 4 --steps 6          # quick
@@ -17,7 +20,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import bench
 import paper_2603_08982_b200 as P
-from paper_2603_08982_b200 import _lib
+from paper_2603_08982_b200 import _lib, schedule
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="wan2.2-720p")
@@ -55,32 +58,28 @@ class Layer:
 
 
 layers = [Layer() for _ in range(a.layers)]
-ws = torch.empty(_lib.workspace_bytes(_lib.Shape(H, S, S, d, cq, ck)), dtype=torch.uint8, device=dev)
 
 
-def run(warm):
-    for L in layers:
-        L.q_cent = L.k_cent = None
+def run(warm, dense_warmup=False):
+    """One denoising run through the product scheduler (schedule.SvgEarStack)."""
+    sched = (schedule.WarmupSchedule(a.steps, max(1, a.steps // 5), a.layers, min(1, a.layers - 1))
+             if dense_warmup else schedule.WarmupSchedule.none(a.steps, a.layers))
+    stack = schedule.SvgEarStack(cq, ck, a.rho, schedule=sched, warm_start=warm, warm_iters=a.warm_iters)
     iters = []
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    gen_ms = 0.0
     e0.record()
     for t in range(a.steps):
-        for L in layers:
+        for li, L in enumerate(layers):
             q, k, v = L.sample()
-            kw = {}
-            if warm and L.q_cent is not None:
-                kw = dict(q_init=L.q_cent, k_init=L.k_cent, kmeans_iters=a.warm_iters)
-            out, mask, aux = P.svg_ear_attention(q, k, v, cq, ck, a.rho, init="device", return_aux=True,
-                                                 workspace_buffer=ws, **kw)
-            L.q_cent, L.k_cent = aux["q_centroids"][0], aux["k_centroids"][0]
-            iters.append((aux["q_iters"], aux["k_iters"]))
+            stack.attend(li, t, q, k, v)
+            if not sched.is_dense(li, t):
+                iters.append(stack.lloyd_iterations(li))
     e1.record()
     torch.cuda.synchronize()
-    qi = torch.stack([i[0].float().mean() for i in iters]).mean().item()
-    ki = torch.stack([i[1].float().mean() for i in iters]).mean().item()
-    return e0.elapsed_time(e1), qi, ki
+    qi = torch.stack([i[0].float().mean() for i in iters]).mean().item() if iters else 0.0
+    ki = torch.stack([i[1].float().mean() for i in iters]).mean().item() if iters else 0.0
+    return e0.elapsed_time(e1), qi, ki, dict(stack.calls)
 
 
 # input generation is inside the timed loop; time it alone and subtract
@@ -94,10 +93,16 @@ g1.record()
 torch.cuda.synchronize()
 gen = g0.elapsed_time(g1)
 run(False)  # warm-up
+_q, _k, _v = layers[0].sample()
+torch.nn.functional.scaled_dot_product_attention(_q, _k, _v)  # builds the library's dense plan outside the timing
+del _q, _k, _v
+torch.cuda.synchronize()
 res = {}
-for name, warm in (("cold", False), ("warm", True)):
-    ms, qi, ki = run(warm)
-    n = a.layers * a.steps
-    res[name] = {"total_ms": ms - gen, "ms_per_layer": (ms - gen) / n, "mean_lloyd_iters_q": qi, "mean_lloyd_iters_k": ki}
+n = a.layers * a.steps
+for name, warm, dense in (("cold", False, False), ("warm", True, False), ("warm_paper_schedule", True, True)):
+    ms, qi, ki, calls = run(warm, dense)
+    res[name] = {"total_ms": ms - gen, "ms_per_layer": (ms - gen) / n, "mean_lloyd_iters_q": qi, "mean_lloyd_iters_k": ki,
+                 "calls": calls}
 print(json.dumps({"workload": a.workload, "heads": H, "layers": a.layers, "steps": a.steps, "rho": a.rho,
-                  "drift": a.drift, "warm_iters": a.warm_iters, "input_generation_ms": gen, **res}))
+                  "drift": a.drift, "warm_iters": a.warm_iters, "input_generation_ms": gen,
+                  "paper_schedule": "dense for the first 20% of the steps and for layer 0 (PAPER.md Table config)", **res}))
