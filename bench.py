@@ -401,12 +401,12 @@ def run_ours(args):
         achieved = attend_flops / t_att / 1e12
         # the attend kernel is timed alone between events -> burst peak
         # DRAM bytes of the attention launch from the committed ncu --set full capture
-        # (profiles/r01_ncu_full_summary.txt, 8 Wan2.2 heads: two-half kernel 522.4 MB read + 138.6 MB
-        # written, remainder-tile kernel 402.0 MB read + 4.8 MB written (cold L2 under ncu));
+        # (profiles/r01b_ncu_full_summary.txt, 8 Wan2.2 heads: two-half kernel 521.4 MB read + 140.7 MB
+        # written, remainder-tile kernel 399.1 MB read + 5.6 MB written (cold L2 under ncu));
         # reported only for the workload and executor that capture was taken on
         traffic = None
         if args.workload == "wan2.2-720p" and not args.fp32_check and abs(args.rho - 0.25) < 1e-9:
-            traffic = (522.377472e6 + 138.584832e6 + 402.021376e6 + 4.755200e6) / 8.0 * hl
+            traffic = (521.449728e6 + 140.697600e6 + 399.122432e6 + 5.622528e6) / 8.0 * hl
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk["tf_burst"], "unit": "TFLOP/s",
                 "frac": achieved / pk["tf_burst"], "traffic": traffic,
                 "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum, 8-head capture scaled by heads"
