@@ -751,3 +751,32 @@ class TestHeadGroups:
         a = P.svg_ear_attention(q, k, v, cq, ck, 0.3, init="device", workspace_buffer=ws, head_groups=2)
         b = P.svg_ear_attention(q, k, v, cq, ck, 0.3, init="device", head_groups=1)
         assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+class TestConcurrentCallers:
+    """Calls issued on different caller streams overlap (helper streams are keyed by the caller's
+    stream) and must return what the same calls return one after the other."""
+
+    def test_two_streams_interleaved(self):
+        d, S = 64, 1400
+        cases = []
+        for i, (H, cq, ck, rho) in enumerate(((3, 10, 24, 0.2), (2, 14, 18, 0.4), (4, 6, 30, 0.1))):
+            heads = [tuple(O.round_to_bf16(a) for a in O.blob_instance(S, S, d, cq, ck, 0.15, 300 + 10 * i + h))
+                     for h in range(H)]
+            q, k, v = (dev(np.stack([hd[j] for hd in heads])).unsqueeze(0) for j in range(3))
+            cases.append((q, k, v, cq, ck, rho))
+        serial = [P.svg_ear_attention(*c, init="device", seed=5, return_aux=True) for c in cases]
+        torch.cuda.synchronize()
+        streams = [torch.cuda.Stream() for _ in cases]
+        for _ in range(3):
+            got = [None] * len(cases)
+            for i, c in enumerate(cases):
+                streams[i].wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(streams[i]):
+                    got[i] = P.svg_ear_attention(*c, init="device", seed=5, return_aux=True)
+            for s in streams:
+                torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            for g, r in zip(got, serial):
+                assert torch.equal(g[0], r[0]) and torch.equal(g[1], r[1])
+                assert torch.equal(g[2]["q_perm"], r[2]["q_perm"]) and torch.equal(g[2]["lse"], r[2]["lse"])
