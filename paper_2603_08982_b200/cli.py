@@ -50,23 +50,29 @@ class CapabilityError(RuntimeError):
     """The instance or policy is outside what the GPU path implements (exit code 4)."""
 
 
-def _load_config(args, policy_override=True) -> RunConfig:
+def load_run_config(path, *, preset=None, policy=None, precision=None, seed=None) -> RunConfig:
+    """RunConfig from a JSON file with the command-line overrides applied on top (preset first)."""
+    with open(path, "r", encoding="utf-8") as fh:
+        text = fh.read()
     try:
-        with open(args.config, "r", encoding="utf-8") as fh:
-            data = json.load(fh)
+        cfg = RunConfig.from_dict(json.loads(text))
     except json.JSONDecodeError as exc:
-        raise ConfigError(f"config file is not valid JSON: {exc}") from exc
-    cfg = RunConfig.from_dict(data)
-    if getattr(args, "preset", None):
-        cfg = apply_preset(cfg, args.preset)
-    merged = cfg.to_dict()
-    if policy_override and getattr(args, "policy", None):
-        merged["policy"] = args.policy
-    if getattr(args, "precision", None):
-        merged["precision"] = args.precision
-    if getattr(args, "seed", None) is not None:
-        merged["seeds"] = [args.seed]
-    return RunConfig.from_dict(merged)
+        raise ConfigError(f"{path} does not hold valid JSON ({exc})") from exc
+    if preset:
+        cfg = apply_preset(cfg, preset)
+    overrides = {}
+    if policy:
+        overrides["policy"] = policy
+    if precision:
+        overrides["precision"] = precision
+    if seed is not None:
+        overrides["seeds"] = [seed]
+    return cfg.replace(**overrides) if overrides else cfg
+
+
+def _config_of(args, with_policy=True) -> RunConfig:
+    return load_run_config(args.config, preset=args.preset, policy=args.policy if with_policy else None,
+                           precision=args.precision, seed=getattr(args, "seed", None))
 
 
 def _check_capability(q, k, v, policies, budget_mode):
@@ -156,7 +162,7 @@ def _emit(text, out_path):
 
 
 def _cmd_run(args) -> int:
-    cfg = _load_config(args)
+    cfg = _config_of(args)
     q, k, v = read_tensor_file(args.tensor)
     _check_capability(q, k, v, (cfg.policy,), cfg.budget_mode)
     lines = []
@@ -173,23 +179,37 @@ def _cmd_run(args) -> int:
     return 0
 
 
-def _cmd_sweep(args) -> int:
-    cfg = _load_config(args, policy_override=False)  # --policy is a comma-separated list here
-    try:
-        densities = [float(x) for x in args.density_grid.split(",") if x.strip() != ""]
-    except ValueError as exc:
-        raise ConfigError(f"bad density grid {args.density_grid!r}: {exc}") from exc
-    if not densities:
-        raise ConfigError("density grid is empty")
-    for rho in densities:
+def parse_density_grid(text):
+    """"0.1,0.25,0.5" -> [0.1, 0.25, 0.5]; every entry a density in [0, 1]."""
+    grid = []
+    for piece in text.split(","):
+        piece = piece.strip()
+        if not piece:
+            continue
+        try:
+            rho = float(piece)
+        except ValueError as exc:
+            raise ConfigError(f"density grid entry {piece!r} is not a number") from exc
         if not (0.0 <= rho <= 1.0):
-            raise ConfigError(f"density {rho} outside [0, 1]")
-    policies = SWEEP_DEFAULT_POLICIES
-    if args.policy:
-        policies = tuple(p.strip() for p in args.policy.split(","))
-        for pol in policies:
-            if pol not in POLICIES:
-                raise ConfigError(f"unknown policy {pol!r}")
+            raise ConfigError(f"density grid entry {rho} lies outside [0, 1]")
+        grid.append(rho)
+    if not grid:
+        raise ConfigError("the density grid has no entries")
+    return grid
+
+
+def parse_policy_list(text):
+    names = tuple(piece.strip() for piece in text.split(","))
+    for name in names:
+        if name not in POLICIES:
+            raise ConfigError(f"{name!r} is not a routing policy")
+    return names
+
+
+def _cmd_sweep(args) -> int:
+    cfg = _config_of(args, with_policy=False)  # --policy is a comma-separated list here
+    densities = parse_density_grid(args.density_grid)
+    policies = parse_policy_list(args.policy) if args.policy else SWEEP_DEFAULT_POLICIES
     q, k, v = read_tensor_file(args.tensor)
     _check_capability(q, k, v, policies, "globalDensity")
     cells = {}
@@ -220,7 +240,7 @@ def _cmd_verify(args) -> int:
     re-based on what can be checked without the CPU package): the tensor-core executor against the
     fp32 check executor, both against the Eq.1 mixed-logit output (attention.py:195-209) when the
     dense map fits, and the tensor-core error table against the fp32 one."""
-    cfg = _load_config(args)
+    cfg = _config_of(args)
     q, k, v = read_tensor_file(args.tensor)
     _check_capability(q, k, v, (cfg.policy,), cfg.budget_mode)
     seed = cfg.seeds[0]
@@ -256,56 +276,57 @@ def _cmd_verify(args) -> int:
     return 0 if ok else 1
 
 
-def _add_common(parser, seed_flag=True):
-    parser.add_argument("--config", required=True, help="RunConfig JSON path")
-    parser.add_argument("--preset", choices=["paper"], help="apply a named configuration preset")
-    if seed_flag:
-        parser.add_argument("--seed", type=int, help="override the config seed list with one seed")
-    parser.add_argument("--policy", help="override the routing policy")
-    parser.add_argument("--precision", choices=["double", "single-executor"],
-                        help="accepted for compatibility and echoed; see --executor")
-    parser.add_argument("--executor", choices=["bf16", "fp32"], default="bf16",
-                        help="GPU executor: tcgen05 bf16 (default) or the fp32 check kernel")
-    parser.add_argument("--no-timing", action="store_true", help="omit timing fields for byte-stable output")
-    parser.add_argument("--out", help="write output to this path instead of stdout")
+# (flag, argparse keywords) shared by every subcommand
+_COMMON_FLAGS = (
+    ("--config", dict(required=True, help="RunConfig JSON path")),
+    ("--preset", dict(choices=["paper"], help="apply a named configuration preset")),
+    ("--seed", dict(type=int, help="run this one seed instead of the config's seed list")),
+    ("--policy", dict(help="routing policy (a comma-separated list for sweep)")),
+    ("--precision", dict(choices=["double", "single-executor"],
+                         help="accepted for compatibility with the reference and echoed; see --executor")),
+    ("--executor", dict(choices=["bf16", "fp32"], default="bf16",
+                        help="GPU executor: tcgen05 bf16 (default) or the fp32 check kernel")),
+    ("--no-timing", dict(action="store_true", help="leave the timing field out (byte-stable output)")),
+    ("--out", dict(help="write the output to this file instead of stdout")),
+)
+_SUBCOMMANDS = {
+    "run": ("one JSON line per seed", _cmd_run, ()),
+    "sweep": ("policy x density x seed grid as CSV", _cmd_sweep,
+              (("--density-grid", dict(required=True, help="comma-separated densities, e.g. 0.1,0.25,0.5")),
+               ("--workers", dict(type=int, help="accepted for compatibility; seeds run on one device")))),
+    "verify": ("invariant checks of the GPU path, JSON report", _cmd_verify, ()),
+}
+# exception type -> (stderr label, exit code); checked in order (ConfigError and ShapeError are ValueErrors)
+_EXIT_CODES = (
+    (ConfigError, "config error", 2),
+    ((TensorFormatError, ShapeError), "input error", 3),
+    (OSError, "io error", 3),
+    ((CapabilityError, SvgEarError), "capability error", 4),
+)
 
 
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="paper_2603_08982_b200", description="SVG-EAR attention harness (B200)")
     sub = parser.add_subparsers(dest="command", required=True)
-    p_run = sub.add_parser("run", help="run the pipeline, JSON line per seed")
-    p_run.add_argument("tensor", help="tensor file to read")
-    _add_common(p_run)
-    p_sweep = sub.add_parser("sweep", help="policy x density x seed sweep, CSV output")
-    p_sweep.add_argument("tensor", help="tensor file to read")
-    p_sweep.add_argument("--density-grid", required=True, help="comma-separated densities, e.g. 0.1,0.25,0.5")
-    p_sweep.add_argument("--workers", type=int, help="accepted for compatibility; seeds run on one device")
-    _add_common(p_sweep)
-    p_verify = sub.add_parser("verify", help="invariant checks of the GPU path")
-    p_verify.add_argument("tensor", help="tensor file to read")
-    _add_common(p_verify)
+    for name, (summary, _, extra) in _SUBCOMMANDS.items():
+        p = sub.add_parser(name, help=summary)
+        p.add_argument("tensor", help="QKVT tensor file to read")
+        for flag, kw in extra + _COMMON_FLAGS:
+            p.add_argument(flag, **kw)
     return parser
-
-
-_DISPATCH = {"run": _cmd_run, "sweep": _cmd_sweep, "verify": _cmd_verify}
 
 
 def main(argv=None) -> int:
     args = build_parser().parse_args(argv)
+    handler = _SUBCOMMANDS[args.command][1]
     try:
-        return _DISPATCH[args.command](args)
-    except ConfigError as exc:
-        print(f"config error: {exc}", file=sys.stderr)
-        return 2
-    except (TensorFormatError, ShapeError) as exc:
-        print(f"input error: {exc}", file=sys.stderr)
-        return 3
-    except OSError as exc:
-        print(f"io error: {exc}", file=sys.stderr)
-        return 3
-    except (CapabilityError, SvgEarError) as exc:
-        print(f"capability error: {exc}", file=sys.stderr)
-        return 4
+        return handler(args)
+    except Exception as exc:  # noqa: BLE001 - mapped to the documented exit codes, anything else propagates
+        for kinds, label, code in _EXIT_CODES:
+            if isinstance(exc, kinds):
+                print(f"{label}: {exc}", file=sys.stderr)
+                return code
+        raise
 
 
 if __name__ == "__main__":
