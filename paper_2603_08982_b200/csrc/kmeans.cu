@@ -929,6 +929,7 @@ int launch_seed_pp(int bh, int n, int d, int c, const bf16* x, int oversample, u
 namespace svg {
 
 constexpr int kGramPer = 4;  // samples per thread (m <= 4096)
+constexpr int kGramBatch = 8;  // centres drawn per round while many remain (graded down towards the end)
 
 __global__ void __launch_bounds__(1024)
     seed_gram_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gram, int n, int d, int c, int m,
@@ -936,7 +937,7 @@ __global__ void __launch_bounds__(1024)
   const int h = blockIdx.x;
   __shared__ float s_warp[32];
   __shared__ float s_total;
-  __shared__ int s_pick[kSeedBatch];
+  __shared__ int s_pick[kGramBatch];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bf16* xh = x + (size_t)h * n * d;
   const bf16* gh = gram + (size_t)h * m * m;
@@ -950,7 +951,7 @@ __global__ void __launch_bounds__(1024)
     nrm[e] = s < m ? __bfloat162float(gh[(size_t)s * m + s]) : 0.f;
     mind[e] = s < m ? INFINITY : 0.f;
   }
-  int picks[kSeedBatch];
+  int picks[kGramBatch];
   picks[0] = (int)(hash_u32(seed, (uint32_t)(first + h), 0u) % (uint32_t)m);
   int cnt = 1, npicked = 0;
   while (true) {
@@ -990,7 +991,7 @@ __global__ void __launch_bounds__(1024)
     }
     __syncthreads();  // previous round's readers of s_warp / s_pick are done
     if (lane == 31) s_warp[warp] = inc;
-    if (tid < kSeedBatch) s_pick[tid] = -1;
+    if (tid < kGramBatch) s_pick[tid] = -1;
     __syncthreads();
     if (warp == 0) {
       float w = s_warp[lane], wi = w;
@@ -1005,7 +1006,9 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
     const float total = s_total;
     const int left = c - npicked;
-    const int next = left >= 128 ? kSeedBatch : 1;
+    // the draws of a round share one D^2 distribution; the later a centre is drawn the more the
+    // distribution it is drawn from matters, so the batch shrinks towards the end
+    const int next = left >= 256 ? kGramBatch : (left >= 128 ? 4 : (left >= 32 ? 2 : 1));
     if (total > 0.f && mine > 0.f) {
       const float lo = s_warp[warp] + inc - mine;
       for (int i = 0; i < next; ++i) {
