@@ -269,3 +269,47 @@ class TestDitBlock:
         y1 = blk(x, full, 0, 0, rope=rope)
         assert full.calls["cold"] == 1
         assert float((y1.float() - ref.float().detach()).norm() / ref.float().detach().norm()) < 2e-2
+
+
+@pytest.mark.gpu
+class TestStackPaperMode:
+    def test_top_p_budget_through_the_stack_equals_the_operator(self):
+        """The paper's production setting (perClusterTopP, p = 0.85) through SvgEarStack: a cold call is
+        the operator call, a warm call is the operator call started from the cached centroids."""
+        S, d, cq, ck, H = 768, 64, 8, 16, 3
+        data = _drifted_instances(S, d, cq, ck, 2, H)
+        stack = schedule.SvgEarStack(cq, ck, 0.85, budget_mode="perClusterTopP",
+                                     schedule=schedule.WarmupSchedule.none(2, 1), warm_iters=5)
+        mk = lambda t: tuple(torch.from_numpy(np.stack([data[h][t][i] for h in range(H)])).to("cuda", torch.bfloat16)
+                             .unsqueeze(0) for i in range(3))
+        q0, k0, v0 = mk(0)
+        out0, mask0 = stack.attend(0, 0, q0, k0, v0, return_mask=True)
+        ref0 = P.svg_ear_attention(q0, k0, v0, cq, ck, 0.85, budget_mode="perClusterTopP", init="device", seed=0,
+                                   return_aux=True)
+        assert torch.equal(out0, ref0[0]) and torch.equal(mask0, ref0[1])
+        q1, k1, v1 = mk(1)
+        out1, mask1 = stack.attend(0, 1, q1, k1, v1, return_mask=True)
+        ref1 = P.svg_ear_attention(q1, k1, v1, cq, ck, 0.85, budget_mode="perClusterTopP", kmeans_iters=5,
+                                   q_init=ref0[2]["q_centroids"], k_init=ref0[2]["k_centroids"])
+        assert torch.equal(out1, ref1[0]) and torch.equal(mask1, ref1[1])
+        # every query cluster keeps at least its own top-p share of key clusters exact
+        assert bool(mask1.any(dim=-1).all())
+
+    def test_hunyuan_style_block_with_text_tokens(self):
+        torch.manual_seed(1)
+        dim, h, video, text = 256, 2, 512, 64
+        blk = dit.SvgEarSelfAttention(dim, h, norm="head", device="cuda")
+        x = torch.randn(1, video + text, dim, device="cuda").to(torch.bfloat16)
+        rope = dit.rope_table_3d((2, 16, 16), 128, device="cuda")  # covers the video tokens only
+        dense = schedule.SvgEarStack(8, 12, 0.25, schedule=schedule.WarmupSchedule(1, 1, 1, 1))
+        y = blk(x, dense, 0, 0, rope=rope)
+        qkv = blk.qkv(x)
+        rq, rk, rv = _prologue_reference(qkv, h, 128, "head", blk.q_norm_weight, blk.k_norm_weight, blk.eps, rope,
+                                         "interleaved")
+        # text rows are normalised but not rotated
+        q, k, v = dit.qkv_prologue(qkv, h, norm="head", q_weight=blk.q_norm_weight, k_weight=blk.k_norm_weight,
+                                   eps=blk.eps, rope=rope)
+        assert bool(((q.float() - rq).abs() <= 2.0 ** -8 * rq.abs() + 1e-6).all())
+        o = torch.nn.functional.scaled_dot_product_attention(rq, rk, rv)
+        ref = blk.proj(o.permute(0, 2, 1, 3).reshape(1, video + text, dim).to(torch.bfloat16)).float().detach()
+        assert float((y.float() - ref).norm() / ref.norm()) < 2e-2
