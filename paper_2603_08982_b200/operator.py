@@ -16,7 +16,7 @@ import torch
 from . import _lib
 from ._tensors import ShapeError, require_cuda, stream_ptr, workspace
 from .analysis import side_seeds
-from .clustering import _seed_inputs, device_start, device_start_pair, seeded_start, strided_start
+from .clustering import _seed_inputs, device_start_pair, seeded_start, strided_start
 from .router import _OVERSHOOT, entry_capacity
 
 _EST = {"valueAware": _lib.EST_VALUE_AWARE, "plain": _lib.EST_PLAIN}
@@ -169,7 +169,7 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
     ws_base = (ws.data_ptr() + 255) // 256 * 256 if groups > 1 else ws.data_ptr()
     out = torch.empty((bh, n_q, d), dtype=torch.float32 if check_fp32 else torch.bfloat16, device=dev)
     mask = torch.empty((bh, c_q, c_k), dtype=torch.uint8, device=dev)
-    aux_t, aux_c = {}, None
+    aux_t = {}
     if return_aux:
         i32, f32 = torch.int32, torch.float32
         aux_t = dict(

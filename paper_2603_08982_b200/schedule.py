@@ -21,8 +21,7 @@ from dataclasses import dataclass, field
 
 import torch
 
-from . import _lib
-from .operator import svg_ear_attention
+from .operator import operator_workspace_bytes, svg_ear_attention
 
 
 @dataclass(frozen=True)
@@ -113,49 +112,46 @@ class SvgEarStack:
         self._layers.clear()
         self.calls = {"dense": 0, "cold": 0, "warm": 0}
 
-    def plan(self, layer: int, step: int) -> str:
-        """'dense' | 'cold' | 'warm' — what `attend(layer, step, ...)` would do now."""
+    def plan(self, layer: int, step: int, q=None, k=None) -> str:
+        """'dense' | 'cold' | 'warm' — what `attend(layer, step, ...)` does now.  A warm start needs
+        the layer's centroids from step - 1 and, when q and k are given, centroids of their shape."""
         if self.schedule.is_dense(layer, step):
             return "dense"
         st = self._layers.get(layer)
-        if self.warm_start and st is not None and st.q_centroids is not None and st.last_step == step - 1:
-            return "warm"
-        return "cold"
+        if not (self.warm_start and st is not None and st.q_centroids is not None and st.last_step == step - 1):
+            return "cold"
+        if q is not None and k is not None:
+            want_q = tuple(q.shape[:-2]) + (self.n_q_clusters, q.shape[-1])
+            want_k = tuple(k.shape[:-2]) + (self.n_k_clusters, k.shape[-1])
+            if tuple(st.q_centroids.shape) != want_q or tuple(st.k_centroids.shape) != want_k:
+                return "cold"  # the layer's shape changed: its cached centres are meaningless
+        return "warm"
 
-    def _workspace(self, shape, device):
-        need = _lib.workspace_bytes(shape)
+    def _workspace(self, bh, n_q, n_k, d, device):
+        need = operator_workspace_bytes(bh, n_q, n_k, d, self.n_q_clusters, self.n_k_clusters)
         if self._ws is None or self._ws.numel() < need or self._ws.device != device:
             self._ws = torch.empty(need, dtype=torch.uint8, device=device)
         return self._ws
 
     def attend(self, layer, step, q, k, v, *, return_mask=False):
-        mode = self.plan(layer, step)
+        mode = self.plan(layer, step, q, k)
         self.calls[mode] += 1
         if mode == "dense":
             out = torch.nn.functional.scaled_dot_product_attention(q, k, v)
             return (out, None) if return_mask else out
         st = self._layers.setdefault(layer, _LayerState())
-        kw = {}
         if mode == "warm":
-            c_shape_q = tuple(q.shape[:-2]) + (self.n_q_clusters, q.shape[-1])
-            c_shape_k = tuple(k.shape[:-2]) + (self.n_k_clusters, k.shape[-1])
-            if tuple(st.q_centroids.shape) == c_shape_q and tuple(st.k_centroids.shape) == c_shape_k:
-                kw = dict(q_init=st.q_centroids, k_init=st.k_centroids, kmeans_iters=self.warm_iters)
-            else:  # the layer's shape changed: its cached centres are meaningless
-                self.calls["warm"] -= 1
-                self.calls["cold"] += 1
-                mode = "cold"
-        if mode == "cold":
+            kw = dict(q_init=st.q_centroids, k_init=st.k_centroids, kmeans_iters=self.warm_iters)
+        else:
             kw = dict(init=self.init, kmeans_iters=self.cold_iters)
         lead = q.shape[:-2]
         bh = 1
         for x in lead:
             bh *= int(x)
-        shape = _lib.Shape(bh, q.shape[-2], k.shape[-2], q.shape[-1], self.n_q_clusters, self.n_k_clusters)
         out, mask, aux = svg_ear_attention(
             q, k, v, self.n_q_clusters, self.n_k_clusters, self.budget, budget_mode=self.budget_mode,
             seed=self.seed + layer, estimator=self.estimator, return_aux=True,
-            workspace_buffer=self._workspace(shape, q.device), **kw)
+            workspace_buffer=self._workspace(bh, q.shape[-2], k.shape[-2], q.shape[-1], q.device), **kw)
         st.q_centroids, st.k_centroids = aux["q_centroids"], aux["k_centroids"]
         st.q_iters, st.k_iters = aux["q_iters"], aux["k_iters"]
         st.last_step = step
