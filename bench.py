@@ -396,7 +396,7 @@ def run_ours(args):
     # ---- stage timings (CUDA events on the launching stream) for the roofline -------------------
     stages, roof, density, iters = {}, None, None, None
     if hl > 0:
-        stages, attend_flops, density, iters = stage_times(torch, P, _lib, q, k, v, cq, ck, args, max(2, min(args.steps, 3)))
+        stages, attend_flops, density, iters = stage_times(torch, P, _lib, q, k, v, cq, ck, args, 3)
         t_att = stages["attend"] * 1e-3
         achieved = attend_flops / t_att / 1e12
         # the attend kernel is timed alone between events -> burst peak
@@ -444,7 +444,7 @@ def run_ours(args):
             "dtype": "f32" if args.fp32_check else "bf16", "data": "synthetic",
             "config": {"workload": args.workload, "heads": H, "seq_len": S, "head_dim": d, "c_q": cq,
                        "c_k": ck, "rho": args.rho, "kmeans_max_iters": args.kmeans_iters,
-                       "kmeans_iters_run": iters, "kmeans_init": {"device": "k-means++ on a strided 8x subsample, on device (svgear_kmeans_seed)",
+                       "kmeans_iters_run": iters, "kmeans_init": {"device": "k-means++ on a strided 8x subsample, on device (inside svgear_forward_seeded)",
                                        "strided": "strided tokens"}[args.init],
                        "inputs": f"per-head blob mixture sigma={args.sigma}, generated on device",
                        "executor": "fp32-check" if args.fp32_check else "bf16-tcgen05",
@@ -508,12 +508,15 @@ def stage_times(torch, P, _lib, q, k, v, cq, ck, args, reps):
             continue  # warm-up
         for (_, a), (name, b) in zip(marks, marks[1:]):
             if not name.startswith("_"):
-                acc[name] = acc.get(name, 0.0) + a.elapsed_time(b) / reps
+                acc.setdefault(name, []).append(a.elapsed_time(b))
         flops = float(res.flops.exact_block + res.flops.compensation)
         density = float(mask.density.double().mean())
         iters = {"q_max": int(rq["iters"].max()), "k_max": int(rk["iters"].max())}
-    # error_table stage above includes a redundant segment_means inside the mirror call; report as is
-    return acc, flops, density, iters
+    # error_table stage above includes a redundant segment_means inside the mirror call; report as is.
+    # Median over the repetitions: the mirror calls allocate their workspaces, and one cudaMalloc in
+    # one repetition (a host stall between two events) would otherwise dominate a stage's mean.
+    med = lambda xs: sorted(xs)[len(xs) // 2] if len(xs) % 2 else 0.5 * (sorted(xs)[len(xs) // 2 - 1] + sorted(xs)[len(xs) // 2])
+    return {name: med(xs) for name, xs in acc.items()}, flops, density, iters
 
 
 if __name__ == "__main__":

@@ -90,6 +90,10 @@ typedef struct SvgEarAux {
   float* stabilizers;   /* [bh][c_q] per-row reference logit the sums were taken at                */
   int64_t* mask_entries;/* [bh] entries covered by selected blocks (BlockMask.density_entries)     */
   float* lse;           /* [bh][n_q] final log-sum-exp per query, ORIGINAL token order             */
+  void* kmeans_done_event; /* optional cudaEvent_t (not an output array): recorded on `stream` once both
+                           Lloyd loops and the permuted copies of this call are complete, so a caller
+                           can start another call's latency-bound clustering under this call's
+                           attention kernel                                                        */
 } SvgEarAux;
 
 const char* svgear_strerror(int status);

@@ -46,7 +46,7 @@ class Aux(C.Structure):
     FIELDS = ("q_assign", "k_assign", "q_perm", "k_perm", "q_sizes", "k_sizes", "q_offsets",
               "k_offsets", "q_centroids", "k_centroids", "v_centroids", "q_iters", "k_iters",
               "error_table", "stabilizers", "mask_entries", "lse")
-    _fields_ = [(n, C.c_void_p) for n in FIELDS]
+    _fields_ = [(n, C.c_void_p) for n in FIELDS] + [("kmeans_done_event", C.c_void_p)]
 
 
 # symbol -> argtypes; every symbol include/svgear.h declares must appear here

@@ -426,6 +426,7 @@ int forward_impl(const SvgEarShape* shape, const void* q, const void* k, const v
   }
   if (rc) return rc;
   if (rc_k) return rc_k;
+  if (a.kmeans_done_event) SVG_CUDA_OK(cudaEventRecord((cudaEvent_t)a.kmeans_done_event, st));
   // (2) error table + routing
   rc = launch_error_table(s, exec_mode, estimator_mode, q_cent, k_cent, v_cent, p.kp, p.vp, q_sizes,
                           k_sizes, k_offsets, err, stab, p.es, st, keys_early);

@@ -73,7 +73,7 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
                       k_init=None, init="reference", kmeans_iters=25, estimator="valueAware",
                       overshoot="fillRemainder", single_item_fallback=True, check_fp32=False,
                       return_aux=False, workspace_buffer=None, budget_mode="globalDensity",
-                      head_groups=None):
+                      head_groups=None, stagger_groups=False):
     """SVG-EAR attention.
 
     q, k, v : bf16 CUDA tensors [B, H, S, d] (or [H, S, d] / [S, d]); d in {64, 128}.
@@ -92,6 +92,11 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
              latency-bound phases of one group (late Lloyd iterations, routing) overlap the
              throughput-bound phases of another.  Results are bit-identical for every value.
              None -> 2 groups for large batches (>= 16 instances of >= 16k tokens), else 1.
+    stagger_groups : group g + 1 starts when group g has finished its k-means (an event recorded
+             inside svgear_forward), so its latency-bound clustering runs under group g's attention
+             kernel instead of next to group g's clustering.  Same results either way; measured
+             SLOWER at the Wan2.2 shape (46.8 vs 45.0 ms: the chain of small clustering kernels
+             queues behind 0.3 ms attention CTAs on every SM), hence off by default.
     Returns (out, mask) — out [.., S, d] in ORIGINAL token order, mask [.., C_q, C_k] bool
     (True = block computed exactly) — plus a dict of intermediates when return_aux=True.
     """
@@ -194,12 +199,14 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
     fn = "svgear_forward_seeded" if seeded is not None else "svgear_forward"
     capacity = 0 if budget_mode == "perClusterTopP" else entry_capacity(float(budget), n_q * n_k)
 
-    def launch(a, b, ws_ptr, ws_bytes):
+    def launch(a, b, ws_ptr, ws_bytes, done_event=None):
         """svgear_forward for instances [a, b) on the current stream."""
         row = lambda t: t.data_ptr() + a * t.stride(0) * t.element_size()
         aux_g = None
-        if return_aux:
-            aux_g = _lib.Aux(**{name: row(aux_t[name]) for name in _lib.Aux.FIELDS})
+        if return_aux or done_event is not None:
+            aux_g = _lib.Aux(**({name: row(aux_t[name]) for name in _lib.Aux.FIELDS} if return_aux else {}))
+            if done_event is not None:
+                aux_g.kmeans_done_event = done_event.cuda_event
         head = (row(q_init), row(k_init))
         if seeded is not None:
             head = (row(seeded[0]), row(seeded[2]), seeded[1], seeded[3], int(seed) & 0xFFFFFFFF, a) + head
@@ -218,10 +225,18 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
         cur = torch.cuda.current_stream(dev)
         streams = _group_streams(dev, groups)
         off = ws_base
+        prev_done = None
         for g in range(groups):
             streams[g].wait_stream(cur)
+            if prev_done is not None:
+                streams[g].wait_event(prev_done)
+            done = None
             with torch.cuda.stream(streams[g]):
-                launch(bounds[g], bounds[g + 1], off, needs[g])
+                if stagger_groups and g + 1 < groups:
+                    done = torch.cuda.Event()
+                    done.record(streams[g])  # creates the handle; re-recorded inside the call
+                launch(bounds[g], bounds[g + 1], off, needs[g], done)
+            prev_done = done
             off += needs[g]
         for g in range(groups):
             cur.wait_stream(streams[g])

@@ -780,3 +780,13 @@ class TestConcurrentCallers:
             for g, r in zip(got, serial):
                 assert torch.equal(g[0], r[0]) and torch.equal(g[1], r[1])
                 assert torch.equal(g[2]["q_perm"], r[2]["q_perm"]) and torch.equal(g[2]["lse"], r[2]["lse"])
+
+
+def test_staggered_head_groups_are_bit_identical():
+    d, H, S, cq, ck = 64, 4, 1100, 10, 20
+    heads = [tuple(O.round_to_bf16(a) for a in O.blob_instance(S, S, d, cq, ck, 0.15, 400 + h)) for h in range(H)]
+    q, k, v = (dev(np.stack([hd[i] for hd in heads])).unsqueeze(0) for i in range(3))
+    base = P.svg_ear_attention(q, k, v, cq, ck, 0.3, init="device", head_groups=1)
+    for g in (2, 4):
+        got = P.svg_ear_attention(q, k, v, cq, ck, 0.3, init="device", head_groups=g, stagger_groups=True)
+        assert torch.equal(got[0], base[0]) and torch.equal(got[1], base[1])
