@@ -13,14 +13,16 @@ Metric: effective TFLOP/s = dense attention FLOPs of the layer (4*H*S^2*d) / lay
 dense-equivalent throughput; `ms_per_step` is ms/layer.  `value` is measured with inputs resident
 in HBM; `e2e` runs the same call with pinned HOST buffers (H2D of q,k,v and D2H of output+mask
 inside the timed region).  `roofline` reports the fused attention kernel's achieved tensor
-TFLOP/s against the measured bf16 peak, from CUDA-event stage timings taken in this process.
+TFLOP/s against the measured bf16 peak, from CUDA-event stage timings taken in this process;
+`stages_roofline` puts the bandwidth-bound stages against the measured HBM peak (SURVEY 8d bytes).
+The headline runs on `--inputs` (default: blobs, the best case); `config.inputs_sweep` repeats the
+resident-input measurement on the other input kinds (ragged cluster sizes, unstructured iid tokens).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -38,6 +40,12 @@ WORKLOADS = {
 }
 METRIC = "svg_ear_attention_effective_tflops"
 UNIT = "TFLOP/s (dense-equivalent: 4*H*S^2*d / layer time)"
+INPUT_KINDS = ("blobs", "ragged", "iid")
+INPUT_DESC = {
+    "blobs": "per-head mixture of equal-size Gaussian blobs, as many as clusters, sigma={sigma} (best case)",
+    "ragged": "per-head mixture of 0.7*C_q / 1.3*C_k Gaussian blobs with Dirichlet(0.5) sizes, sigma={sigma}",
+    "iid": "iid N(0,1) tokens (no structure; Lloyd does not converge)",
+}
 
 
 def parse():
@@ -47,8 +55,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="wan2.2-720p", choices=sorted(WORKLOADS))
+    ap.add_argument("--inputs", default="blobs", choices=INPUT_KINDS)
+    ap.add_argument("--no-sweep", action="store_true", help="skip config.inputs_sweep (the other input kinds)")
     ap.add_argument("--rho", type=float, default=0.25)
-    ap.add_argument("--kmeans-iters", type=int, default=25)
+    ap.add_argument("--kmeans-iters", type=int, default=25, help="Lloyd iteration cap (the reference's default)")
+    ap.add_argument("--kmeans-iters-iid", type=int, default=8,
+                    help="Lloyd iteration cap on unstructured (iid) input, where Lloyd never converges")
     ap.add_argument("--heads", type=int, default=0, help="override head count (debug)")
     ap.add_argument("--fp32-check", action="store_true", help="run the fp32 CUDA-core executor")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -73,6 +85,19 @@ def peaks():
         return dict(hbm=p["hbm_gbs"], tf_burst=p["bf16_tflops"], tf_sustained=p["bf16_tflops_sustained"],
                     source="MEASURED_PEAKS.json")
     return dict(hbm=6650.0, tf_burst=1590.0, tf_sustained=1400.0, source="fallback (B200_PROFILING.md)")
+
+
+def committed_traffic(workload, kind, heads):
+    """DRAM bytes of the attention launches from a committed `ncu --set full` capture
+    (profiles/attention_traffic.json, written by tools/ncu_full_summary.py), scaled from the heads of
+    the capture to the heads of this run; None when no capture exists for this workload/input."""
+    path = os.path.join(ROOT, "profiles", "attention_traffic.json")
+    if not os.path.exists(path):
+        return None, None
+    rec = json.load(open(path)).get(f"{workload}/{kind}")
+    if not rec:
+        return None, None
+    return rec["dram_bytes"] / rec["heads"] * heads, rec["source"]
 
 
 # ------------------------------------------------------------------------------------------------
@@ -111,46 +136,121 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------------
-# synthetic workload: per-head Gaussian blob mixture (the reference generator's structure,
-# analysis.py:86-118, drawn on the device), seeded per GLOBAL head index
+# synthetic workload, generated on the device, seeded per GLOBAL head index
 # ------------------------------------------------------------------------------------------------
-def make_heads(torch, lo, hi, S, d, cq, ck, sigma, device):
+def make_heads(torch, lo, hi, S, d, cq, ck, sigma, device, kind="blobs"):
+    """Synthetic Q, K, V [1, hi-lo, S, d] bf16, generated on the device, seeded per GLOBAL head.
+    blobs : equal-size Gaussian blobs, as many as clusters (the reference generator's structure,
+            analysis.py:86-118; the best case: Lloyd converges fast and query clusters fill the
+            executor's 256-row tiles);
+    ragged: blob sizes drawn from a Dirichlet(0.5) partition and a blob count that does not match the
+            cluster count (0.7*C_q query blobs, 1.3*C_k key blobs): ragged cluster sizes, split and
+            merged blobs;
+    iid   : N(0,1) tokens with no structure (SURVEY 8d stress case: Lloyd never converges)."""
     qs, ks, vs = [], [], []
     for h in range(lo, hi):
         g = torch.Generator(device=device).manual_seed(1000 + h)
         def blobs(nb):
             centres = torch.randn(nb, d, generator=g, device=device)
-            labels = torch.arange(S, device=device).remainder(nb)[torch.randperm(S, generator=g, device=device)]
+            if kind == "ragged":
+                w = torch._standard_gamma(torch.full((nb,), 0.5, device=device), generator=g) + 1e-3
+                labels = torch.multinomial(w / w.sum(), S, replacement=True, generator=g)
+            else:
+                labels = torch.arange(S, device=device).remainder(nb)[torch.randperm(S, generator=g, device=device)]
             return centres[labels] + sigma * torch.randn(S, d, generator=g, device=device), labels
-        q, _ = blobs(cq)
-        k, lab = blobs(ck)
-        vc = torch.randn(ck, d, generator=g, device=device)
-        v = vc[lab] + sigma * torch.randn(S, d, generator=g, device=device)
+        if kind == "iid":
+            q, k, v = (torch.randn(S, d, generator=g, device=device) for _ in range(3))
+        else:
+            nq, nk = (cq, ck) if kind == "blobs" else (max(1, int(0.7 * cq)), int(1.3 * ck))
+            q, _ = blobs(nq)
+            k, lab = blobs(nk)
+            vc = torch.randn(nk, d, generator=g, device=device)
+            v = vc[lab] + sigma * torch.randn(S, d, generator=g, device=device)
         qs.append(q.to(torch.bfloat16)); ks.append(k.to(torch.bfloat16)); vs.append(v.to(torch.bfloat16))
     st = lambda xs: torch.stack(xs).unsqueeze(0).contiguous()
     return st(qs), st(ks), st(vs)
 
 
 # ------------------------------------------------------------------------------------------------
-# CPU arm: the oracle port of the reference path on a bounded sample of the workload
+# CPU arm: the oracle port of the reference path, ONE head at the FULL workload shape, every stage
+# timed on a bounded part of its units and scaled by the exact unit count
 # ------------------------------------------------------------------------------------------------
-def cpu_sample(workload, rho, sigma, shrink):
-    """One head of the workload with S, C_q, C_k all divided by `shrink` (every stage's cost scales
-    by shrink^2, so layer time ~= sample time * shrink^2 * H).  Returns (seconds, description)."""
+def cpu_sample(workload, rho, sigma, frac, iters_q, iters_k):
+    """Seconds per head of prepare -> build_error_table -> route_error_aware -> sparse_attend
+    (oracle/svgear_oracle.py, float64 numpy, all BLAS threads) at the full S, C_q, C_k of the
+    workload.  A whole head takes minutes on the host, so every stage runs on a fraction `frac` of its
+    own units and is scaled by the unit count: k-means++ seeding by centres drawn, Lloyd by iterations
+    (one full iteration per side is timed; the iteration counts are the ones the GPU run needed on
+    the same kind of input), the estimator by key clusters, the router by table rows, the executor
+    by query clusters.  Returns (seconds per head, per-stage seconds, description)."""
     import numpy as np
+    from types import SimpleNamespace
     from oracle import svgear_oracle as O
 
     H, S, d, cq, ck = WORKLOADS[workload]
-    s, a, b = S // shrink, max(2, cq // shrink), max(2, ck // shrink)
-    q, k, v = (O.round_to_bf16(x) for x in O.blob_instance(s, s, d, a, b, sigma, 1000))
-    t0 = time.perf_counter()
-    res = O.forward(q, k, v, a, b, rho, seed=0)
-    dt = time.perf_counter() - t0
-    desc = (f"oracle port of prepare->build_error_table->route_error_aware->sparse_attend on 1 head, "
-            f"S={s} d={d} C_q={a} C_k={b} rho={rho} (workload/{shrink} in S, C_q, C_k); layer time "
-            f"extrapolated x{shrink * shrink} (work per head) x{H} heads; k-means iters q/k="
-            f"{res.prep.q_model.iters}/{res.prep.k_model.iters}")
-    return dt, desc
+    q, k, v = (O.round_to_bf16(x) for x in O.blob_instance(S, S, d, cq, ck, sigma, 1000))
+    stage = {}
+    take = lambda n: max(1, min(n, int(round(n * frac))))
+    tick = time.perf_counter
+
+    # (1) k-means++ seeding (clustering.py:65-84): `rounds` of the C sequential D^2 rounds per side
+    for name, x, c in (("seed_q", q, cq), ("seed_k", k, ck)):
+        rounds = max(2, take(c))
+        t0 = tick()
+        O.kmeanspp_centres(x, rounds, np.random.default_rng(0))
+        stage[name] = (tick() - t0) * c / rounds
+    # (2) Lloyd (clustering.py:104-141): one full iteration per side (distances, argmin, sizes, means)
+    models = {}
+    for name, x, c, iters in (("lloyd_q", q, cq, iters_q), ("lloyd_k", k, ck, iters_k)):
+        centres = x[(np.arange(c) * S) // c].copy()
+        t0 = tick()
+        dist = O.squared_distances(x, centres)
+        labels = dist.argmin(axis=1)
+        own = dist[np.arange(S), labels]
+        np.bincount(labels, minlength=c)
+        float(own.sum())
+        del dist
+        # every cluster non-empty for the mean update of the timing run
+        labels[(np.arange(c) * S) // c] = np.arange(c)
+        O.means_by_label(x, labels, c)
+        stage[name] = (tick() - t0) * iters
+        t0 = tick()
+        models[name[-1]] = O.cluster_model(x, labels, c)  # final means, stable argsort, offsets
+        stage["model_" + name[-1]] = tick() - t0
+    qm, km = models["q"], models["k"]
+    t0 = tick()
+    qp, kp, vp = q[qm.permutation], k[km.permutation], v[km.permutation]
+    stage["permute"] = tick() - t0
+    # (3) streaming estimator (estimator.py:187-253) on the first `jk` key clusters
+    jk = take(ck)
+    sub = SimpleNamespace(num_clusters=jk, centroids=km.centroids[:jk], sizes=km.sizes[:jk], offsets=km.offsets[:jk],
+                          assignments=km.assignments, permutation=km.permutation, iters=0)
+    t0 = tick()
+    O.error_table_streaming(qm, sub, kp, vp)
+    keys = int(km.sizes[:jk].sum())
+    stage["error_table"] = (tick() - t0) * S / max(1, keys)
+    # (4) router (estimator.py:83-96, router.py:100-190) on the first `iq` table rows
+    iq = take(cq)
+    rng = np.random.default_rng(1)
+    table = SimpleNamespace(error_sum=rng.random((iq, ck)) * qm.sizes[:iq, None], q_sizes=qm.sizes[:iq].copy(),
+                            k_sizes=km.sizes.copy(), stabilizers=np.zeros(iq), mode="valueAware")
+    t0 = tick()
+    mask = O.route_error_aware(table, rho)
+    stage["route"] = (tick() - t0) * cq / iq
+    # (5) executor (attention.py:57-192) on the first `iq` query clusters
+    subq = SimpleNamespace(num_clusters=iq, centroids=qm.centroids[:iq], sizes=qm.sizes[:iq], offsets=qm.offsets[:iq],
+                           assignments=qm.assignments, permutation=qm.permutation, iters=0)
+    rows = int(qm.sizes[:iq].sum())
+    t0 = tick()
+    O.sparse_attend(qp[: int(qm.offsets[iq - 1] + qm.sizes[iq - 1])], kp, vp, subq, km, mask.selected)
+    stage["attend"] = (tick() - t0) * S / max(1, rows)
+    total = sum(stage.values())
+    desc = (f"oracle port (float64 numpy) of prepare->build_error_table->route_error_aware->sparse_attend on ONE head "
+            f"at the full shape S={S} d={d} C_q={cq} C_k={ck} rho={rho}; per stage a {frac:.3f} fraction of its units "
+            f"is timed and scaled by the unit count: k-means++ rounds, 1 Lloyd iteration per side x iterations "
+            f"q/k={iters_q}/{iters_k} (as the GPU run needed), {jk}/{ck} key clusters of the estimator, {iq}/{cq} "
+            f"rows of the router and of the executor; layer time = head time x {H} heads")
+    return total, {n: round(t, 3) for n, t in stage.items()}, desc
 
 
 def run_reference(args):
@@ -160,15 +260,17 @@ def run_reference(args):
     H, S, d, cq, ck = WORKLOADS[args.workload]
     if args.heads:
         H = args.heads
-    shrink = 3 if S > 20000 else 1
     cores = os.cpu_count()
-    times = []
-    desc = ""
-    for i in range(args.warmup + args.steps):
-        dt, desc = cpu_sample(args.workload, args.rho, args.sigma, shrink)
+    n_runs = args.warmup + args.steps
+    # whole arm within a few minutes: a full head costs ~300 s on 8-16 cores
+    frac = max(0.004, min(0.1, 200.0 / max(1, n_runs) / 300.0)) if S > 20000 else 1.0
+    iters = (args.kmeans_iters_iid,) * 2 if args.inputs == "iid" else (20, 9)
+    times, stages, desc = [], {}, ""
+    for i in range(n_runs):
+        dt, stages, desc = cpu_sample(args.workload, args.rho, args.sigma, frac, *iters)
         if i >= args.warmup:
             times.append(dt)
-    layer_s = (sum(times) / len(times)) * shrink * shrink * H
+    layer_s = (sum(times) / len(times)) * H
     value = dense_flops(H, S, d) / layer_s / 1e12
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -176,8 +278,9 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": args.workload, "heads": H, "seq_len": S, "head_dim": d, "c_q": cq,
-                   "c_k": ck, "rho": args.rho},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc},
+                   "c_k": ck, "rho": args.rho, "inputs": args.inputs},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc,
+                         "stage_seconds_per_head": stages},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -210,112 +313,20 @@ def run_ours(args):
     hl = hi - lo
     lib = P.load_library()
     pk = peaks()
+    out_dtype = torch.float32 if args.fp32_check else torch.bfloat16
+    iters_for = lambda kind: min(args.kmeans_iters, args.kmeans_iters_iid) if kind == "iid" else args.kmeans_iters
 
-    q, k, v = make_heads(torch, lo, hi, S, d, cq, ck, args.sigma, dev)
-    shape = _lib.Shape(max(hl, 1), S, S, d, cq, ck)
+    q, k, v = make_heads(torch, lo, hi, S, d, cq, ck, args.sigma, dev, args.inputs)
     ws = torch.empty(P.operator_workspace_bytes(max(hl, 1), S, S, d, cq, ck, args.head_groups), dtype=torch.uint8,
                      device=dev)
-    kw = dict(init=args.init, kmeans_iters=args.kmeans_iters, check_fp32=args.fp32_check,
-              workspace_buffer=ws, head_groups=args.head_groups)
 
-    def layer(qq, kk, vv, aux=False):
-        if hl == 0:
-            return None
-        return P.svg_ear_attention(qq, kk, vv, cq, ck, args.rho, return_aux=aux, **kw)
-
-    def step_resident():
-        res = layer(q, k, v)
-        if world > 1:
-            return gather_heads(res[0], H), gather_heads(res[1], H)
-        return res
-
-    # pinned host staging for the e2e leg
-    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
-    out_dtype = torch.float32 if args.fp32_check else torch.bfloat16
-    ho = torch.empty((1, H if world > 1 else hl, S, d), dtype=out_dtype).pin_memory()
-    hm = torch.empty((1, H if world > 1 else hl, cq, ck), dtype=torch.bool).pin_memory()
-    dq, dk, dv = (torch.empty_like(t) for t in (q, k, v))
-
-    # The e2e leg streams the layer through the public operator in head groups: while group g is
-    # computed, the host->device copy of group g+1 and the device->host copy of group g-1 run on a
-    # copy stream (heads are independent instances, so the grouping does not change any result of
-    # a head except the device-side seeding draw, which is keyed by the instance index).
-    n_groups = 5 if (hl >= 16 and world == 1) else (4 if (hl >= 8 and world == 1) else 1)
-    if n_groups == 1:
-        bounds = [0, hl]
-    elif n_groups == 4:
-        # a small first group lets compute start early; the rest is split evenly (big groups run the
-        # latency-bound stages more efficiently)
-        first = max(1, hl // 10)
-        rest = hl - first
-        bounds = [0] + [first + rest * g // (n_groups - 1) for g in range(n_groups)]
-    else:
-        # every group computes on its own stream as soon as its inputs have landed, so the groups'
-        # latency-bound stages overlap; a small first group starts compute early and a small last
-        # group keeps the tail after the final host->device copy short
-        edge = max(1, hl // 10)
-        mid = hl - 2 * edge
-        bounds = [0] + [edge + mid * g // (n_groups - 2) for g in range(n_groups - 1)] + [hl]
-    copy_stream = torch.cuda.Stream(device=dev)   # host -> device
-    back_stream = torch.cuda.Stream(device=dev)   # device -> host (PCIe is full duplex)
-    gmax = max(bounds[g + 1] - bounds[g] for g in range(n_groups))
-    ws_g = [ws] if n_groups == 1 else [torch.empty(
-        P.operator_workspace_bytes(max(gmax, 1), S, S, d, cq, ck, args.head_groups), dtype=torch.uint8, device=dev)
-        for _ in range(n_groups)]
-    group_streams = [torch.cuda.Stream(device=dev) for _ in range(n_groups)]
-    do = torch.empty((1, hl, S, d), dtype=out_dtype, device=dev)
-    dm = torch.empty((1, hl, cq, ck), dtype=torch.bool, device=dev)
-
-    def group_compute(g):
-        """The public operator on head group g of the device staging buffers -> do/dm slices."""
-        a, b = bounds[g], bounds[g + 1]
-        o, m = P.svg_ear_attention(dq[:, a:b], dk[:, a:b], dv[:, a:b], cq, ck, args.rho, seed=a,
-                                   init=args.init, kmeans_iters=args.kmeans_iters,
-                                   check_fp32=args.fp32_check, workspace_buffer=ws_g[g],
-                                   head_groups=args.head_groups)
-        do[:, a:b].copy_(o); dm[:, a:b].copy_(m)
-
-    # per-group CUDA graphs of the operator call (filled in after the warm-up below): a group's ~3000
-    # eager launches cost more host time than its kernels take, so the e2e leg was host bound
-    group_graphs = [None] * n_groups
-
-    def step_e2e():
-        if n_groups == 1:
-            dq.copy_(hq, non_blocking=True); dk.copy_(hk, non_blocking=True); dv.copy_(hv, non_blocking=True)
-            o, m = layer(dq, dk, dv)
-            if world > 1:
-                o, m = gather_heads(o, H), gather_heads(m, H)
-            ho.copy_(o, non_blocking=True); hm.copy_(m, non_blocking=True)
-            return
-        cur = torch.cuda.current_stream(dev)
-        copy_stream.wait_stream(cur)
-        h2d, done = [], []
-        with torch.cuda.stream(copy_stream):
-            for g in range(n_groups):
-                a, b = bounds[g], bounds[g + 1]
-                dq[:, a:b].copy_(hq[:, a:b], non_blocking=True)
-                dk[:, a:b].copy_(hk[:, a:b], non_blocking=True)
-                dv[:, a:b].copy_(hv[:, a:b], non_blocking=True)
-                ev = torch.cuda.Event(); ev.record(copy_stream); h2d.append(ev)
-        for g in range(n_groups):
-            a, b = bounds[g], bounds[g + 1]
-            gs = group_streams[g]
-            gs.wait_stream(cur)
-            gs.wait_event(h2d[g])
-            with torch.cuda.stream(gs):
-                if group_graphs[g] is not None:
-                    group_graphs[g].replay()
-                else:
-                    group_compute(g)
-                ev = torch.cuda.Event(); ev.record(gs); done.append(ev)
-            with torch.cuda.stream(back_stream):
-                back_stream.wait_event(ev)
-                ho[:, a:b].copy_(do[:, a:b], non_blocking=True)
-                hm[:, a:b].copy_(dm[:, a:b], non_blocking=True)
-        for gs in group_streams:
-            cur.wait_stream(gs)
-        cur.wait_stream(back_stream)
-        cur.wait_stream(copy_stream)
+    def op(qq, kk, vv, kind, first_head, workspace, aux=False):
+        """The public operator on heads [first_head, first_head + n) of the layer: every instance is
+        seeded by its global head index, so any split of the heads returns the unsplit result."""
+        return P.svg_ear_attention(qq, kk, vv, cq, ck, args.rho, return_aux=aux, init=args.init,
+                                   kmeans_iters=iters_for(kind), check_fp32=args.fp32_check,
+                                   workspace_buffer=workspace, head_groups=args.head_groups,
+                                   head_offset=first_head, total_heads=H)
 
     def timed(fn, steps):
         if world > 1:
@@ -334,44 +345,154 @@ def run_ours(args):
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms) / steps
 
-    for _ in range(max(args.warmup, 3)):
-        step_resident()
-    # The resident-input step is the same ~600 launches every time (two k-means sides forked onto a
-    # helper stream, two attention kernels): capture it once in a CUDA graph and replay it — same
-    # kernels, same buffers, no per-launch host latency.  Falls back to eager launches if capture is
-    # not possible (N > 1 keeps the NCCL gather eager).
-    graph, launches_per_step = None, None
-    if world == 1 and hl > 0 and not args.no_graph:
+    # ---- resident-input step ----------------------------------------------------------------------
+    # The per-rank compute (~1200 launches: two k-means sides forked onto a helper stream, two
+    # attention kernels) is captured once in a CUDA graph and replayed — same kernels, same buffers,
+    # no per-launch host latency — at every N.  With N > 1 the replay is followed by ONE
+    # all_gather_into_tensor per output straight into the final [1, H, S, d] / [1, H, C_q, C_k]
+    # buffers (rank r's heads are range r of them) on a communication stream.
+    full_o = torch.empty((1, H, S, d), dtype=out_dtype, device=dev) if world > 1 else None
+    full_m = torch.empty((1, H, cq, ck), dtype=torch.bool, device=dev) if world > 1 else None
+    comm_stream = torch.cuda.Stream(device=dev) if world > 1 else None
+    state = {"graph": None, "out": None, "kind": args.inputs}
+
+    def compute_local():
+        if hl == 0:
+            return None
+        return op(q, k, v, state["kind"], lo, ws)
+
+    def step_resident():
+        res = state["out"]
+        if state["graph"] is not None:
+            state["graph"].replay()
+        else:
+            res = compute_local()
+        if world == 1:
+            return res
+        cur = torch.cuda.current_stream(dev)
+        comm_stream.wait_stream(cur)
+        with torch.cuda.stream(comm_stream):
+            o = res[0] if res is not None else full_o[:, :0]
+            m = res[1] if res is not None else full_m[:, :0]
+            gather_heads(o, H, out=full_o)
+            gather_heads(m, H, out=full_m)
+        cur.wait_stream(comm_stream)
+        return full_o, full_m
+
+    def capture(kind):
+        """(Re)capture the per-rank compute for the current contents of q, k, v; checked bit-identical
+        against the eager call.  Returns launches per replay (None when running eagerly)."""
+        state.update(graph=None, out=None, kind=kind)
+        for _ in range(max(args.warmup, 3)):
+            step_resident()
+        if hl == 0 or args.no_graph:
+            return None
         try:
             torch.cuda.synchronize()
             l0 = lib.svgear_launch_count()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                graph_out = step_resident()
-            launches_per_step = lib.svgear_launch_count() - l0
+                graph_out = compute_local()
+            n_launch = lib.svgear_launch_count() - l0
             torch.cuda.synchronize()
-            eager_out = step_resident()
+            eager_out = compute_local()
             g.replay()
             torch.cuda.synchronize()
             if not (torch.equal(graph_out[0], eager_out[0]) and torch.equal(graph_out[1], eager_out[1])):
                 raise RuntimeError("graph replay differs from the eager result")
-            graph = g
+            state.update(graph=g, out=graph_out)
+            return n_launch
         except Exception as exc:  # noqa: BLE001
             print(f"[bench] CUDA graph capture unavailable, launching eagerly: {exc}", file=sys.stderr)
-            graph = None
+            state.update(graph=None, out=None)
             torch.cuda.synchronize()
-    run_step = graph.replay if graph is not None else step_resident
+            return None
+
+    launches_per_step = capture(args.inputs)
     for _ in range(2):
-        run_step()
+        step_resident()
     sampler = ClockSampler(local)
     sampler.start()
     l0 = lib.svgear_launch_count()
-    ms_step = timed(run_step, args.steps)
-    launches = (lib.svgear_launch_count() - l0) if graph is None else launches_per_step * args.steps
+    ms_step = timed(step_resident, args.steps)
+    launches = (lib.svgear_launch_count() - l0) if state["graph"] is None else launches_per_step * args.steps
     clocks = sampler.stop()
+
+    # ---- e2e leg: pinned host buffers, H2D and D2H inside the timed region ---------------------------
+    # The layer streams through the public operator in head groups: while group g is computed, the
+    # host->device copy of group g+1 and the device->host copy of group g-1 run on copy streams
+    # (heads are independent instances seeded by their global index, so the grouping changes nothing).
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    ho = torch.empty((1, H if world > 1 else hl, S, d), dtype=out_dtype).pin_memory()
+    hm = torch.empty((1, H if world > 1 else hl, cq, ck), dtype=torch.bool).pin_memory()
+    dq, dk, dv = (torch.empty_like(t) for t in (q, k, v))
+    n_groups = 5 if hl >= 16 else (4 if hl >= 8 else (2 if hl >= 4 else 1))
+    if n_groups <= 2:
+        bounds = [hl * g // n_groups for g in range(n_groups + 1)]
+    elif n_groups == 4:
+        first = max(1, hl // 10)  # a small first group lets compute start early
+        rest = hl - first
+        bounds = [0] + [first + rest * g // (n_groups - 1) for g in range(n_groups)]
+    else:
+        edge = max(1, hl // 10)   # small first and last groups: early start, short tail after the last copy
+        mid = hl - 2 * edge
+        bounds = [0] + [edge + mid * g // (n_groups - 2) for g in range(n_groups - 1)] + [hl]
+    copy_stream = torch.cuda.Stream(device=dev)   # host -> device
+    back_stream = torch.cuda.Stream(device=dev)   # device -> host (PCIe is full duplex)
+    gmax = max(bounds[g + 1] - bounds[g] for g in range(n_groups))
+    ws_g = [ws] if n_groups == 1 else [torch.empty(
+        P.operator_workspace_bytes(max(gmax, 1), S, S, d, cq, ck, args.head_groups), dtype=torch.uint8, device=dev)
+        for _ in range(n_groups)]
+    group_streams = [torch.cuda.Stream(device=dev) for _ in range(n_groups)]
+    do = torch.empty((1, hl, S, d), dtype=out_dtype, device=dev)
+    dm = torch.empty((1, hl, cq, ck), dtype=torch.bool, device=dev)
+    group_graphs = [None] * n_groups
+
+    def group_compute(g):
+        a, b = bounds[g], bounds[g + 1]
+        if b > a:
+            o, m = op(dq[:, a:b], dk[:, a:b], dv[:, a:b], args.inputs, lo + a, ws_g[g])
+            do[:, a:b].copy_(o); dm[:, a:b].copy_(m)
+
+    def step_e2e():
+        cur = torch.cuda.current_stream(dev)
+        copy_stream.wait_stream(cur)
+        h2d = []
+        with torch.cuda.stream(copy_stream):
+            for g in range(n_groups):
+                a, b = bounds[g], bounds[g + 1]
+                dq[:, a:b].copy_(hq[:, a:b], non_blocking=True)
+                dk[:, a:b].copy_(hk[:, a:b], non_blocking=True)
+                dv[:, a:b].copy_(hv[:, a:b], non_blocking=True)
+                ev = torch.cuda.Event(); ev.record(copy_stream); h2d.append(ev)
+        for g in range(n_groups):
+            a, b = bounds[g], bounds[g + 1]
+            gs = group_streams[g]
+            gs.wait_stream(cur)
+            gs.wait_event(h2d[g])
+            with torch.cuda.stream(gs):
+                if group_graphs[g] is not None:
+                    group_graphs[g].replay()
+                else:
+                    group_compute(g)
+                ev = torch.cuda.Event(); ev.record(gs)
+            if world == 1:
+                with torch.cuda.stream(back_stream):
+                    back_stream.wait_event(ev)
+                    ho[:, a:b].copy_(do[:, a:b], non_blocking=True)
+                    hm[:, a:b].copy_(dm[:, a:b], non_blocking=True)
+        for gs in group_streams:
+            cur.wait_stream(gs)
+        if world > 1:  # gather the rank slabs into the final buffers, then one device->host read
+            gather_heads(do, H, out=full_o)
+            gather_heads(dm, H, out=full_m)
+            ho.copy_(full_o, non_blocking=True); hm.copy_(full_m, non_blocking=True)
+        cur.wait_stream(back_stream)
+        cur.wait_stream(copy_stream)
+
     step_e2e()
     e2e_graphs = False
-    if graph is not None and n_groups > 1:
+    if state["graph"] is not None:
         try:
             torch.cuda.synchronize()
             eager_o, eager_m = do.clone(), dm.clone()
@@ -392,27 +513,14 @@ def run_ours(args):
             group_graphs[:] = [None] * n_groups
             torch.cuda.synchronize()
     ms_e2e = timed(step_e2e, args.steps)
-
-    # ---- stage timings (CUDA events on the launching stream) for the roofline -------------------
-    stages, roof, density, iters = {}, None, None, None
-    if hl > 0:
-        stages, attend_flops, density, iters = stage_times(torch, P, _lib, q, k, v, cq, ck, args, 3)
-        t_att = stages["attend"] * 1e-3
-        achieved = attend_flops / t_att / 1e12
-        # the attend kernel is timed alone between events -> burst peak
-        # DRAM bytes of the attention launch from the committed ncu --set full capture
-        # (profiles/r01b_ncu_full_summary.txt, 8 Wan2.2 heads: two-half kernel 521.4 MB read + 140.7 MB
-        # written, remainder-tile kernel 399.1 MB read + 5.6 MB written (cold L2 under ncu));
-        # reported only for the workload and executor that capture was taken on
-        traffic = None
-        if args.workload == "wan2.2-720p" and not args.fp32_check and abs(args.rho - 0.25) < 1e-9:
-            traffic = (521.449728e6 + 140.697600e6 + 399.122432e6 + 5.622528e6) / 8.0 * hl
-        roof = {"bound": "tensor", "achieved": achieved, "peak": pk["tf_burst"], "unit": "TFLOP/s",
-                "frac": achieved / pk["tf_burst"], "traffic": traffic,
-                "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum, 8-head capture scaled by heads"
-                                  if traffic else None,
-                "kernel": "attend_fp32_kernel" if args.fp32_check else "attend_tc_kernel",
-                "algorithmic_flops_per_launch": attend_flops, "peak_source": pk["source"] + " (burst)"}
+    # the e2e result equals the resident result (same operator, same global head seeds)
+    e2e_equal = None
+    if hl > 0 and world == 1:
+        ref_out = state["out"] if state["graph"] is not None else compute_local()
+        torch.cuda.synchronize()
+        e2e_equal = bool(torch.equal(do, ref_out[0].view_as(do)) and torch.equal(dm, ref_out[1].view_as(dm)))
+    group_graphs[:] = [None] * n_groups
+    del ws_g, dq, dk, dv, do, dm
 
     # ---- dense bf16 attention on the same device (context; library kernel) -----------------------
     dense_ms = None
@@ -425,13 +533,55 @@ def run_ours(args):
         except Exception as exc:  # noqa: BLE001
             dense_ms = f"unavailable: {exc}"[:120]
 
+    # ---- stage timings + rooflines for the headline input, then the other input kinds ---------------
+    def analyse(kind):
+        stages, attend_flops, density, iters = stage_times(torch, P, _lib, q, k, v, cq, ck, args, iters_for(kind), 3)
+        achieved = attend_flops / (stages["attend"] * 1e-3) / 1e12
+        traffic, traffic_src = (None, None) if args.fp32_check or abs(args.rho - 0.25) > 1e-9 else \
+            committed_traffic(args.workload, kind, hl)
+        roof = {"bound": "tensor", "achieved": achieved, "peak": pk["tf_burst"], "unit": "TFLOP/s",
+                "frac": achieved / pk["tf_burst"], "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": "attend_fp32_kernel" if args.fp32_check else "attend_tc_kernel",
+                "algorithmic_flops_per_launch": attend_flops, "peak_source": pk["source"] + " (burst: timed alone)"}
+        # bandwidth-bound stages against the measured HBM peak; algorithmic bytes per SURVEY 8d
+        per_iter = 2 * S * d * 2 + S * 4                       # tokens read twice + assignments written, per side
+        hbm = {"kmeans_q": per_iter * iters["q_sum"], "kmeans_k": per_iter * iters["k_sum"],
+               "permute": hl * 3 * 2 * S * d * 2, "error_table": hl * (2 * S * d * 2 + 4 * cq * ck)}
+        sroof = {n: {"bytes": b, "achieved_gbs": b / (stages[n] * 1e-3) / 1e9, "peak_gbs": pk["hbm"],
+                     "frac": b / (stages[n] * 1e-3) / 1e9 / pk["hbm"]} for n, b in hbm.items()}
+        return stages, roof, sroof, density, iters
+
+    stages, roof, sroof, density, iters = ({}, None, None, None, None)
+    if hl > 0:
+        stages, roof, sroof, density, iters = analyse(args.inputs)
+    sweep = {}
+    if world == 1 and hl > 0 and not args.no_sweep:
+        for kind in INPUT_KINDS:
+            if kind == args.inputs:
+                continue
+            nq, nk, nv = make_heads(torch, lo, hi, S, d, cq, ck, args.sigma, dev, kind)
+            q.copy_(nq); k.copy_(nk); v.copy_(nv)
+            del nq, nk, nv
+            n_l = capture(kind)
+            ms_kind = timed(step_resident, max(3, min(args.steps, 5)))
+            st_k, roof_k, sroof_k, dens_k, it_k = analyse(kind)
+            sweep[kind] = {
+                "inputs": INPUT_DESC[kind].format(sigma=args.sigma), "ms_per_step": ms_kind,
+                "value": dense_flops(H, S, d) / (ms_kind * 1e-3) / 1e12,
+                "speedup_vs_dense_sdpa": (dense_ms / ms_kind) if isinstance(dense_ms, float) else None,
+                "kmeans_max_iters": iters_for(kind), "kmeans_iters_run": it_k, "density_achieved": dens_k,
+                "cuda_graph": state["graph"] is not None, "gpu_launches_per_step": n_l,
+                "roofline": roof_k, "stages_ms": st_k, "stages_roofline": sroof_k}
+        state.update(graph=None, out=None)
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        shrink = 3 if S > 20000 else 1
-        dt, desc = cpu_sample(args.workload, args.rho, args.sigma, shrink)
-        layer_s = dt * shrink * shrink * H
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and S > 20000:
+        it = iters or {"q_max": 20, "k_max": 9}
+        per_head, cpu_stages, desc = cpu_sample(args.workload, args.rho, args.sigma, 0.08, it["q_max"], it["k_max"])
+        layer_s = per_head * H
         cpu = {"value": dense_flops(H, S, d) / layer_s / 1e12, "unit": UNIT, "cores": os.cpu_count(),
-               "kind": "port", "sample": desc, "ms_per_layer_extrapolated": layer_s * 1e3}
+               "kind": "port", "sample": desc, "ms_per_layer_extrapolated": layer_s * 1e3,
+               "stage_seconds_per_head": cpu_stages}
 
     if rank == 0:
         fl = dense_flops(H, S, d)
@@ -443,15 +593,18 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32" if args.fp32_check else "bf16", "data": "synthetic",
             "config": {"workload": args.workload, "heads": H, "seq_len": S, "head_dim": d, "c_q": cq,
-                       "c_k": ck, "rho": args.rho, "kmeans_max_iters": args.kmeans_iters,
-                       "kmeans_iters_run": iters, "kmeans_init": {"device": "k-means++ on a strided 8x subsample, on device (inside svgear_forward_seeded)",
+                       "c_k": ck, "rho": args.rho, "kmeans_max_iters": iters_for(args.inputs),
+                       "kmeans_iters_run": iters,
+                       "kmeans_init": {"device": "k-means++ on a strided 8x subsample, on device (inside svgear_forward_seeded)",
                                        "strided": "strided tokens"}[args.init],
-                       "inputs": f"per-head blob mixture sigma={args.sigma}, generated on device",
+                       "inputs": INPUT_DESC[args.inputs].format(sigma=args.sigma) + ", generated on device",
+                       "inputs_sweep": sweep or None,
                        "executor": "fp32-check" if args.fp32_check else "bf16-tcgen05",
                        "density_achieved": density, "parallelism": f"head-parallel x{world}",
                        "l2": "inputs (%.0f MB/rank) exceed the 126 MB L2; no explicit flush" % (in_bytes / 1e6),
                        "e2e_pipeline": f"{n_groups} head groups, each computed on its own stream as soon as its inputs land (H2D and D2H on their own streams)",
-                       "cuda_graph": graph is not None, "e2e_cuda_graphs": e2e_graphs,
+                       "e2e_equals_resident": e2e_equal,
+                       "cuda_graph": launches_per_step is not None, "e2e_cuda_graphs": e2e_graphs,
                        "head_groups": ("operator default (2 concurrent head groups at >= 16 heads)"
                                        if args.head_groups is None else args.head_groups)},
             "clocks": clocks,
@@ -459,6 +612,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": out_bytes},
             "gpu_launches": int(launches),
             "roofline": roof,
+            "stages_roofline": sroof,
             "cpu_baseline": cpu,
             "stages_ms": stages,
             "dense_bf16_sdpa_ms": dense_ms,
@@ -469,14 +623,13 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def stage_times(torch, P, _lib, q, k, v, cq, ck, args, reps):
+def stage_times(torch, P, _lib, q, k, v, cq, ck, args, kmeans_iters, reps):
     """Run the layer through the STAGED C-ABI entry points (same kernels as svgear_forward) with
     CUDA events between stages.  Returns ({stage: ms}, attention algorithmic FLOPs, density, iters)."""
     from paper_2603_08982_b200.clustering import ClusterModel, device_start_pair, run_lloyd, strided_start
     from paper_2603_08982_b200 import router as R
 
     qb, kb, vb = q[0], k[0], v[0]
-    bh, S, d = qb.shape
     acc = {}
     ev = lambda: torch.cuda.Event(enable_timing=True)
     flops = density = iters = None
@@ -490,13 +643,13 @@ def stage_times(torch, P, _lib, q, k, v, cq, ck, args, reps):
         else:
             qi, ki = strided_start(qb, cq), strided_start(kb, ck)
         mark("kmeans_seed")
-        rq = run_lloyd(qb, qi, args.kmeans_iters); mark("kmeans_q")
-        rk = run_lloyd(kb, ki, args.kmeans_iters); mark("kmeans_k")
+        rq = run_lloyd(qb, qi, kmeans_iters, want_inertia=False); mark("kmeans_q")
+        rk = run_lloyd(kb, ki, kmeans_iters, want_inertia=False); mark("kmeans_k")
         qm = ClusterModel(cq, rq["assign"], rq["centroids"], rq["sizes"], rq["perm"], rq["offsets"])
         km = ClusterModel(ck, rk["assign"], rk["centroids"], rk["sizes"], rk["perm"], rk["offsets"])
         qp, kp, vp = P.permute_rows(qb, qm), P.permute_rows(kb, km), P.permute_rows(vb, km); mark("permute")
         vc = P.segment_means(vp, km); mark("segment_means")
-        table = P.estimate_errors_streaming(qm, km, kp, vp); mark("error_table")
+        table = P.estimate_errors_streaming(qm, km, kp, vp, v_centroids=vc); mark("error_table")
         mask = R.route_error_aware(table, R.DensityBudget.global_density(args.rho)); mark("route")
         # keep the GPU busy for ~2 ms while the host enqueues the executor (tile list, tensor maps,
         # launches), so that the event pair below brackets device time only, not host latency
@@ -511,8 +664,8 @@ def stage_times(torch, P, _lib, q, k, v, cq, ck, args, reps):
                 acc.setdefault(name, []).append(a.elapsed_time(b))
         flops = float(res.flops.exact_block + res.flops.compensation)
         density = float(mask.density.double().mean())
-        iters = {"q_max": int(rq["iters"].max()), "k_max": int(rk["iters"].max())}
-    # error_table stage above includes a redundant segment_means inside the mirror call; report as is.
+        iters = {"q_max": int(rq["iters"].max()), "k_max": int(rk["iters"].max()),
+                 "q_sum": int(rq["iters"].sum()), "k_sum": int(rk["iters"].sum())}
     # Median over the repetitions: the mirror calls allocate their workspaces, and one cudaMalloc in
     # one repetition (a host stall between two events) would otherwise dominate a stage's mean.
     med = lambda xs: sorted(xs)[len(xs) // 2] if len(xs) % 2 else 0.5 * (sorted(xs)[len(xs) // 2 - 1] + sorted(xs)[len(xs) // 2])

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SVGEAR_VERSION 100 /* 0.1.0 */
+#define SVGEAR_VERSION 110 /* 0.1.1: seeding computes its own Gram matrix; fused Lloyd step */
 
 enum {
   SVGEAR_OK = 0,
@@ -124,18 +124,16 @@ int svgear_kmeans(int32_t exec_mode, int32_t bh, int32_t n, int32_t d, int32_t c
 
 /* Device-side start centres for svgear_kmeans when the caller has none: k-means++ D^2 sampling
  * (the reference's seeding rule, clustering.py:65-84) over a strided subsample of
- * min(n, oversample*c) tokens with a counter-based hash RNG keyed by (seed, instance).  This is
- * NOT the reference's numpy draw (the Python shim reproduces that one on the host for parity);
- * it is deterministic and costs O(c * oversample * c * d) per instance.
- *   centroids [bh][c][d] f32 (out)                                                              */
+ * m = min(n, oversample*c, 4096) tokens (sample i = token floor(i*n/m)) with a counter-based hash RNG
+ * keyed by (seed, first_instance + b).  This is NOT the reference's numpy draw (the Python shim
+ * reproduces that one on the host for parity runs); it is deterministic.  Two kernels: the Gram
+ * matrix of the subsample on the tensor cores (tcgen05), then the sequential D^2 rounds, which
+ * read only the Gram rows of the centres drawn so far.
+ *   centroids [bh][c][d] f32 (out); workspace: >= bh*m*m*2 bytes (svgear_workspace_bytes covers
+ *   oversample <= 8)                                                                             */
 int svgear_kmeans_seed(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
-                       int32_t oversample, uint32_t seed, float* centroids, void* stream);
-
-/* Same seeding rule, driven by a precomputed Gram matrix of the strided subsample
- * (sample s = token floor(s*n/m); gram[b][s][t] = <x_s, x_t> in bf16, e.g. one batched library
- * GEMM): a round then reads only the Gram rows of its new centres.  m <= 4096.              */
-int svgear_kmeans_seed_gram(int32_t bh, int32_t n, int32_t d, int32_t c, int32_t m, const void* x,
-                            const void* gram, uint32_t seed, float* centroids, void* stream);
+                       int32_t oversample, uint32_t seed, int32_t first_instance, float* centroids,
+                       void* workspace, size_t workspace_bytes, void* stream);
 
 /* out[b][i][:] = x[b][perm[b][i]][:]   — clustering.permute_rows (clustering.py:210-212). */
 int svgear_permute_rows(int32_t bh, int32_t n, int32_t d, const void* x, const int32_t* perm,
@@ -221,24 +219,21 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
                    void* stream);
 
 /* svgear_forward with the device-side k-means++ seeding folded in: equivalent to
- * svgear_kmeans_seed_gram(q side, seed) + svgear_kmeans_seed_gram(k side, seed + 0x9E37) followed by
- * svgear_forward, but each side's seeding kernel runs on the stream of that side's Lloyd loop, so
- * the query side does not wait for the (longer) key-side seeding.  NOT the reference's numpy draw:
- * for parity runs hand svgear_forward the reference's start centres.
- *   q_gram [bh][m_q][m_q], k_gram [bh][m_k][m_k] bf16: Gram matrices of the strided subsamples
- *   (token i*n/m, i < m), as for svgear_kmeans_seed_gram; c <= m <= min(n, 4096)
+ * svgear_kmeans_seed(q side, seed) + svgear_kmeans_seed(k side, seed + 0x9E37) followed by
+ * svgear_forward, but each side's seeding runs on the stream of that side's Lloyd loop, so the
+ * query side does not wait for the (longer) key-side seeding.  NOT the reference's numpy draw: for
+ * parity runs hand svgear_forward the reference's start centres.
+ *   oversample: subsample size per centre, 1..8 (8 is what the operator uses)
  *   first_instance: instance b of this call draws as instance first_instance + b of the whole batch,
- *   so a caller that splits a batch into groups (one call per group, e.g. on concurrent streams)
- *   gets the centres of the unsplit call
+ *   so a caller that splits a batch into groups (one call per group, e.g. on concurrent streams, or
+ *   head ranges on different GPUs) gets the centres of the unsplit call
  *   q_init [bh][c_q][d], k_init [bh][c_k][d] f32: OUT, the start centres that were drawn          */
 int svgear_forward_seeded(const SvgEarShape* shape, const void* q, const void* k, const void* v,
-                          const void* q_gram, const void* k_gram, int32_t m_q, int32_t m_k,
-                          uint32_t seed, int32_t first_instance, float* q_init, float* k_init,
-                          int32_t kmeans_iters,
-                          int32_t estimator_mode, int64_t capacity_entries, int32_t overshoot,
-                          int32_t single_item_fallback, int32_t exec_mode, double top_p, void* out,
-                          uint8_t* mask, const SvgEarAux* aux, void* workspace,
-                          size_t workspace_bytes, void* stream);
+                          int32_t oversample, uint32_t seed, int32_t first_instance, float* q_init,
+                          float* k_init, int32_t kmeans_iters, int32_t estimator_mode,
+                          int64_t capacity_entries, int32_t overshoot, int32_t single_item_fallback,
+                          int32_t exec_mode, double top_p, void* out, uint8_t* mask,
+                          const SvgEarAux* aux, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- the callers either side of the operator in a DiT attention block ----
  * The reference stops at single (Q,K,V) matrices; the paper's deployment feeds

@@ -15,7 +15,7 @@ import threading
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_PATH = os.path.join(PKG_DIR, "libsvgear.so")
-SOURCES = ("api.cu", "kmeans.cu", "kmeans_tc.cu", "stats_route.cu", "errtab_tc.cu", "attend_ref.cu", "attend_tc.cu", "dit.cu")
+SOURCES = ("api.cu", "kmeans.cu", "lloyd_step.cu", "kmeans_tc.cu", "seed.cu", "stats_route.cu", "errtab_tc.cu", "attend_ref.cu", "attend_tc.cu", "dit.cu")
 NVCC_FLAGS = (
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-shared", "-Xcompiler", "-fPIC",
@@ -57,8 +57,7 @@ SIGNATURES = {
     "svgear_launch_count": ([], C.c_int64),
     "svgear_workspace_bytes": ([C.POINTER(Shape), C.POINTER(_SZ)], C.c_int),
     "svgear_kmeans": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
-    "svgear_kmeans_seed": ([_I32, _I32, _I32, _I32, _P, _I32, C.c_uint32, _P, _P], C.c_int),
-    "svgear_kmeans_seed_gram": ([_I32, _I32, _I32, _I32, _I32, _P, _P, C.c_uint32, _P, _P], C.c_int),
+    "svgear_kmeans_seed": ([_I32, _I32, _I32, _I32, _P, _I32, C.c_uint32, _I32, _P, _P, _SZ, _P], C.c_int),
     "svgear_permute_rows": ([_I32, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "svgear_segment_means": ([_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P], C.c_int),
     "svgear_error_table": ([C.POINTER(Shape), _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
@@ -66,7 +65,7 @@ SIGNATURES = {
     "svgear_route_score": ([C.POINTER(Shape), _P, _P, _P, _P, _I64, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_route_error_aware_top_p": ([C.POINTER(Shape), _P, _P, _P, _P, _P, C.c_double, _I32, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_sparse_attend": ([C.POINTER(Shape), _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
-    "svgear_forward_seeded": ([C.POINTER(Shape), _P, _P, _P, _P, _P, _I32, _I32, C.c_uint32, _I32, _P, _P, _I32, _I32, _I64, _I32, _I32, _I32, C.c_double, _P, _P, C.POINTER(Aux), _P, _SZ, _P], C.c_int),
+    "svgear_forward_seeded": ([C.POINTER(Shape), _P, _P, _P, _I32, C.c_uint32, _I32, _P, _P, _I32, _I32, _I64, _I32, _I32, _I32, C.c_double, _P, _P, C.POINTER(Aux), _P, _SZ, _P], C.c_int),
     "svgear_qkv_prologue": ([_I32, _I32, _I32, _I32, _P, _I32, _P, _P, C.c_float, _I32, _I32, _P, _P, _P, _P, _P, _P], C.c_int),
     "svgear_heads_to_tokens": ([_I32, _I32, _I32, _I32, _P, _P, _P], C.c_int),
     "svgear_forward": ([C.POINTER(Shape), _P, _P, _P, _P, _P, _I32, _I32, _I64, _I32, _I32, _I32, C.c_double, _P, _P, C.POINTER(Aux), _P, _SZ, _P], C.c_int),
@@ -86,17 +85,42 @@ def _stale():
 
 
 def build_library(force=False, verbose=False):
-    """Compile csrc/*.cu into libsvgear.so for sm_100a (nvcc cross-compiles without a GPU)."""
+    """Compile csrc/*.cu into libsvgear.so for sm_100a (nvcc cross-compiles without a GPU).  Each
+    source becomes an object under build/ (recompiled only when it or a header changed, in
+    parallel), then one link step."""
     if not force and not _stale():
         return LIB_PATH
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *[os.path.join(CSRC, s) for s in SOURCES]]
+    from concurrent.futures import ThreadPoolExecutor
+
+    obj_dir = os.path.join(PKG_DIR, "build")
+    os.makedirs(obj_dir, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + [
+        os.path.join(os.path.dirname(PKG_DIR), "include", "svgear.h")]
+    newest_header = max(os.path.getmtime(h) for h in headers)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(obj_dir, src[:-3] + ".o")
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(path), newest_header):
+            return obj, ""
+        cmd = ["nvcc", *compile_flags, "-c", "-o", obj, path]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n" + res.stdout + res.stderr)
+        return obj, res.stderr
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as pool:
+        results = list(pool.map(compile_one, SOURCES))
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    res = subprocess.run(cmd, capture_output=True, text=True)
+        print("".join(err for _, err in results))
+    link = ["nvcc", "-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB_PATH,
+            *[obj for obj, _ in results], "-lcuda"]
+    res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
-    if verbose:
-        print(res.stderr)
+        raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
     return LIB_PATH
 
 

@@ -55,10 +55,12 @@ def prepare(q_raw, k_raw, v_raw, c_q: int, c_k: int, *, seed: int = 0, restarts:
         raise ValueError(f"key/value row counts differ: {k.shape[1]} vs {v.shape[1]}")
     if q2:
         q, k, v = q[0], k[0], v[0]
-    q_seed, k_seed = side_seeds(seed)
-    q_model = kmeans(q, c_q, seed=q_seed, restarts=restarts, init_centroids=q_init_centroids,
+    # instance b of a batch is seeded like the operator seeds it: side_seeds(seed + b)
+    bh = 1 if q2 else q.shape[0]
+    seeds = [side_seeds(seed + b) for b in range(bh)]
+    q_model = kmeans(q, c_q, seed=[s_[0] for s_ in seeds], restarts=restarts, init_centroids=q_init_centroids,
                      max_iters=max_iters)
-    k_model = kmeans(k, c_k, seed=k_seed, restarts=restarts, init_centroids=k_init_centroids,
+    k_model = kmeans(k, c_k, seed=[s_[1] for s_ in seeds], restarts=restarts, init_centroids=k_init_centroids,
                      max_iters=max_iters)
     return Prepared(q_raw=q, k_raw=k, v_raw=v, q_model=q_model, k_model=k_model,
                     q=permute_rows(q, q_model), k=permute_rows(k, k_model), v=permute_rows(v, k_model))

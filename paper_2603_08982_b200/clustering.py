@@ -2,9 +2,10 @@
 
 Same names and argument meaning as the reference (clustering.py:144-257); arrays are torch CUDA
 tensors.  `kmeans` accepts one instance [n, d] (as the reference) or a batch [bh, n, d].
-The k-means++ seeding is host-side numpy with the reference's RNG call sequence
-(clustering.py:65-84, 178-180) so a given `seed` starts from the identical centres; Lloyd
-iterations, repair, permutation and means run in libsvgear (svgear_kmeans).
+`kmeans` (the reference's entry point, seed-faithful) draws its k-means++ start on the host with
+the reference's RNG call sequence (clustering.py:65-84, 178-180) so a given `seed` starts from the
+identical centres — the parity path; `device_start` is the device-side seeding the operator uses.
+Lloyd iterations, repair, permutation and means run in libsvgear (svgear_kmeans).
 """
 
 from __future__ import annotations
@@ -68,52 +69,42 @@ def strided_start(tokens, k):
     return tokens.index_select(-2, idx).float().contiguous()
 
 
-def _seed_inputs(tokens, k, oversample):
-    """Output buffer and (when the subsample can hold k centres) the Gram matrix of the strided
-    subsample — one plain batched library GEMM (bf16 in, bf16 out)."""
-    x = tokens if tokens.ndim == 3 else tokens.unsqueeze(0)
-    x = x.contiguous()
+SEED_OVERSAMPLE = 8  # subsample tokens per centre of the device-side seeding
+
+
+def _seed_launch(x, k, seed, oversample, first_instance):
+    """svgear_kmeans_seed on x [bh, n, d] bf16 -> start centres [bh, k, d] f32 (current stream)."""
     bh, n, d = x.shape
     out = torch.empty((bh, k, d), dtype=torch.float32, device=x.device)
     m = min(n, int(oversample) * k, 4096)
-    g = None
-    if m >= k:
-        idx = torch.div(torch.arange(m, device=x.device, dtype=torch.int64) * n, m, rounding_mode="floor")
-        xs = x.index_select(1, idx)
-        g = torch.bmm(xs, xs.transpose(1, 2)).contiguous()
-    return x, out, g, m
+    if m < k:
+        raise ValueError(f"device seeding needs a subsample of >= {k} tokens, got {m} (n={n}, oversample={oversample})")
+    ws = workspace(bh * m * m * 2 + 256, x.device)
+    rc = _lib.lib().svgear_kmeans_seed(bh, n, d, k, x.data_ptr(), int(oversample), int(seed) & 0xFFFFFFFF,
+                                       int(first_instance), out.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr())
+    _lib.check("svgear_kmeans_seed", rc)
+    return out
 
 
-def _seed_launch(x, out, g, m, k, seed, oversample):
-    bh, n, d = x.shape
-    if g is not None:
-        rc = _lib.lib().svgear_kmeans_seed_gram(bh, n, d, k, m, x.data_ptr(), g.data_ptr(),
-                                                int(seed) & 0xFFFFFFFF, out.data_ptr(), stream_ptr())
-        _lib.check("svgear_kmeans_seed_gram", rc)
-    else:
-        rc = _lib.lib().svgear_kmeans_seed(bh, n, d, k, x.data_ptr(), int(oversample), int(seed) & 0xFFFFFFFF,
-                                           out.data_ptr(), stream_ptr())
-        _lib.check("svgear_kmeans_seed", rc)
-
-
-def device_start(tokens, k, seed=0, oversample=8, gram=True):
-    """Device-side k-means++ start on a strided subsample (svgear_kmeans_seed).  Deterministic, but
-    NOT the reference's numpy draw — use `seeded_start` / init="reference" for parity runs."""
-    x, out, g, m = _seed_inputs(tokens, k, oversample)
-    _seed_launch(x, out, g if gram else None, m, k, seed, oversample)
+def device_start(tokens, k, seed=0, oversample=SEED_OVERSAMPLE, first_instance=0):
+    """Device-side k-means++ start on a strided subsample (svgear_kmeans_seed: Gram matrix of the
+    subsample on the tensor cores, then the D^2 rounds).  Deterministic, but NOT the reference's numpy
+    draw — use `seeded_start` / init="reference" for parity runs.  Instance b of a batch draws as
+    instance first_instance + b."""
+    x = (tokens if tokens.ndim == 3 else tokens.unsqueeze(0)).contiguous()
+    out = _seed_launch(x, int(k), seed, oversample, first_instance)
     return out if tokens.ndim == 3 else out[0]
 
 
 _SIDE_STREAMS = {}
 
 
-def device_start_pair(q, c_q, k, c_k, seed=0, oversample=8):
-    """device_start for the query and the key side with the two seeding KERNELS on two streams:
-    each runs one CTA per instance (c sequential D^2 rounds), so the sides overlap on disjoint SMs.
-    Every tensor is allocated on the current stream; the helper stream only carries one kernel and
-    is joined before returning."""
-    xq, oq, gq, mq = _seed_inputs(q, c_q, oversample)
-    xk, ok, gk, mk = _seed_inputs(k, c_k, oversample)
+def device_start_pair(q, c_q, k, c_k, seed=0, oversample=SEED_OVERSAMPLE, first_instance=0):
+    """device_start for the query and the key side on two streams: the D^2 rounds run one CTA per
+    instance (c sequential rounds), so the sides overlap on disjoint SMs.  The key side draws with
+    seed + 0x9E37, as svgear_forward_seeded does.  The helper stream is joined before returning."""
+    xq = (q if q.ndim == 3 else q.unsqueeze(0)).contiguous()
+    xk = (k if k.ndim == 3 else k.unsqueeze(0)).contiguous()
     dev = xq.device
     cur = torch.cuda.current_stream(dev)
     side = _SIDE_STREAMS.get(dev.index)
@@ -121,8 +112,9 @@ def device_start_pair(q, c_q, k, c_k, seed=0, oversample=8):
         side = _SIDE_STREAMS[dev.index] = torch.cuda.Stream(device=dev)
     side.wait_stream(cur)
     with torch.cuda.stream(side):
-        _seed_launch(xk, ok, gk, mk, c_k, seed + 0x9E37, oversample)
-    _seed_launch(xq, oq, gq, mq, c_q, seed, oversample)
+        ok = _seed_launch(xk, int(c_k), seed + 0x9E37, oversample, first_instance)
+        ok.record_stream(cur)
+    oq = _seed_launch(xq, int(c_q), seed, oversample, first_instance)
     cur.wait_stream(side)
     return (oq if q.ndim == 3 else oq[0]), (ok if k.ndim == 3 else ok[0])
 
@@ -143,7 +135,7 @@ def _pad_centers(tok_f32, centers, k):
     return centers
 
 
-def run_lloyd(x, starts, max_iters, fp32_check=False, full_eval=False):
+def run_lloyd(x, starts, max_iters, fp32_check=False, full_eval=False, want_inertia=True):
     """x [bh,n,d] bf16, starts [bh,c,d] f32 -> dict of raw svgear_kmeans outputs.
 
     `full_eval` evaluates every token against every centre in every iteration; by default the
@@ -167,7 +159,7 @@ def run_lloyd(x, starts, max_iters, fp32_check=False, full_eval=False):
         (_lib.EXEC_FP32_CHECK if fp32_check else _lib.EXEC_BF16_TENSOR) | (_lib.KMEANS_FULL_EVAL if full_eval else 0),
         bh, n, d, c, x.data_ptr(), starts.data_ptr(), int(max_iters), out["assign"].data_ptr(),
         out["perm"].data_ptr(), out["sizes"].data_ptr(), out["offsets"].data_ptr(),
-        out["centroids"].data_ptr(), out["iters"].data_ptr(), out["inertia"].data_ptr(),
+        out["centroids"].data_ptr(), out["iters"].data_ptr(), out["inertia"].data_ptr() if want_inertia else None,
         ws.data_ptr(), ws.numel(), stream_ptr())
     _lib.check("svgear_kmeans", rc)
     return out
@@ -182,16 +174,20 @@ def kmeans(tokens, num_clusters, *, max_iters=25, seed=0, restarts=1, init_centr
     """Cluster token rows; best of `restarts` seeded runs (+ an optional warm start).
 
     Mirrors clustering.kmeans (clustering.py:144-207) including its validation errors.  For a
-    batch [bh, n, d], instance b is seeded with `seed + b` and `init_centroids` may be [bh, c', d].
+    batch [bh, n, d], instance b is seeded with `seed + b` (or `seed[b]` when a list of per-instance
+    seeds is given) and `init_centroids` may be [bh, c', d].
     """
     x, was_2d = _validated(tokens, num_clusters, restarts, max_iters)
     bh, n, d = x.shape
     k = int(num_clusters)
     x_host = x.float().cpu().numpy().astype(np.float64)
+    seeds = [int(s_) for s_ in seed] if isinstance(seed, (list, tuple)) else [int(seed) + b for b in range(bh)]
+    if len(seeds) != bh:
+        raise ValueError(f"got {len(seeds)} seeds for {bh} instances")
     pool = []  # list over starts of [bh,k,d] f32
     for r in range(restarts):
         pool.append(torch.from_numpy(np.stack(
-            [seeded_start(x_host[b], k, seed + b, r) for b in range(bh)])).to(x.device, torch.float32))
+            [seeded_start(x_host[b], k, seeds[b], r) for b in range(bh)])).to(x.device, torch.float32))
     if init_centroids is not None:
         ic = torch.as_tensor(np.asarray(init_centroids) if not isinstance(init_centroids, torch.Tensor)
                              else init_centroids)

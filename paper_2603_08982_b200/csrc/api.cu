@@ -1,5 +1,7 @@
 // extern "C" entry points of libsvgear.so (declared in include/svgear.h).
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <mutex>
 #include <string.h>
@@ -10,6 +12,11 @@ using namespace svg;
 
 namespace svg {
 long long g_launches = 0;
+
+void report_cuda_error(cudaError_t e, const char* file, int line) {
+  static const bool on = getenv("SVGEAR_DEBUG") != nullptr;
+  if (on) fprintf(stderr, "libsvgear: %s at %s:%d\n", cudaGetErrorString(e), file, line);
+}
 
 namespace {
 // Helper streams are keyed by (lane, slot): a lane belongs to one caller stream, so that calls issued
@@ -72,6 +79,8 @@ HelperFork::~HelperFork() { (void)join(); }
 
 namespace {
 
+constexpr int kSeedOversampleMax = 8;  // the workspace holds Gram matrices for oversample <= 8
+
 bool shape_ok(const SvgEarShape* s) {
   if (!s) return false;
   if (s->bh < 1 || s->n_q < 1 || s->n_k < 1) return false;
@@ -95,6 +104,7 @@ struct ForwardPlan {
   unsigned long long* route_keys;
   int64_t* entries;
   bf16 *qp, *kp, *vp;
+  bf16 *q_gram, *k_gram;  // Gram matrices of the seeding subsamples (svgear_forward_seeded)
 };
 
 bool plan_forward(const SvgEarShape& s, Carver& cv, ForwardPlan& p) {
@@ -125,6 +135,10 @@ bool plan_forward(const SvgEarShape& s, Carver& cv, ForwardPlan& p) {
   p.qp = cv.take<bf16>((size_t)s.bh * s.n_q * s.d);
   p.kp = cv.take<bf16>((size_t)s.bh * s.n_k * s.d);
   p.vp = cv.take<bf16>((size_t)s.bh * s.n_k * s.d);
+  const size_t mq = (size_t)seed_subsample(s.n_q, s.c_q, kSeedOversampleMax);
+  const size_t mk = (size_t)seed_subsample(s.n_k, s.c_k, kSeedOversampleMax);
+  p.q_gram = cv.take<bf16>((size_t)s.bh * mq * mq);
+  p.k_gram = cv.take<bf16>((size_t)s.bh * mk * mk);
   return cv.ok;
 }
 
@@ -190,25 +204,20 @@ int svgear_kmeans(int32_t exec_mode, int32_t bh, int32_t n, int32_t d, int32_t c
                        offsets, centroids, iters, inertia, sc, (cudaStream_t)stream);
 }
 
-int svgear_kmeans_seed(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
-                       int32_t oversample, uint32_t seed, float* centroids, void* stream) {
-  if (!x || !centroids) return SVGEAR_EINVAL;
-  if (oversample < 1) return SVGEAR_EINVAL;
+int svgear_kmeans_seed(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x, int32_t oversample,
+                       uint32_t seed, int32_t first_instance, float* centroids, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  if (!x || !centroids || !workspace) return SVGEAR_EINVAL;
+  if (oversample < 1 || first_instance < 0) return SVGEAR_EINVAL;
   if (bh < 1 || n < 1 || (d != 64 && d != 128) || c < 1 || c > n || c > kMaxClusters)
     return SVGEAR_ESHAPE;
   if (!device_present()) return SVGEAR_ECUDA;
-  return launch_seed_pp(bh, n, d, c, (const bf16*)x, oversample, seed, centroids, (cudaStream_t)stream);
-}
-
-int svgear_kmeans_seed_gram(int32_t bh, int32_t n, int32_t d, int32_t c, int32_t m, const void* x,
-                            const void* gram, uint32_t seed, float* centroids, void* stream) {
-  if (!x || !gram || !centroids) return SVGEAR_EINVAL;
-  if (bh < 1 || n < 1 || (d != 64 && d != 128) || c < 1 || c > n || c > kMaxClusters || m < c || m > n ||
-      m > 4096)
-    return SVGEAR_ESHAPE;
-  if (!device_present()) return SVGEAR_ECUDA;
-  return launch_seed_gram(bh, n, d, c, m, (const bf16*)x, (const bf16*)gram, seed, centroids,
-                          (cudaStream_t)stream);
+  const size_t m = (size_t)seed_subsample(n, c, oversample);
+  Carver cv(workspace, workspace_bytes);
+  bf16* gram = cv.take<bf16>((size_t)bh * m * m);
+  if (!cv.ok) return SVGEAR_EWORKSPACE;
+  return launch_seed(bh, n, d, c, oversample, (const bf16*)x, seed, first_instance, centroids, gram,
+                     (cudaStream_t)stream);
 }
 
 int svgear_permute_rows(int32_t bh, int32_t n, int32_t d, const void* x, const int32_t* perm,
@@ -340,9 +349,7 @@ namespace {
 // stream of that side's Lloyd loop (svgear_forward_seeded), so the short query-side seeding does not
 // wait for the long key-side one.
 struct SeedPlan {
-  const bf16* q_gram;
-  const bf16* k_gram;
-  int m_q, m_k;
+  int oversample;
   uint32_t seed;
   int first;  // index of this call's first instance in the caller's whole batch
 };
@@ -401,8 +408,8 @@ int forward_impl(const SvgEarShape* shape, const void* q, const void* k, const v
     HelperFork fk(st, 0);
     if (!fk.ok()) return SVGEAR_ECUDA;
     cudaStream_t side = fk.side();
-    rc_k = sp ? launch_seed_gram(s.bh, s.n_k, s.d, s.c_k, sp->m_k, (const bf16*)k, sp->k_gram, sp->seed + 0x9E37u,
-                                 k_init, side, sp->first)
+    rc_k = sp ? launch_seed(s.bh, s.n_k, s.d, s.c_k, sp->oversample, (const bf16*)k, sp->seed + 0x9E37u, sp->first,
+                            k_init, p.k_gram, side)
               : SVGEAR_OK;
     if (!rc_k)
       rc_k = launch_kmeans(exec_mode, s.bh, s.n_k, s.d, s.c_k, (const bf16*)k, k_init, kmeans_iters, k_assign,
@@ -415,7 +422,8 @@ int forward_impl(const SvgEarShape* shape, const void* q, const void* k, const v
     // stream, under the (usually longer) query-side Lloyd loop
     if (!rc_k && keys_early)
       rc_k = launch_error_table_keys(s, estimator_mode, k_cent, v_cent, p.kp, p.vp, k_sizes, k_offsets, p.es, side);
-    rc = sp ? launch_seed_gram(s.bh, s.n_q, s.d, s.c_q, sp->m_q, (const bf16*)q, sp->q_gram, sp->seed, q_init, st, sp->first)
+    rc = sp ? launch_seed(s.bh, s.n_q, s.d, s.c_q, sp->oversample, (const bf16*)q, sp->seed, sp->first, q_init,
+                          p.q_gram, st)
             : SVGEAR_OK;
     if (!rc)
       rc = launch_kmeans(exec_mode, s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign,
@@ -461,16 +469,16 @@ int svgear_forward(const SvgEarShape* shape, const void* q, const void* k, const
 }
 
 int svgear_forward_seeded(const SvgEarShape* shape, const void* q, const void* k, const void* v,
-                          const void* q_gram, const void* k_gram, int32_t m_q, int32_t m_k, uint32_t seed,
-                          int32_t first_instance, float* q_init, float* k_init, int32_t kmeans_iters, int32_t estimator_mode,
-                          int64_t capacity_entries, int32_t overshoot, int32_t single_item_fallback,
-                          int32_t exec_mode, double top_p, void* out, uint8_t* mask, const SvgEarAux* aux,
-                          void* workspace, size_t workspace_bytes, void* stream) {
-  if (!shape || !q_gram || !k_gram || first_instance < 0) return SVGEAR_EINVAL;
+                          int32_t oversample, uint32_t seed, int32_t first_instance, float* q_init, float* k_init,
+                          int32_t kmeans_iters, int32_t estimator_mode, int64_t capacity_entries, int32_t overshoot,
+                          int32_t single_item_fallback, int32_t exec_mode, double top_p, void* out, uint8_t* mask,
+                          const SvgEarAux* aux, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape || first_instance < 0 || oversample < 1 || oversample > kSeedOversampleMax) return SVGEAR_EINVAL;
   if (!shape_ok(shape)) return SVGEAR_ESHAPE;
-  if (m_q < shape->c_q || m_q > shape->n_q || m_q > 4096 || m_k < shape->c_k || m_k > shape->n_k || m_k > 4096)
+  if (seed_subsample(shape->n_q, shape->c_q, oversample) < shape->c_q ||
+      seed_subsample(shape->n_k, shape->c_k, oversample) < shape->c_k)
     return SVGEAR_ESHAPE;
-  SeedPlan sp{(const bf16*)q_gram, (const bf16*)k_gram, m_q, m_k, seed, first_instance};
+  SeedPlan sp{oversample, seed, first_instance};
   return forward_impl(shape, q, k, v, q_init, k_init, &sp, kmeans_iters, estimator_mode, capacity_entries,
                       overshoot, single_item_fallback, exec_mode, top_p, out, mask, aux, workspace,
                       workspace_bytes, stream);

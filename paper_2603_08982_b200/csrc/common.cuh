@@ -6,17 +6,21 @@
 
 #include "../../include/svgear.h"
 
-#define SVG_CUDA_OK(call)                       \
-  do {                                          \
-    cudaError_t e__ = (call);                   \
-    if (e__ != cudaSuccess) return SVGEAR_ECUDA; \
+// SVGEAR_DEBUG=1 in the environment names the failing CUDA call on stderr (diagnostic only).
+#define SVG_CUDA_OK(call)                                    \
+  do {                                                       \
+    cudaError_t e__ = (call);                                \
+    if (e__ != cudaSuccess) {                                \
+      svg::report_cuda_error(e__, __FILE__, __LINE__);       \
+      return SVGEAR_ECUDA;                                   \
+    }                                                        \
   } while (0)
 
 #define SVG_LAUNCH_OK()                                      \
   do {                                                       \
     ++svg::g_launches;                                       \
     if (cudaPeekAtLastError() != cudaSuccess) {              \
-      (void)cudaGetLastError();                              \
+      svg::report_cuda_error(cudaGetLastError(), __FILE__, __LINE__); \
       return SVGEAR_ECUDA;                                   \
     }                                                        \
   } while (0)
@@ -24,6 +28,7 @@
 namespace svg {
 
 extern long long g_launches;  // diagnostic: kernels launched by this library in this process
+void report_cuda_error(cudaError_t e, const char* file, int line);
 
 typedef __nv_bfloat16 bf16;
 
@@ -112,10 +117,8 @@ struct KmeansScratch {
   int32_t* prev_assign;   // [bh][n]
   float* own_d2;          // [bh][n]
   float* cnorm;           // [bh][c]
-  int32_t* chunk_counts;  // [bh][nchunks][c]
   double* chunk_inertia;  // [bh][nchunks]
   int32_t* done;          // [bh]
-  int32_t* changed;       // [bh]
   bf16* pieces;           // [bh][pieces][cpad][d]  split-bf16 centroids (tensor-core assignment)
   float* cnorm_pad;       // [bh][cpad]
   float* xnorm;           // [bh][n]
@@ -127,22 +130,38 @@ struct KmeansScratch {
   float* move;            // [bh][c]  |c_new - c_old| of the last update
   uint8_t* dirty;         // [bh][c]  membership changed this iteration
   int32_t* iters_run;     // [bh]     iterations executed (internal copy of `iters`)
-  int32_t* ticket;        // [bh]     block ticket counter of sizes_hist_kernel
-  int32_t* has_empty;     // [bh]     some cluster is empty after this iteration's assignment
   int32_t* resid_nz;      // [bh]     the second bf16 piece of some centre is non-zero
-  float* dmin;            // [bh][c]  distance from each centre to the nearest big mover (movers_kernel)
-  float2* movers;         // [bh]     {number of big movers (0: none), max movement of the other centres}
+  float* dmin;            // [bh][c]  distance from each centre to the nearest big mover (lloyd_step_kernel B2)
   bool carve(Carver& cv, int bh, int n, int c, int d);
 };
+
+// Arguments of the fused per-iteration kernel (lloyd_step.cu); all arrays are the [bh][...] ones above.
+struct LloydStepArgs {
+  const bf16* x;
+  int n, c, cpad;
+  int iter;           // -1: set up the state of iteration 0 (norms, pieces, all-active list)
+  int max_iters;
+  int use_tc;         // tensor-core assignment: pieces / bounds / active lists are maintained
+  int bounded;        // bound-based skipping (use_tc and not FULL_EVAL)
+  int bounded_state;  // ub / lb / dirty exist (== use_tc)
+  int phases;         // bit 0: histograms .. permutation, bit 1: means + next iteration's inputs
+  int wsort, scratch_bytes;  // filled by the launcher
+  int32_t *assign, *prev, *perm, *sizes, *offsets, *iters;
+  float *cent, *cnorm, *own, *ub, *lb, *move, *dmin, *cnorm_pad, *xnorm;
+  uint8_t* dirty;
+  bf16* pieces;
+  int32_t *active, *nactive, *resid_nz, *done, *iters_run;
+};
+int launch_lloyd_step(const LloydStepArgs& args, int bh, int d, cudaStream_t st);
 
 int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, const float* init,
                   int max_iters, int32_t* assign, int32_t* perm, int32_t* sizes, int32_t* offsets,
                   float* centroids, int32_t* iters, double* inertia, KmeansScratch& sc,
                   cudaStream_t st);
-int launch_seed_pp(int bh, int n, int d, int c, const bf16* x, int oversample, uint32_t seed, float* cent,
-                   cudaStream_t st);
-int launch_seed_gram(int bh, int n, int d, int c, int m, const bf16* x, const bf16* gram, uint32_t seed,
-                     float* cent, cudaStream_t st, int first_instance = 0);
+// device-side k-means++ seeding (seed.cu): subsample size, and the two-kernel launch
+int seed_subsample(int n, int c, int oversample);
+int launch_seed(int bh, int n, int d, int c, int oversample, const bf16* x, uint32_t seed, int first_instance,
+                float* cent, bf16* gram_ws, cudaStream_t st);
 int launch_gather_rows(int bh, int n, int d, const bf16* x, const int32_t* perm, bf16* out,
                        cudaStream_t st);
 int launch_segment_means(int bh, int n, int d, int c, const bf16* xp, const int32_t* sizes,

@@ -50,239 +50,60 @@ struct KSmem {
 };
 }  // namespace
 
-// fp32 centroids -> kPieces bf16 pieces [bh][piece][cpad][d] + padded norms (inf beyond c)
-__global__ void split_centroids_kernel(const float* __restrict__ cent, const float* __restrict__ cnorm,
-                                       int d, int c, int cpad, bf16* __restrict__ pieces,
-                                       float* __restrict__ cnorm_pad, int32_t* __restrict__ resid_nz,
-                                       const int32_t* __restrict__ done) {
-  const int h = blockIdx.y;
-  if (done[h]) return;
-  int nz = 0;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < cpad * d; idx += gridDim.x * blockDim.x) {
-    const int j = idx / d;
-    float v = j < c ? cent[(size_t)h * c * d + idx] : 0.f;
-#pragma unroll
-    for (int p = 0; p < kPieces; ++p) {
-      const bf16 b = __float2bfloat16_rn(v);
-      pieces[((size_t)h * kPieces + p) * cpad * d + idx] = b;
-      v -= __bfloat162float(b);
-      if (p == 0) nz |= (v != 0.f);
-    }
-    if (idx % d == 0) cnorm_pad[(size_t)h * cpad + j] = j < c ? cnorm[(size_t)h * c + j] : INFINITY;
-  }
-  // centres that are exactly bf16 (start centres picked from the tokens) need only the first piece
-  if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(&resid_nz[h], 1);
-}
-
-__global__ void token_norm_kernel(const bf16* __restrict__ x, int d, long long total, float* __restrict__ xn) {
+// |x|^2 per token (a per-token constant of the arg-min; it only enters own_d2 and the bounds).  One warp
+// per row, lanes split the row (8-byte loads at d=128), fixed shuffle tree; 4 rows in flight per warp.
+__global__ void __launch_bounds__(256)
+    token_norm_kernel(const bf16* __restrict__ x, int d, long long total, float* __restrict__ xn) {
   const int lane = threadIdx.x & 31;
   const long long warp_id = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const long long nwarps = (long long)gridDim.x * (blockDim.x / 32);
-  for (long long row = warp_id; row < total; row += nwarps) {
-  // sequential-in-k accumulation per lane chunk is not needed for parity: |x|^2 is a per-token
-  // constant of the argmin; it only enters own_d2.  Lanes split the row, fixed shuffle tree.
-  // each lane takes d/32 consecutive elements (8-byte loads at d=128), fixed shuffle tree
-  const bf16* p = x + row * d;
-  float s = 0.f;
-  if (d == 128) {
-    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p) + lane);
-    const float f0 = __uint_as_float(u.x << 16), f1 = __uint_as_float(u.x & 0xffff0000u);
-    const float f2 = __uint_as_float(u.y << 16), f3 = __uint_as_float(u.y & 0xffff0000u);
-    s = fmaf(f0, f0, s); s = fmaf(f1, f1, s); s = fmaf(f2, f2, s); s = fmaf(f3, f3, s);
-  } else {
-    for (int k = lane * 2; k < d; k += 64) {
-      const uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(p + k));
-      const float f0 = __uint_as_float(u << 16), f1 = __uint_as_float(u & 0xffff0000u);
-      s = fmaf(f0, f0, s); s = fmaf(f1, f1, s);
+  constexpr int R = 4;
+  for (long long row0 = warp_id * R; row0 < total; row0 += nwarps * R) {
+    float s[R];
+    if (d == 128) {
+      uint2 u[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const long long row = row0 + r < total ? row0 + r : total - 1;
+        u[r] = __ldg(reinterpret_cast<const uint2*>(x + row * d) + lane);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float f0 = __uint_as_float(u[r].x << 16), f1 = __uint_as_float(u[r].x & 0xffff0000u);
+        const float f2 = __uint_as_float(u[r].y << 16), f3 = __uint_as_float(u[r].y & 0xffff0000u);
+        float a = 0.f;
+        a = fmaf(f0, f0, a); a = fmaf(f1, f1, a); a = fmaf(f2, f2, a); a = fmaf(f3, f3, a);
+        s[r] = a;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const long long row = row0 + r < total ? row0 + r : total - 1;
+        float a = 0.f;
+        for (int k = lane * 2; k < d; k += 64) {
+          const uint32_t u = __ldg(reinterpret_cast<const uint32_t*>(x + row * d + k));
+          const float f0 = __uint_as_float(u << 16), f1 = __uint_as_float(u & 0xffff0000u);
+          a = fmaf(f0, f0, a); a = fmaf(f1, f1, a);
+        }
+        s[r] = a;
+      }
     }
-  }
-  s = warp_sum(s);
-  if (lane == 0) xn[row] = s;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float v = warp_sum(s[r]);
+      if (lane == 0 && row0 + r < total) xn[row0 + r] = v;
+    }
   }
 }
 
 // ------------------------------------------------------------------------------------------------
 // Exact bound-based skipping (Hamerly's bounds) — same assignments as plain Lloyd, fewer distances.
-// Every token carries ub >= dist(x, c[assign]) and lb <= min_{j != assign} dist(x, c[j]).  After a
-// centroid update that moved centre j by move[j] (triangle inequality):
-//     ub += move[assign],   lb -= max_{j != assign} move[j].
-// A token whose ub is still below lb (with a margin that covers the fp32 / split-bf16 rounding of
-// the distances the tensor-core kernel would compute) keeps its cluster without being evaluated;
-// the others are compacted into the instance's `active` list and re-evaluated by assign_tc_kernel,
-// which refreshes both bounds.  Iteration 0 (and SVGEAR_KMEANS_FULL_EVAL) marks every token active.
-// Block 0 of each instance also resets the per-iteration counters (sizes, changed, dirty).
+// Every token carries ub >= dist(x, c[assign]) and lb <= min_{j != assign} dist(x, c[j]); after a
+// centroid update lloyd_step_kernel (lloyd_step.cu, phase B2) shifts them by the centre movements
+// and compacts the tokens whose bounds overlap into the instance's `active` list.  This kernel
+// re-evaluates exactly those tokens and refreshes both bounds.  Iteration 0 (and
+// SVGEAR_KMEANS_FULL_EVAL) has every token active.
 // ------------------------------------------------------------------------------------------------
-constexpr int kFilterTokens = 2048;  // tokens per CTA
-constexpr int kMaxMovers = 64;
-
-// A few centres that moved far — typically clusters refilled by the empty-cluster repair, whose centre
-// jumps onto the donor token — would push EVERY token's lower bound below its upper bound through
-// the global max-movement term.  Per instance this kernel separates the big movers
-// L = {j : move[j] > max_move / 4} (used only when |L| <= kMaxMovers) and gives every cluster a the
-// distance from its (new) centre to the nearest big mover e != a.  For a token x of cluster a,
-//     dist(x, c_e) >= dist(c_a, c_e) - dist(x, c_a) >= dmin[a] - ub(x)      (triangle inequality)
-// so the filter may charge only the movement of the REMAINING centres to the lower bound:
-//     lb <- min(lb - max_{j not in L} move[j],  dmin[a] - ub).
-// info[h] = {|L| (0 = plain Hamerly), max movement outside L}.
-__global__ void __launch_bounds__(256)
-    movers_kernel(int c, int d, const float* __restrict__ cent, const float* __restrict__ move,
-                  float* __restrict__ dmin, float2* __restrict__ info, const int32_t* __restrict__ done) {
-  const int h = blockIdx.y;
-  if (done[h]) return;
-  extern __shared__ float s_mc[];  // [kMaxMovers][d] centres of the big movers
-  __shared__ int s_list[kMaxMovers];
-  __shared__ int s_n;
-  __shared__ float s_red[8];
-  __shared__ float s_m1, s_rest;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // every block of the instance derives the same mover set (32 clusters per block below)
-  const float* mv = move + (size_t)h * c;
-  float m = 0.f;
-  for (int j = tid; j < c; j += 256) m = fmaxf(m, mv[j]);
-  m = warp_max(m);
-  if (lane == 0) s_red[warp] = m;
-  if (tid == 0) s_n = 0;
-  __syncthreads();
-  if (tid == 0) {
-    float v = s_red[0];
-    for (int w = 1; w < 8; ++w) v = fmaxf(v, s_red[w]);
-    s_m1 = v;
-  }
-  __syncthreads();
-  const float thr = s_m1 * 0.25f;
-  float rest = 0.f;
-  for (int j = tid; j < c; j += 256) {
-    const float v = mv[j];
-    if (v > thr && s_m1 > 0.f) {
-      const int pos = atomicAdd(&s_n, 1);
-      if (pos < kMaxMovers) s_list[pos] = j;
-    } else {
-      rest = fmaxf(rest, v);
-    }
-  }
-  rest = warp_max(rest);
-  __syncthreads();
-  if (lane == 0) s_red[warp] = rest;
-  __syncthreads();
-  if (tid == 0) {
-    float v = s_red[0];
-    for (int w = 1; w < 8; ++w) v = fmaxf(v, s_red[w]);
-    s_rest = v;
-  }
-  __syncthreads();
-  const int nl = s_n;
-  if (nl == 0 || nl > kMaxMovers || c <= nl) {  // no outliers (or too many): plain Hamerly
-    if (tid == 0 && blockIdx.x == 0) info[h] = make_float2(0.f, 0.f);
-    return;
-  }
-  for (int i = tid; i < nl * d; i += 256) s_mc[i] = cent[((size_t)h * c + s_list[i / d]) * d + i % d];
-  __syncthreads();
-  // 8 lanes per cluster (d/8 consecutive elements each), 4 clusters per warp, 32 per block
-  const int a = blockIdx.x * 32 + warp * 4 + (lane >> 3), sub = lane & 7, epl = d / 8;
-  const int aa = min(a, c - 1);
-  float ca[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) ca[k] = k < epl ? cent[((size_t)h * c + aa) * d + sub * epl + k] : 0.f;
-  float best = INFINITY;
-  for (int q = 0; q < nl; ++q) {
-    const float* mc = s_mc + q * d + sub * epl;
-    float acc = 0.f;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      if (k < epl) {
-        const float df = ca[k] - mc[k];
-        acc = fmaf(df, df, acc);
-      }
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-    if (s_list[q] != aa) best = fminf(best, acc);
-  }
-  if (a < c && sub == 0) dmin[(size_t)h * c + a] = sqrtf(best) * (1.0f - 1.0f / 65536.0f);
-  if (tid == 0 && blockIdx.x == 0) info[h] = make_float2((float)nl, s_rest);
-}
-
-__global__ void __launch_bounds__(256)
-    bound_filter_kernel(int n, int c, int all_active, const int32_t* __restrict__ assign,
-                        const float* __restrict__ move, const float* __restrict__ dmin,
-                        const float2* __restrict__ info, const float* __restrict__ cnorm,
-                        const float* __restrict__ xnorm, float* __restrict__ ub, float* __restrict__ lb,
-                        int32_t* __restrict__ active, int32_t* __restrict__ nactive,
-                        int32_t* __restrict__ sizes, int32_t* __restrict__ changed,
-                        uint8_t* __restrict__ dirty, const int32_t* __restrict__ done) {
-  const int h = blockIdx.y;
-  if (done[h]) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lo = blockIdx.x * kFilterTokens, hi = min(n, lo + kFilterTokens);
-  if (blockIdx.x == 0) {
-    for (int j = tid; j < c; j += 256) {
-      sizes[(size_t)h * c + j] = 0;
-      dirty[(size_t)h * c + j] = all_active ? 1 : 0;
-    }
-    if (tid == 0) {
-      changed[h] = 0;
-      if (all_active) nactive[h] = n;
-    }
-  }
-  if (all_active) {
-    for (int t = lo + tid; t < hi; t += 256) active[(size_t)h * n + t] = t;
-    return;
-  }
-  // largest / second largest centre movement and the largest centre norm of this instance
-  __shared__ float s_m1[8], s_m2[8], s_cn[8];
-  __shared__ int s_a1[8];
-  float m1 = 0.f, m2 = 0.f, cn = 0.f;
-  int a1 = -1;
-  for (int j = tid; j < c; j += 256) {
-    const float v = move[(size_t)h * c + j];
-    if (v > m1) { m2 = m1; m1 = v; a1 = j; } else if (v > m2) m2 = v;
-    cn = fmaxf(cn, cnorm[(size_t)h * c + j]);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float om1 = __shfl_xor_sync(0xffffffffu, m1, o), om2 = __shfl_xor_sync(0xffffffffu, m2, o);
-    const int oa1 = __shfl_xor_sync(0xffffffffu, a1, o);
-    if (om1 > m1) { m2 = fmaxf(m1, om2); m1 = om1; a1 = oa1; } else m2 = fmaxf(m2, om1);
-    cn = fmaxf(cn, __shfl_xor_sync(0xffffffffu, cn, o));
-  }
-  if (lane == 0) { s_m1[warp] = m1; s_m2[warp] = m2; s_a1[warp] = a1; s_cn[warp] = cn; }
-  __syncthreads();
-  m1 = s_m1[0]; m2 = s_m2[0]; a1 = s_a1[0]; cn = s_cn[0];
-  for (int w = 1; w < 8; ++w) {
-    if (s_m1[w] > m1) { m2 = fmaxf(m1, s_m2[w]); m1 = s_m1[w]; a1 = s_a1[w]; } else m2 = fmaxf(m2, s_m1[w]);
-    cn = fmaxf(cn, s_cn[w]);
-  }
-  // movements are rounded fp32 norms: inflate them slightly so the bounds stay bounds
-  constexpr float kInfl = 1.0f + 1.0f / 65536.0f;
-  m1 *= kInfl; m2 *= kInfl;
-  const float2 inf = info[h];
-  const bool movers = inf.x > 0.f;  // big movers handled through the inter-centre bound (movers_kernel)
-  const float mrest = inf.y * kInfl;
-  for (int t0 = lo; t0 < hi; t0 += 256) {
-    const int t = t0 + tid;
-    bool act = false;
-    if (t < hi) {
-      const size_t g = (size_t)h * n + t;
-      const int a = assign[g];
-      const float u = ub[g] + move[(size_t)h * c + a] * kInfl;
-      const float l = movers ? fminf(lb[g] - mrest, dmin[(size_t)h * c + a] - u) : lb[g] - (a == a1 ? m2 : m1);
-      ub[g] = u;
-      lb[g] = l;
-      // squared-space margin: the evaluated distances carry an absolute error of a few
-      // 2^-17 (|x|^2 + |c|^2) (2-piece bf16 split + fp32 accumulation); 2^-12 covers it 30x
-      const float marg = (xnorm[g] + cn) * (1.0f / 4096.0f);
-      act = !(l > 0.f && u * u * kInfl + marg < l * l * (2.0f - kInfl));
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, act);
-    if (bal) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&nactive[h], __popc(bal));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (act) active[(size_t)h * n + base + __popc(bal & ((1u << lane) - 1u))] = t;
-    }
-  }
-}
 
 // Persistent kernel: grid = #SMs; CTA b handles work items b, b+grid, ... where an item is a
 // 256-token tile of a not-yet-converged instance.  Token tiles are double buffered (the next item's
@@ -558,29 +379,15 @@ __global__ void __launch_bounds__(KTHREADS, 1)
 
 int launch_token_norms(int bh, int n, int d, const bf16* x, float* xnorm, cudaStream_t st) {
   const long long total = (long long)bh * n;
-  token_norm_kernel<<<(unsigned)((total + 63) / 64 < 148 * 32 ? (total + 63) / 64 : 148 * 32), 256, 0, st>>>(x, d, total, xnorm);
+  token_norm_kernel<<<(unsigned)((total + 31) / 32 < 148 * 16 ? (total + 31) / 32 : 148 * 16), 256, 0, st>>>(x, d, total, xnorm);
   SVG_LAUNCH_OK();
   return SVGEAR_OK;
 }
 
-int launch_kmeans_assign_tc(int bh, int n, int d, int c, int iter, bool full_eval, const bf16* x,
-                            const float* cent, const float* cnorm, KmeansScratch& sc, int32_t* assign,
-                            int32_t* sizes, cudaStream_t st) {
+int launch_kmeans_assign_tc(int bh, int n, int d, int c, int iter, const bf16* x, KmeansScratch& sc,
+                            int32_t* assign, cudaStream_t st) {
   const int cpad = ceil_div(c, KN) * KN;     // row stride of the piece arrays / norm array
   const int cpad16 = ceil_div(c, 16) * 16;   // columns actually multiplied
-  split_centroids_kernel<<<dim3(min(ceil_div(cpad * d, 256), 64), bh), 256, 0, st>>>(cent, cnorm, d, c, cpad, sc.pieces,
-                                                                           sc.cnorm_pad, sc.resid_nz, sc.done);
-  SVG_LAUNCH_OK();
-  const int all_active = (iter == 0 || full_eval) ? 1 : 0;
-  if (!all_active) {
-    movers_kernel<<<dim3(ceil_div(c, 32), bh), 256, (size_t)kMaxMovers * d * sizeof(float), st>>>(c, d, cent, sc.move, sc.dmin, sc.movers,
-                                                                         sc.done);
-    SVG_LAUNCH_OK();
-  }
-  bound_filter_kernel<<<dim3(ceil_div(n, kFilterTokens), bh), 256, 0, st>>>(
-      n, c, all_active, assign, sc.move, sc.dmin, sc.movers, cnorm, sc.xnorm, sc.ub, sc.lb, sc.active, sc.nactive, sizes,
-      sc.changed, sc.dirty, sc.done);
-  SVG_LAUNCH_OK();
   static int num_sms = 0;
   if (num_sms == 0) {
     int dev = 0;

@@ -46,7 +46,7 @@ class BlockErrorTable:
         return self.error_sum * torch.exp(2.0 * self.stabilizers.double()).unsqueeze(-1)
 
 
-def _run(q_model: ClusterModel, k_model: ClusterModel, k, v, mode, fp32_check=False):
+def _run(q_model: ClusterModel, k_model: ClusterModel, k, v, mode, fp32_check=False, v_centroids=None):
     kp, was_2d = as_tokens(k, "k", check_finite=False)
     bh, n_k, d = kp.shape
     vp = None
@@ -61,8 +61,10 @@ def _run(q_model: ClusterModel, k_model: ClusterModel, k, v, mode, fp32_check=Fa
     qs = q_model.sizes.view(bh, c_q).contiguous()
     ks = k_model.sizes.view(bh, c_k).contiguous()
     ko = k_model.offsets.view(bh, c_k).contiguous()
-    vc = segment_means(vp, ClusterModel(c_k, k_model.assignments, kc, ks, k_model.permutation, ko)) \
-        if vp is not None else None
+    vc = None
+    if vp is not None:  # v̄ (clustering.segment_means): computed here unless the caller already has it
+        vc = v_centroids.view(bh, c_k, d).float().contiguous() if v_centroids is not None else \
+            segment_means(vp, ClusterModel(c_k, k_model.assignments, kc, ks, k_model.permutation, ko))
     err = torch.empty((bh, c_q, c_k), dtype=torch.float64, device=dev)
     stab = torch.empty((bh, c_q), dtype=torch.float32, device=dev)
     n_q = int(qs[0].sum())
@@ -81,12 +83,13 @@ def _run(q_model: ClusterModel, k_model: ClusterModel, k, v, mode, fp32_check=Fa
                            mode=mode, flops=c_q * n_k * per_key)
 
 
-def estimate_errors_streaming(q_model, k_model, k, v, *, tile_size: int = 64, fp32_check=False):
+def estimate_errors_streaming(q_model, k_model, k, v, *, tile_size: int = 64, fp32_check=False, v_centroids=None):
     """Value-aware table (estimator.py:187-253).  `k`, `v` cluster-contiguous for k_model.  The
-    result does not depend on the tile size (the kernel streams 32-key tiles)."""
+    result does not depend on the tile size (the kernel streams 32-key tiles).  `v_centroids`
+    (optional, [.., C_k, d] float32 = segment_means(v, k_model)) saves recomputing them."""
     if tile_size < 1:
         raise ValueError(f"tile_size must be >= 1, got {tile_size}")
-    return _run(q_model, k_model, k, v, "valueAware", fp32_check)
+    return _run(q_model, k_model, k, v, "valueAware", fp32_check, v_centroids)
 
 
 def estimate_errors_value_aware(q_model, k_model, k, v):

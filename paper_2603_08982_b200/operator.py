@@ -16,7 +16,7 @@ import torch
 from . import _lib
 from ._tensors import ShapeError, require_cuda, stream_ptr, workspace
 from .analysis import side_seeds
-from .clustering import _seed_inputs, device_start_pair, seeded_start, strided_start
+from .clustering import SEED_OVERSAMPLE, seeded_start, strided_start
 from .router import _OVERSHOOT, entry_capacity
 
 _EST = {"valueAware": _lib.EST_VALUE_AWARE, "plain": _lib.EST_PLAIN}
@@ -58,7 +58,8 @@ def operator_workspace_bytes(bh, n_q, n_k, d, n_q_clusters, n_k_clusters, head_g
 def reference_init(q, k, n_q_clusters, n_k_clusters, seed):
     """k-means++ start centres the reference would draw for `prepare(seed=...)`, for every
     instance of a [.., S, d] batch (instance index b uses seed + b).  Host-side numpy; meant for
-    parity runs — it is O(C*S*d) per instance on the CPU."""
+    parity runs only — it is O(C*S*d) per instance on the CPU (minutes at video scale), which is why
+    the operator's default start is the device-side seeding."""
     qf = q.reshape(-1, q.shape[-2], q.shape[-1]).float().cpu().numpy().astype(np.float64)
     kf = k.reshape(-1, k.shape[-2], k.shape[-1]).float().cpu().numpy().astype(np.float64)
     qi, ki = [], []
@@ -70,10 +71,10 @@ def reference_init(q, k, n_q_clusters, n_k_clusters, seed):
 
 
 def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_init=None,
-                      k_init=None, init="reference", kmeans_iters=25, estimator="valueAware",
+                      k_init=None, init="device", kmeans_iters=25, estimator="valueAware",
                       overshoot="fillRemainder", single_item_fallback=True, check_fp32=False,
                       return_aux=False, workspace_buffer=None, budget_mode="globalDensity",
-                      head_groups=None, stagger_groups=False):
+                      head_groups=None, stagger_groups=False, head_offset=0, total_heads=None, _row_base=0):
     """SVG-EAR attention.
 
     q, k, v : bf16 CUDA tensors [B, H, S, d] (or [H, S, d] / [S, d]); d in {64, 128}.
@@ -82,10 +83,17 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
              (router.DensityBudget.global_density, router.py:59-61); with
              budget_mode="perClusterTopP" it is the per-query-cluster score mass p in (0, 1]
              (router.DensityBudget.top_p, router.py:63-65 — the paper's production setting p=0.85).
-    init   : "reference" -> k-means++ centres drawn with the reference's RNG recipe from `seed`
-             (host side, slow at scale); "device" -> k-means++ on a strided subsample, on the
-             device (svgear_kmeans_seed); "strided" -> evenly strided tokens;
-             ignored for a side whose q_init / k_init ([.., C, d] float32 centres) is given.
+    init   : "device" (default) -> k-means++ on a strided subsample, on the device, inside the one
+             C-ABI call; "reference" -> k-means++ centres drawn with the reference's RNG recipe
+             from `seed` — the parity switch: it copies Q and K to the HOST and runs O(C*S*d)
+             float64 numpy per instance, so it is for tests at small shapes only; "strided" ->
+             evenly strided tokens; ignored for a side whose q_init / k_init ([.., C, d] float32
+             centres) is given.
+    seed   : instance (b, h) of a [B, H, S, d] call is seeded by `seed + g` with the GLOBAL
+             instance index g = b * total_heads + head_offset + h.
+    head_offset, total_heads : for a caller that holds only heads [head_offset, head_offset + H)
+             of a layer with total_heads heads (head-parallel sharding): makes g, and with it every
+             result, independent of how the heads are split.  Default: the call holds all heads.
     check_fp32 : run the executor in fp32 on CUDA cores and return a float32 output.
     head_groups : split the B*H instances into this many contiguous groups and run one
              svgear_forward per group on its own CUDA stream (joined before returning): the
@@ -135,24 +143,46 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
     dev = require_cuda()
     lead = tuple(q.shape[:-2])
     bh = int(np.prod(lead)) if lead else 1
+    h_local = lead[-1] if lead else 1
+    total_heads = h_local if total_heads is None else int(total_heads)
+    head_offset = int(head_offset)
+    if head_offset < 0 or head_offset + h_local > total_heads:
+        raise ValueError(f"heads [{head_offset}, {head_offset + h_local}) do not fit in total_heads={total_heads}")
+    if len(lead) == 2 and lead[0] > 1 and total_heads != h_local:
+        # the global instance indices of a head shard are contiguous per batch row only
+        rows = [svg_ear_attention(
+            q[b], k[b], v[b], n_q_clusters, n_k_clusters, budget, seed=seed, _row_base=b * total_heads,
+            q_init=None if q_init is None else q_init[b], k_init=None if k_init is None else k_init[b],
+            init=init, kmeans_iters=kmeans_iters, estimator=estimator, overshoot=overshoot,
+            single_item_fallback=single_item_fallback, check_fp32=check_fp32, return_aux=return_aux,
+            budget_mode=budget_mode, head_groups=head_groups, stagger_groups=stagger_groups,
+            head_offset=head_offset, total_heads=total_heads) for b in range(lead[0])]
+        stacked = tuple(torch.stack([r[i] for r in rows]) for i in range(2))
+        if not return_aux:
+            return stacked
+        return stacked + ({name: torch.stack([r[2][name] for r in rows]) for name in rows[0][2]},)
+    first_instance = int(_row_base) + head_offset  # global index of this call's first instance
     qb = q.to(dev, torch.bfloat16).reshape(bh, n_q, d).contiguous()
     kb = k.to(dev, torch.bfloat16).reshape(bh, n_k, d).contiguous()
     vb = v.to(dev, torch.bfloat16).reshape(bh, n_k, d).contiguous()
     c_q, c_k = int(n_q_clusters), int(n_k_clusters)
 
-    seeded = None  # (q_gram, m_q, k_gram, m_k): seed inside the forward call, each side on its own stream
+    # start centres: given, or drawn on the device INSIDE the forward call (each side's seeding on the
+    # stream of its own Lloyd loop), or — parity switch — the reference's host-side draw
+    seeded = False
     if q_init is None and k_init is None and init == "device":
-        _, q_init, gq, mq = _seed_inputs(qb, c_q, 8)
-        _, k_init, gk, mk = _seed_inputs(kb, c_k, 8)
-        if gq is not None and gk is not None:
-            seeded = (gq, mq, gk, mk)
-        else:
-            q_init = k_init = None
+        for c, n in ((c_q, n_q), (c_k, n_k)):
+            if min(n, SEED_OVERSAMPLE * c, 4096) < c:
+                raise ValueError(f"device seeding cannot hold {c} clusters in its subsample (n={n}); pass init centres")
+        seeded = True
+        q_init = torch.empty((bh, c_q, d), dtype=torch.float32, device=dev)
+        k_init = torch.empty((bh, c_k, d), dtype=torch.float32, device=dev)
     if q_init is None or k_init is None:
         if init == "reference":
-            rq, rk = reference_init(qb, kb, c_q, c_k, seed)
+            rq, rk = reference_init(qb, kb, c_q, c_k, seed + first_instance)
         elif init == "device":
-            rq, rk = device_start_pair(qb, c_q, kb, c_k, seed)
+            from .clustering import device_start_pair
+            rq, rk = device_start_pair(qb, c_q, kb, c_k, seed, first_instance=first_instance)
         else:
             rq, rk = strided_start(qb, c_q), strided_start(kb, c_k)
         q_init = rq if q_init is None else q_init
@@ -196,7 +226,7 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
             mask_entries=torch.zeros((bh,), dtype=torch.int64, device=dev),
             lse=torch.empty((bh, n_q), dtype=f32, device=dev),
         )
-    fn = "svgear_forward_seeded" if seeded is not None else "svgear_forward"
+    fn = "svgear_forward_seeded" if seeded else "svgear_forward"
     capacity = 0 if budget_mode == "perClusterTopP" else entry_capacity(float(budget), n_q * n_k)
 
     def launch(a, b, ws_ptr, ws_bytes, done_event=None):
@@ -208,8 +238,8 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
             if done_event is not None:
                 aux_g.kmeans_done_event = done_event.cuda_event
         head = (row(q_init), row(k_init))
-        if seeded is not None:
-            head = (row(seeded[0]), row(seeded[2]), seeded[1], seeded[3], int(seed) & 0xFFFFFFFF, a) + head
+        if seeded:
+            head = (SEED_OVERSAMPLE, int(seed) & 0xFFFFFFFF, first_instance + a) + head
         shape_g = _lib.Shape(b - a, n_q, n_k, d, c_q, c_k)
         rc = getattr(_lib.lib(), fn)(
             C.byref(shape_g), row(qb), row(kb), row(vb), *head, int(kmeans_iters), _EST[estimator], capacity,

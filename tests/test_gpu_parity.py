@@ -102,7 +102,7 @@ class TestOperatorVsGolden:
     def test_seeded_default_init_matches_reference(self, gcase):
         name, g = gcase
         q, k, v = dev(g["q"]), dev(g["k"]), dev(g["v"])
-        out, mask, aux = P.svg_ear_attention(q, k, v, int(g["c_q"]), int(g["c_k"]), 0.25,
+        out, mask, aux = P.svg_ear_attention(q, k, v, int(g["c_q"]), int(g["c_k"]), 0.25, init="reference",
                                              seed=int(g["seed"]), check_fp32=True, return_aux=True)
         assert np.array_equal(host(aux["q_perm"]), g["q_perm"])
         assert np.array_equal(host(aux["k_perm"]), g["k_perm"])
@@ -472,8 +472,8 @@ class TestConfig1:
         q = dev(np.stack(qs)).unsqueeze(0); k = dev(np.stack(ks)).unsqueeze(0); v = dev(np.stack(vs)).unsqueeze(0)
         results = {}
         for mode in ("fp32", "bf16"):
-            results[mode] = P.svg_ear_attention(q, k, v, cq, ck, rho, seed=0, check_fp32=(mode == "fp32"),
-                                                return_aux=True)
+            results[mode] = P.svg_ear_attention(q, k, v, cq, ck, rho, seed=0, init="reference",
+                                                check_fp32=(mode == "fp32"), return_aux=True)
         for h in range(2):
             ref = O.forward(qs[h], ks[h], vs[h], cq, ck, rho, seed=h)
             for mode, tol in (("fp32", TOL_FP32), ("bf16", TOL_BF16)):
@@ -648,8 +648,8 @@ class TestOperatorTopP:
         S, d, cq, ck = 2048, 64, 16, 40
         qf, kf, vf = (O.round_to_bf16(t) for t in O.blob_instance(S, S, d, cq, ck, 0.1, 3))
         out, mask, aux = P.svg_ear_attention(dev(qf)[None, None], dev(kf)[None, None], dev(vf)[None, None], cq, ck,
-                                             p, budget_mode="perClusterTopP", seed=3, check_fp32=True,
-                                             return_aux=True)
+                                             p, budget_mode="perClusterTopP", seed=3, init="reference",
+                                             check_fp32=True, return_aux=True)
         prep = O.prepare(qf, kf, vf, cq, ck, seed=3)
         assert np.array_equal(host(aux["q_perm"][0, 0]), prep.q_model.permutation)
         assert np.array_equal(host(aux["k_perm"][0, 0]), prep.k_model.permutation)
@@ -696,7 +696,7 @@ class TestRandomShapes:
 
 
 class TestSeededForward:
-    """svgear_forward_seeded = svgear_kmeans_seed_gram per side + svgear_forward, with each side's
+    """svgear_forward_seeded = svgear_kmeans_seed per side + svgear_forward, with each side's
     seeding on the stream of its own Lloyd loop: results must be bit-identical to the two-step path."""
 
     @pytest.mark.parametrize("d,H,S,cq,ck", [(64, 3, 1500, 16, 40), (128, 2, 2304, 20, 64)])
@@ -712,19 +712,37 @@ class TestSeededForward:
             assert torch.equal(aux1["q_perm"], aux2["q_perm"]) and torch.equal(aux1["k_perm"], aux2["k_perm"])
             assert torch.equal(mask1, mask2) and torch.equal(out1, out2)
 
-    def test_c_abi_rejects_bad_subsample_sizes(self):
+    def test_c_abi_rejects_bad_seeding_arguments(self):
         from paper_2603_08982_b200 import _lib
         import ctypes as C
         shape = _lib.Shape(1, 256, 256, 64, 8, 8)
         buf = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
         p = buf.data_ptr()
-        call = lambda mq, mk, g=p: _lib.lib().svgear_forward_seeded(
-            C.byref(shape), p, p, p, g, p, mq, mk, 0, 0, p, p, 5, 0, 100, 0, 1, 0, 0.0, p, p, None, p, buf.numel(), None)
-        assert call(4, 64) == _lib.ESHAPE      # fewer subsample tokens than centres
-        assert call(64, 512) == _lib.ESHAPE    # more than the instance has
-        assert call(64, 64, None) == _lib.EINVAL
-        assert _lib.lib().svgear_forward_seeded(C.byref(shape), p, p, p, p, p, 64, 64, 0, -1, p, p, 5, 0, 100, 0, 1, 0, 0.0, p, p,
-                                                None, p, buf.numel(), None) == _lib.EINVAL
+        call = lambda oversample, first, sh=shape: _lib.lib().svgear_forward_seeded(
+            C.byref(sh), p, p, p, oversample, 0, first, p, p, 5, 0, 100, 0, 1, 0, 0.0, p, p, None, p, buf.numel(), None)
+        assert call(0, 0) == _lib.EINVAL       # no subsample
+        assert call(9, 0) == _lib.EINVAL       # more than the workspace is sized for
+        assert call(8, -1) == _lib.EINVAL      # negative instance index
+        # the standalone seeding entry checks its own workspace
+        assert _lib.lib().svgear_kmeans_seed(1, 256, 64, 8, p, 8, 0, 0, p, p, 16, None) == _lib.EWORKSPACE
+
+    def test_seeding_is_keyed_by_the_global_instance_index(self):
+        """A head shard (head_offset, total_heads) reproduces the unsplit call bit for bit, for B = 1
+        and for B = 2 (seeds per global (batch, head) index)."""
+        S, d, cq, ck, H = 1200, 64, 10, 24, 4
+        rng = np.random.default_rng(11)
+        q, k, v = (dev(O.round_to_bf16(rng.normal(size=(2, H, S, d)))) for _ in range(3))
+        for init in ("device", "reference"):
+            full = P.svg_ear_attention(q, k, v, cq, ck, 0.3, seed=5, init=init, return_aux=True)
+            for lo, hi in ((0, 1), (1, 4)):
+                part = P.svg_ear_attention(q[:, lo:hi], k[:, lo:hi], v[:, lo:hi], cq, ck, 0.3, seed=5, init=init,
+                                           return_aux=True, head_offset=lo, total_heads=H)
+                assert torch.equal(part[2]["q_init"], full[2]["q_init"][:, lo:hi]), (init, lo, hi)
+                assert torch.equal(part[2]["k_perm"], full[2]["k_perm"][:, lo:hi])
+                assert torch.equal(part[1], full[1][:, lo:hi]) and torch.equal(part[0], full[0][:, lo:hi])
+            one = P.svg_ear_attention(q[:1, 1:3], k[:1, 1:3], v[:1, 1:3], cq, ck, 0.3, seed=5, init=init,
+                                      head_offset=1, total_heads=H)
+            assert torch.equal(one[0], full[0][:1, 1:3])
 
 
 class TestHeadGroups:

@@ -30,7 +30,7 @@ class TestCAbi:
 
     def test_version_and_strerror(self):
         lib = P.load_library()
-        assert lib.svgear_version() == 100
+        assert lib.svgear_version() == 110
         assert lib.svgear_strerror(0) == b"ok"
         assert b"workspace" in lib.svgear_strerror(_lib.EWORKSPACE)
 
@@ -97,10 +97,18 @@ class TestHeadGroupLayout:
         p = C.addressof(buf)
         shape = _lib.Shape(1, 256, 256, 64, 8, 8)
         tail = (5, 0, 100, 0, 1, 0, 0.0, p, p, None, p, 4096, None)
-        assert lib.svgear_forward_seeded(C.byref(shape), p, p, p, None, p, 64, 64, 0, 0, p, p, *tail) == _lib.EINVAL
-        assert lib.svgear_forward_seeded(C.byref(shape), p, p, p, p, p, 64, 64, 0, -1, p, p, *tail) == _lib.EINVAL
-        assert lib.svgear_forward_seeded(C.byref(shape), p, p, p, p, p, 4, 64, 0, 0, p, p, *tail) == _lib.ESHAPE
-        assert lib.svgear_forward_seeded(C.byref(shape), p, p, p, p, p, 64, 8192, 0, 0, p, p, *tail) == _lib.ESHAPE
+        fwd = lambda oversample, first, sh=shape: lib.svgear_forward_seeded(C.byref(sh), p, p, p, oversample, 0, first,
+                                                                            p, p, *tail)
+        assert fwd(0, 0) == _lib.EINVAL     # no subsample
+        assert fwd(9, 0) == _lib.EINVAL     # beyond what the workspace is sized for
+        assert fwd(8, -1) == _lib.EINVAL    # negative instance index
+        assert lib.svgear_forward_seeded(None, p, p, p, 8, 0, 0, p, p, *tail) == _lib.EINVAL
+        bad = _lib.Shape(1, 256, 256, 96, 8, 8)
+        assert fwd(8, 0, bad) == _lib.ESHAPE
+        # standalone seeding: argument checks come before any device work
+        assert lib.svgear_kmeans_seed(1, 256, 64, 8, None, 8, 0, 0, p, p, 4096, None) == _lib.EINVAL
+        assert lib.svgear_kmeans_seed(1, 256, 64, 8, p, 0, 0, 0, p, p, 4096, None) == _lib.EINVAL
+        assert lib.svgear_kmeans_seed(1, 256, 64, 300, p, 8, 0, 0, p, p, 4096, None) == _lib.ESHAPE
 
 
 class TestValidationMirrorsReference:

@@ -1,4 +1,4 @@
-"""Times the device-side k-means++ seeding alone (svgear_kmeans_seed_gram through clustering.device_start)
+"""Times the device-side k-means++ seeding alone (svgear_kmeans_seed through clustering.device_start)
 at the Wan2.2 shape, key side (1000 centres) and query side (300 centres)."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -17,3 +17,9 @@ for name, x, c in (("key_side_1000", k[0], ck), ("query_side_300", q[0], cq)):
     e1.record(); torch.cuda.synchronize()
     out[name] = round(e0.elapsed_time(e1) / 10, 4)
 print(json.dumps(out))
+from torch.profiler import profile, ProfilerActivity
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    device_start(k[0], ck); device_start(q[0], cq); torch.cuda.synchronize()
+for e in prof.events():
+    if e.device_type == torch.autograd.DeviceType.CUDA:
+        print(f"{e.device_time / 1e3:8.3f} ms  {e.name[:90]}")
