@@ -175,6 +175,15 @@ int svgear_route_score(const SvgEarShape* shape, const float* q_centroids,
                        int64_t capacity_entries, int32_t overshoot, uint8_t* mask,
                        int64_t* entries, void* workspace, size_t workspace_bytes, void* stream);
 
+/* The top-p baseline as a routing policy of its own — router.score_top_p (router.py:209-236): row i
+ * selects the minimal set of key clusters, in descending softmax mass (ties to the lower index),
+ * whose cumulative mass reaches p; p = 1 selects every block.
+ *   mask [bh][c_q][c_k] u8      entries [bh] i64 (may be NULL)      workspace >= bh*c_q*c_k*8 bytes */
+int svgear_route_score_top_p(const SvgEarShape* shape, const float* q_centroids,
+                             const float* k_centroids, const int32_t* q_sizes, const int32_t* k_sizes,
+                             double p, uint8_t* mask, int64_t* entries, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
 /* Error-aware routing under the per-query-cluster top-p budget — router.route_error_aware with
  * DensityBudget.top_p(p) (router.py:172-190): row i may spend the entries of the minimal set of
  * key clusters whose softmax mass (q̄.k̄/sqrt(d) + ln|k_c|, router.py:193-250) reaches p; inside

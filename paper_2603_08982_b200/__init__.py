@@ -21,7 +21,7 @@ from .estimator import (BlockErrorTable, estimate_errors, estimate_errors_stream
 from .operator import operator_workspace_bytes, reference_init, svg_ear_attention
 from .router import (FILL_REMAINDER, STOP_AT_FIRST_OVERFLOW, BlockMask, DensityBudget,
                      entry_capacity, mask_from_selected, relaxed_objective, route_error_aware,
-                     route_error_aware_entries, route_score)
+                     route_error_aware_entries, route_score, score_top_p)
 from .sharding import gather_heads, head_range, sharded_svg_ear_attention
 from .schedule import SvgEarStack, WarmupSchedule
 from .dit import SvgEarSelfAttention, heads_to_tokens, qkv_prologue, rope_table_3d

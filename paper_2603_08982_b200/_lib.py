@@ -63,6 +63,7 @@ SIGNATURES = {
     "svgear_error_table": ([C.POINTER(Shape), _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_route_error_aware": ([_I32, _I32, _I32, _P, _P, _P, _I64, _I32, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_route_score": ([C.POINTER(Shape), _P, _P, _P, _P, _I64, _I32, _P, _P, _P, _SZ, _P], C.c_int),
+    "svgear_route_score_top_p": ([C.POINTER(Shape), _P, _P, _P, _P, C.c_double, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_route_error_aware_top_p": ([C.POINTER(Shape), _P, _P, _P, _P, _P, C.c_double, _I32, _I32, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_sparse_attend": ([C.POINTER(Shape), _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_forward_seeded": ([C.POINTER(Shape), _P, _P, _P, _I32, C.c_uint32, _I32, _P, _P, _I32, _I32, _I64, _I32, _I32, _I32, C.c_double, _P, _P, C.POINTER(Aux), _P, _SZ, _P], C.c_int),

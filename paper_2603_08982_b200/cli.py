@@ -6,15 +6,16 @@ the reference's config files and QKVT tensor files work unchanged.
     python -m paper_2603_08982_b200 sweep  tensor.qkvt --config cfg.json --density-grid 0.1,0.25,0.5
     python -m paper_2603_08982_b200 verify tensor.qkvt --config cfg.json
 
-Same records (JSON keys, CSV header, cell order) and exit codes as the reference: 0 success,
+Same records (JSON keys, CSV header, cell order; plus one extra key, "executor", naming the GPU
+executor that produced the record) and exit codes as the reference: 0 success,
 1 failed verification, 2 configuration error, 3 unreadable / malformed input or unwritable output,
 4 instance beyond a capability limit.  What differs, by design of this path:
   * inputs are rounded to bf16 on ingest; the executor is the tcgen05 bf16 kernel (`--executor
     bf16`, default) or the fp32 check kernel (`--executor fp32`); the config's `precision` key is
     accepted and echoed but both of its values map to a GPU executor;
-  * policies on the GPU: errorAwareCompensated (both budget modes) and topPCompensated (global
-    density).  topPDrop, random, oracleKnapsack and topPCompensated under perClusterTopP are
-    analysis baselines outside the hot path -> exit code 4; so is a head dimension other than 64/128;
+  * policies on the GPU: errorAwareCompensated and topPCompensated (both budget modes).  topPDrop,
+    random and oracleKnapsack are analysis baselines outside the hot path -> exit code 4; so is a
+    head dimension other than 64/128;
   * the dense comparison (mapMse, outputMse) is evaluated on the device in float64 with torch — it
     is the harness's yardstick, not part of the operator.  `gen` is not provided.
 There is no CPU path: without a CUDA device every subcommand fails (exit code 4).
@@ -32,13 +33,14 @@ import time
 
 import torch
 
+from . import _lib
 from ._lib import SvgEarError
 from ._tensors import ShapeError
 from .analysis import build_error_table, prepare
 from .attention import sparse_attend
 from .config import GPU_POLICIES, POLICIES, ConfigError, RunConfig, apply_preset
 from .estimator import estimate_errors_streaming
-from .router import DensityBudget, relaxed_objective, route_error_aware, route_score
+from .router import DensityBudget, relaxed_objective, route_error_aware, route_score, score_top_p
 from .tensorio import TensorFormatError, read_tensor_file
 
 DENSE_COMPARE_MAX_ENTRIES = 4_194_304  # cli.py:59
@@ -89,8 +91,6 @@ def _check_capability(q, k, v, policies, budget_mode):
     for pol in policies:
         if pol not in GPU_POLICIES:
             raise CapabilityError(f"policy {pol!r} is an analysis baseline outside the GPU hot path")
-        if pol == "topPCompensated" and budget_mode == "perClusterTopP":
-            raise CapabilityError("topPCompensated under perClusterTopP (score_top_p) is not on the GPU path")
 
 
 def _budget(cfg: RunConfig) -> DensityBudget:
@@ -101,8 +101,11 @@ def _mask_for(policy, budget, prep, table):
     if policy == "errorAwareCompensated":  # cli.py:89-95
         return route_error_aware(table, budget, q_centroids=prep.q_model.centroids,
                                  k_centroids=prep.k_model.centroids)
+    if budget.mode == "perClusterTopP":  # cli.py:96-104: the top-p rule itself is the mask
+        return score_top_p(prep.q_model.centroids, prep.k_model.centroids, prep.q_model.sizes,
+                           prep.k_model.sizes, budget.p)
     return route_score(prep.q_model.centroids, prep.k_model.centroids, prep.q_model.sizes,
-                       prep.k_model.sizes, budget)  # cli.py:96-104
+                       prep.k_model.sizes, budget)
 
 
 class _Dense:
@@ -301,8 +304,12 @@ _EXIT_CODES = (
     (ConfigError, "config error", 2),
     ((TensorFormatError, ShapeError), "input error", 3),
     (OSError, "io error", 3),
-    ((CapabilityError, SvgEarError), "capability error", 4),
+    (CapabilityError, "capability error", 4),
 )
+# libsvgear statuses that ARE capability limits (shape / policy the kernels do not implement, or no
+# device at all); the others (bad argument, workspace, a failed CUDA call on a working device) are
+# bugs or runtime faults and propagate with a traceback instead of being reported as a limit
+_CAPABILITY_STATUSES = (_lib.ESHAPE, _lib.EUNSUPPORTED)
 
 
 def build_parser() -> argparse.ArgumentParser:
@@ -322,6 +329,9 @@ def main(argv=None) -> int:
     try:
         return handler(args)
     except Exception as exc:  # noqa: BLE001 - mapped to the documented exit codes, anything else propagates
+        if isinstance(exc, SvgEarError) and exc.status in _CAPABILITY_STATUSES:
+            print(f"capability error: {exc}", file=sys.stderr)
+            return 4
         for kinds, label, code in _EXIT_CODES:
             if isinstance(exc, kinds):
                 print(f"{label}: {exc}", file=sys.stderr)

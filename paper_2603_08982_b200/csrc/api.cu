@@ -321,6 +321,22 @@ int svgear_route_error_aware_top_p(const SvgEarShape* shape, const double* error
                             single_item_fallback ? 1 : 0, mask, entries, st);
 }
 
+int svgear_route_score_top_p(const SvgEarShape* shape, const float* q_centroids, const float* k_centroids,
+                             const int32_t* q_sizes, const int32_t* k_sizes, double p, uint8_t* mask,
+                             int64_t* entries, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!shape || !q_centroids || !k_centroids || !q_sizes || !k_sizes || !mask || !workspace) return SVGEAR_EINVAL;
+  if (!(p > 0.0 && p <= 1.0)) return SVGEAR_EINVAL;
+  if (!shape_ok(shape)) return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  Carver cv(workspace, workspace_bytes);
+  double* mass = cv.take<double>((size_t)shape->bh * shape->c_q * shape->c_k);
+  if (!cv.ok) return SVGEAR_EWORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = launch_score_mass(*shape, q_centroids, k_centroids, k_sizes, mass, st);
+  if (rc != SVGEAR_OK) return rc;
+  return launch_route_top_p(*shape, nullptr, mass, q_sizes, k_sizes, p, SVGEAR_FILL_REMAINDER, 0, mask, entries, st);
+}
+
 int svgear_sparse_attend(const SvgEarShape* shape, int32_t exec_mode, const void* q_permuted,
                          const void* k_permuted, const void* v_permuted, const int32_t* q_perm,
                          const int32_t* q_sizes, const int32_t* q_offsets, const int32_t* k_sizes,

@@ -814,10 +814,21 @@ __global__ void __launch_bounds__(256)
       }
       const int last = min(cut, c_k - 1);
       for (int r = 0; r <= last; ++r) cap += qs * ks[keys[r].idx];
+      s_single = last;
     }
     s_cap = cap;
+    s_single = min(c_k - 1, p >= 1.0 ? c_k - 1 : s_single);
   }
   __syncthreads();
+  if (err == nullptr) {
+    // score_top_p as a policy of its own (router.py:209-236): the prefix itself is the mask
+    const int last = s_single;
+    for (int j = tid; j < c_k; j += 256) out[j] = 0;
+    __syncthreads();
+    for (int r = tid; r <= last; r += 256) out[keys[r].idx] = 1;
+    if (tid == 0 && entries) atomicAdd(&entries[h], (unsigned long long)s_cap);
+    return;
+  }
   // ---- (2) row order (-ratio, -error, index) (estimator.py:83-96 restricted to the row) ------------
   for (int j = tid; j < npad; j += 256) {
     TopPKey k;

@@ -174,5 +174,35 @@ def route_score(q_centroids, k_centroids, q_sizes, k_sizes, budget: DensityBudge
     return _finish(mask, entries, n_q * n_k, was_2d)
 
 
+def score_top_p(q_centroids, k_centroids, q_sizes, k_sizes, p: float, *, size_weighted: bool = True) -> BlockMask:
+    """Per-row minimal prefix of cluster mass reaching cumulative p (router.py:209-236): each
+    query-cluster row softmaxes q̄·k̄/sqrt(d) + ln|k_c|; blocks are taken in descending mass order
+    (ties to the lower key-cluster index) until the cumulative mass reaches p; p = 1 selects all."""
+    if not (0.0 < p <= 1.0):
+        raise ValueError(f"p must be in (0, 1], got {p}")
+    if not size_weighted:
+        raise NotImplementedError("only size-weighted scores run on the GPU path")
+    dev = require_cuda()
+    qc = torch.as_tensor(q_centroids).to(dev, torch.float32).contiguous()
+    kc = torch.as_tensor(k_centroids).to(dev, torch.float32).contiguous()
+    was_2d = qc.ndim == 2
+    if was_2d:
+        qc, kc = qc.unsqueeze(0), kc.unsqueeze(0)
+    bh, c_q, d = qc.shape
+    c_k = kc.shape[1]
+    qs = torch.as_tensor(q_sizes).to(dev, torch.int32).view(bh, c_q).contiguous()
+    ks = torch.as_tensor(k_sizes).to(dev, torch.int32).view(bh, c_k).contiguous()
+    n_q, n_k = int(qs[0].long().sum()), int(ks[0].long().sum())
+    shape = _lib.Shape(bh, n_q, n_k, d, c_q, c_k)
+    mask = torch.empty((bh, c_q, c_k), dtype=torch.uint8, device=dev)
+    entries = torch.empty((bh,), dtype=torch.int64, device=dev)
+    ws = workspace(bh * c_q * c_k * 8 + 1024, dev)
+    rc = _lib.lib().svgear_route_score_top_p(
+        C.byref(shape), qc.data_ptr(), kc.data_ptr(), qs.data_ptr(), ks.data_ptr(), float(p), mask.data_ptr(),
+        entries.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr())
+    _lib.check("svgear_route_score_top_p", rc)
+    return _finish(mask, entries, n_q * n_k, was_2d)
+
+
 def relaxed_objective(table: BlockErrorTable, mask: BlockMask) -> float:  # router.py:297-299
     return float(table.error_sum[~mask.selected].sum())

@@ -86,6 +86,11 @@ class SvgEarStack:
     order).  Sparse calls start k-means from the layer's previous centroids when `warm_start` is
     on and the previous sparse call of that layer was step-1 with the same shape; otherwise they
     seed on the device (`init`) and run up to `cold_iters` Lloyd iterations.
+
+    Classifier-free guidance runs every layer twice per step (conditional and unconditional
+    branch): pass `branch=0` / `branch=1` so that each branch keeps its own centroid cache and
+    warm-starts from ITS previous step (one cache per (layer, branch); a single cache would see
+    the second call of a step as "not step-1" and fall back to a cold start every time).
     """
 
     n_q_clusters: int
@@ -107,17 +112,21 @@ class SvgEarStack:
         if self.cold_iters < 1 or self.warm_iters < 1:
             raise ValueError(f"max_iters must be >= 1, got {min(self.cold_iters, self.warm_iters)}")
 
-    def reset(self):
-        """Forget every layer's centroids (start of a new denoising run)."""
+    def reset(self, release_workspace=False):
+        """Forget every layer's centroids (start of a new denoising run); optionally also drop the
+        cached workspace buffer."""
         self._layers.clear()
         self.calls = {"dense": 0, "cold": 0, "warm": 0}
+        if release_workspace:
+            self._ws = None
 
-    def plan(self, layer: int, step: int, q=None, k=None) -> str:
+    def plan(self, layer: int, step: int, q=None, k=None, branch: int = 0) -> str:
         """'dense' | 'cold' | 'warm' — what `attend(layer, step, ...)` does now.  A warm start needs
-        the layer's centroids from step - 1 and, when q and k are given, centroids of their shape."""
+        the (layer, branch)'s centroids from step - 1 and, when q and k are given, centroids of their
+        shape."""
         if self.schedule.is_dense(layer, step):
             return "dense"
-        st = self._layers.get(layer)
+        st = self._layers.get((layer, branch))
         if not (self.warm_start and st is not None and st.q_centroids is not None and st.last_step == step - 1):
             return "cold"
         if q is not None and k is not None:
@@ -133,13 +142,13 @@ class SvgEarStack:
             self._ws = torch.empty(need, dtype=torch.uint8, device=device)
         return self._ws
 
-    def attend(self, layer, step, q, k, v, *, return_mask=False):
-        mode = self.plan(layer, step, q, k)
+    def attend(self, layer, step, q, k, v, *, return_mask=False, branch: int = 0):
+        mode = self.plan(layer, step, q, k, branch)
         self.calls[mode] += 1
         if mode == "dense":
             out = torch.nn.functional.scaled_dot_product_attention(q, k, v)
             return (out, None) if return_mask else out
-        st = self._layers.setdefault(layer, _LayerState())
+        st = self._layers.setdefault((layer, branch), _LayerState())
         if mode == "warm":
             kw = dict(q_init=st.q_centroids, k_init=st.k_centroids, kmeans_iters=self.warm_iters)
         else:
@@ -157,7 +166,7 @@ class SvgEarStack:
         st.last_step = step
         return (out, mask) if return_mask else out
 
-    def lloyd_iterations(self, layer):
-        """(query-side, key-side) Lloyd iteration counts [bh] of the layer's last sparse call."""
-        st = self._layers.get(layer)
+    def lloyd_iterations(self, layer, branch: int = 0):
+        """(query-side, key-side) Lloyd iteration counts [bh] of the (layer, branch)'s last sparse call."""
+        st = self._layers.get((layer, branch))
         return (None, None) if st is None else (st.q_iters, st.k_iters)

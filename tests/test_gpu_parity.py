@@ -297,6 +297,21 @@ class TestRouter:
             else:
                 assert mm == 0.0, (name, p, mm)
 
+    def test_score_top_p_policy_matches_reference(self, gcase):  # router.py:209-236
+        name, g = gcase
+        for p in (0.5, 0.85, 1.0):
+            m = P.score_top_p(g["q_centroids"], g["k_centroids"], g["q_sizes"], g["k_sizes"], p)
+            want = g[f"mask_scoretopp_{tag(p)}"]
+            mm = float((host(m.selected) != want).mean())
+            if name == "dups_d64":   # exactly tied masses: report the rate, bound it
+                assert mm <= 0.25, (name, p, mm)
+            else:
+                assert mm == 0.0, (name, p, mm)
+                sizes = np.outer(g["q_sizes"], g["k_sizes"])
+                assert m.density_entries == int((want * sizes).sum())
+        with pytest.raises(ValueError):
+            P.score_top_p(g["q_centroids"], g["k_centroids"], g["q_sizes"], g["k_sizes"], 0.0)
+
     def test_top_p_large_table_against_oracle(self):
         rng = np.random.default_rng(12)
         cq, ck, d = 60, 1000, 64
@@ -487,6 +502,24 @@ class TestConfig1:
                       f" (oracle {ref.prep.q_model.iters}/{ref.prep.k_model.iters})")
                 # fp ties: a handful of borderline tokens/blocks at most
                 assert qa <= 2e-3 and ka <= 2e-3
+                # Every later stage is checked UNCONDITIONALLY by running the oracle on what the GPU
+                # produced upstream: the oracle's estimator + router on the GPU's clustering (mask
+                # ties are reported as a rate), then the oracle's executor on the GPU's own mask.
+                qh, kh, vh = qs[h], ks[h], vs[h]
+                qm = O.cluster_model(qh, host(aux["q_assign"][0, h]).astype(np.int64), cq)
+                km = O.cluster_model(kh, host(aux["k_assign"][0, h]).astype(np.int64), ck)
+                assert np.array_equal(host(aux["q_perm"][0, h]), qm.permutation)
+                assert np.array_equal(host(aux["k_perm"][0, h]), km.permutation)
+                from types import SimpleNamespace
+                prep = SimpleNamespace(q_raw=qh, k_raw=kh, v_raw=vh, q_model=qm, k_model=km,
+                                       q=qh[qm.permutation], k=kh[km.permutation], v=vh[km.permutation])
+                want_mask = O.route_error_aware(O.build_error_table(prep, "valueAware"), rho).selected
+                got_mask = host(mask[0, h])
+                mm_given_clusters = float((got_mask != want_mask).mean())
+                assert mm_given_clusters <= 2e-3, mm_given_clusters
+                o_out, _ = O.sparse_attend(prep.q, prep.k, prep.v, qm, km, got_mask)
+                err_given_mask = rel_l2(host(out[0, h].float()), O.unpermute(o_out, qm))
+                assert err_given_mask <= tol, (mode, err_given_mask)
                 if qa == 0.0 and ka == 0.0:
                     assert mm <= 2e-3
                     if mm == 0.0:
@@ -527,6 +560,52 @@ class TestPropertiesAtScale:
             assert bool((aux["mask_entries"] <= cap).all())
             assert bool((aux["mask_entries"] >= 0.97 * cap).all())
             assert bool(torch.isfinite(out.float()).all())
+
+
+class TestBenchedShapes:
+    """One head at the shapes bench.py reports (BASELINE configs 2 and 3): the oracle is far too slow
+    there, so the checks are the size-independent ones — rho = 1 equals dense attention, the bf16
+    tensor-core executor agrees with the fp32 check executor on the same mask, the bounded Lloyd loop
+    equals the full evaluation, the budget is met, the permutation is a stable bijection."""
+
+    @pytest.mark.parametrize("S,cq,ck", [(75600, 300, 1000), (119056, 400, 1000)])
+    def test_one_head_at_the_benched_shape(self, S, cq, ck):
+        import bench
+        from paper_2603_08982_b200.clustering import ClusterModel, run_lloyd
+        d, rho = 128, 0.25
+        q, k, v = bench.make_heads(torch, 0, 1, S, d, cq, ck, 0.1, torch.device("cuda", 0), "ragged")
+        # (1) the operator at rho = 1 is dense attention
+        out, mask = P.svg_ear_attention(q, k, v, cq, ck, 1.0, kmeans_iters=6)
+        assert bool(mask.all())
+        dense = torch.nn.functional.scaled_dot_product_attention(q, k, v)
+        assert rel_l2(host(out.float()), host(dense.float())) <= TOL_BF16
+        del out, dense
+        # (2) staged path at rho = 0.25: clustering invariants, bounded == full evaluation
+        qi, ki = P.device_start(q[0], cq, seed=0), P.device_start(k[0], ck, seed=1)
+        rq, rk = run_lloyd(q[0], qi, 6), run_lloyd(k[0], ki, 6)
+        rk_full = run_lloyd(k[0], ki, 6, full_eval=True)
+        for name in ("assign", "perm", "sizes", "offsets", "centroids", "iters"):
+            assert torch.equal(rk[name], rk_full[name]), name
+        for r, c in ((rq, cq), (rk, ck)):
+            perm = r["perm"].long()
+            assert torch.equal(torch.sort(perm, dim=-1).values, torch.arange(S, device="cuda").expand(1, S))
+            assert bool((r["sizes"] >= 1).all()) and int(r["sizes"].sum()) == S
+            lab = torch.gather(r["assign"].long(), -1, perm)
+            same = lab[..., 1:] == lab[..., :-1]
+            assert bool((lab[..., 1:] >= lab[..., :-1]).all())
+            assert bool((perm[..., 1:][same] > perm[..., :-1][same]).all())
+        qm = ClusterModel(cq, rq["assign"], rq["centroids"], rq["sizes"], rq["perm"], rq["offsets"])
+        km = ClusterModel(ck, rk["assign"], rk["centroids"], rk["sizes"], rk["perm"], rk["offsets"])
+        qp, kp, vp = P.permute_rows(q[0], qm), P.permute_rows(k[0], km), P.permute_rows(v[0], km)
+        table = P.estimate_errors_streaming(qm, km, kp, vp)
+        m = P.route_error_aware(table, P.DensityBudget.global_density(rho))
+        cap = P.entry_capacity(rho, S * S)
+        assert bool((m.density_entries <= cap).all()) and bool((m.density_entries >= 0.97 * cap).all())
+        # (3) bf16 tcgen05 executor against the fp32 CUDA-core executor on the same mask
+        r16 = P.sparse_attend(qp, kp, vp, qm, km, m, dtype=torch.bfloat16, unpermute=True)
+        r32 = P.sparse_attend(qp, kp, vp, qm, km, m, dtype=torch.float32, unpermute=True)
+        assert rel_l2(host(r16.output.float()), host(r32.output)) <= TOL_BF16
+        assert r16.flops.exact_block == r32.flops.exact_block == 4 * d * int(m.density_entries.sum())
 
 
 class TestDeviceSeeding:

@@ -206,7 +206,7 @@ class TestStackWarmStart:
                        .unsqueeze(0) for i in range(3))
             assert stack.plan(0, t) == ("cold" if t == 0 else "warm")
             out, mask = stack.attend(0, t, q, k, v, return_mask=True)
-            st = stack._layers[0]
+            st = stack._layers[(0, 0)]
             for h in range(H):
                 if t == 0:
                     ref = O.forward(*data[h][t], cq, ck, rho, seed=h)
@@ -245,6 +245,25 @@ class TestStackWarmStart:
                     assert plan == ("cold" if t in (1, 3) else "warm")
         stack.reset()
         assert stack.plan(1, 2) == "cold"
+
+    def test_cfg_branches_keep_their_own_centroid_cache(self):
+        """Classifier-free guidance calls every layer twice per step: each branch warm-starts from its
+        own previous step (one cache per layer made the second call of a step cold)."""
+        S, d, cq, ck, H = 512, 64, 8, 12, 2
+        data = _drifted_instances(S, d, cq, ck, 3, H)
+        other = _drifted_instances(S, d, cq, ck, 3, H, seed=77) if "seed" in _drifted_instances.__code__.co_varnames \
+            else [[tuple(np.ascontiguousarray(a[::-1]) for a in step) for step in head] for head in data]
+        stack = schedule.SvgEarStack(cq, ck, 0.25, schedule=schedule.WarmupSchedule.none(3, 1))
+        solo = schedule.SvgEarStack(cq, ck, 0.25, schedule=schedule.WarmupSchedule.none(3, 1))
+        for t in range(3):
+            for branch, src in ((0, data), (1, other)):
+                q, k, v = (torch.from_numpy(np.stack([src[h][t][i] for h in range(H)])).to("cuda", torch.bfloat16)
+                           .unsqueeze(0) for i in range(3))
+                assert stack.plan(0, t, branch=branch) == ("cold" if t == 0 else "warm")
+                out = stack.attend(0, t, q, k, v, branch=branch)
+                if branch == 0:  # the conditional branch is unaffected by the other branch's calls
+                    assert torch.equal(out, solo.attend(0, t, q, k, v))
+        assert stack.calls == {"dense": 0, "cold": 2, "warm": 4}
 
 
 @pytest.mark.gpu
