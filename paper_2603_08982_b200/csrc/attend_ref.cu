@@ -14,43 +14,53 @@ namespace svg {
 // ------------------------------------------------------------------------------------------------
 // q-row tiles that do not cross a query-cluster boundary: (cluster, first row, rows)
 // ------------------------------------------------------------------------------------------------
+// split_rows > 0 (tensor-core executor): tiles with more than split_rows rows fill the list from the
+// front (tile_count[h] of them), the others — at most one per query cluster — from the back
+// (tile_count[bh + h] of them, entry r at index max_tiles - 1 - r), so that each of the two executor
+// kernels launches over its own compact list.  split_rows == 0: one list, tile_count[h] entries.
 __global__ void __launch_bounds__(1024)
-    build_tiles_kernel(int c_q, int rows_per_tile, int max_tiles, const int32_t* __restrict__ q_sizes,
+    build_tiles_kernel(int c_q, int rows_per_tile, int max_tiles, int split_rows, const int32_t* __restrict__ q_sizes,
                        const int32_t* __restrict__ q_offsets, int32_t* __restrict__ tile_list,
                        int32_t* __restrict__ tile_count) {
   const int h = blockIdx.x;
-  __shared__ int s_warp[32];
-  __shared__ int s_carry;
+  __shared__ int s_warp[2][32];
+  __shared__ int s_carry[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_carry = 0;
+  if (tid < 2) s_carry[tid] = 0;
   __syncthreads();
   for (int base = 0; base < c_q; base += 1024) {
     const int i = base + tid;
     const int nq = i < c_q ? q_sizes[(size_t)h * c_q + i] : 0;
     const int nt = ceil_div(nq, rows_per_tile);
-    int inc = nt;
+    const int last_rows = nq - (nt - 1) * rows_per_tile;
+    const int nback = (split_rows > 0 && nt > 0 && last_rows <= split_rows) ? 1 : 0;
+    const int nfront = nt - nback;
+    int inc0 = nfront, inc1 = nback;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
+      const int y0 = __shfl_up_sync(0xffffffffu, inc0, o), y1 = __shfl_up_sync(0xffffffffu, inc1, o);
+      if (lane >= o) { inc0 += y0; inc1 += y1; }
     }
-    if (lane == 31) s_warp[warp] = inc;
+    if (lane == 31) { s_warp[0][warp] = inc0; s_warp[1][warp] = inc1; }
     __syncthreads();
-    if (warp == 0) {
-      int w = s_warp[lane], wi = w;
+    if (warp < 2) {
+      int w = s_warp[warp][lane], wi = w;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, wi, o);
+        const int y = __shfl_up_sync(0xffffffffu, wi, o);
         if (lane >= o) wi += y;
       }
-      s_warp[lane] = wi - w;
+      s_warp[warp][lane] = wi - w;
     }
     __syncthreads();
-    int pos = s_carry + s_warp[warp] + inc - nt;
+    const int pos0 = s_carry[0] + s_warp[0][warp] + inc0 - nfront;
+    const int pos1 = s_carry[1] + s_warp[1][warp] + inc1 - nback;
     if (i < c_q) {
       const int o = q_offsets[(size_t)h * c_q + i];
       for (int t = 0; t < nt; ++t) {
-        int32_t* e = tile_list + ((size_t)h * max_tiles + pos + t) * 4;
+        const bool back = nback && t == nt - 1;
+        const int slot = back ? max_tiles - 1 - pos1 : pos0 + t;
+        int32_t* e = tile_list + ((size_t)h * max_tiles + slot) * 4;
         e[0] = i;
         e[1] = o + t * rows_per_tile;
         e[2] = min(rows_per_tile, nq - t * rows_per_tile);
@@ -58,10 +68,13 @@ __global__ void __launch_bounds__(1024)
       }
     }
     __syncthreads();
-    if (tid == 1023) s_carry = pos + nt;
+    if (tid == 1023) { s_carry[0] = pos0 + nfront; s_carry[1] = pos1 + nback; }
     __syncthreads();
   }
-  if (tid == 0) tile_count[h] = s_carry;
+  if (tid == 0) {
+    tile_count[h] = s_carry[0];
+    tile_count[gridDim.x + h] = s_carry[1];
+  }
 }
 
 // bf16 copies of the key/value centroids (zero-padded to a multiple of 64 rows) and ln|k_c|
@@ -212,7 +225,7 @@ size_t AttendScratch::bytes(const SvgEarShape& s) {
   const int mt = max_tiles(s.n_q, s.c_q, 16);
   size_t b = 0;
   b += align_up((size_t)s.bh * mt * 4 * 4, 256);
-  b += align_up((size_t)s.bh * 4, 256);
+  b += align_up((size_t)s.bh * 8, 256);
   b += align_up((size_t)s.bh * ckpad * s.d * 2, 256) * 2;
   b += align_up((size_t)s.bh * s.c_k * 4, 256);
   return b + 2048;
@@ -222,7 +235,7 @@ bool AttendScratch::carve(Carver& cv, const SvgEarShape& s) {
   const int ckpad = ceil_div(s.c_k, 64) * 64 + 64;
   const int mt = max_tiles(s.n_q, s.c_q, 16);
   tile_list = cv.take<int32_t>((size_t)s.bh * mt * 4);
-  tile_count = cv.take<int32_t>(s.bh);
+  tile_count = cv.take<int32_t>((size_t)2 * s.bh);  // [front counts | back counts]
   kbar_bf16 = cv.take<bf16>((size_t)s.bh * ckpad * s.d);
   vbar_bf16 = cv.take<bf16>((size_t)s.bh * ckpad * s.d);
   lnw = cv.take<float>((size_t)s.bh * s.c_k);
@@ -241,8 +254,8 @@ int launch_attend(const SvgEarShape& s, int exec_mode, const bf16* qp, const bf1
   SVG_LAUNCH_OK();
   const int rows = exec_mode == SVGEAR_EXEC_FP32_CHECK ? 16 : attend_tc_rows_per_tile();
   const int mt = AttendScratch::max_tiles(s.n_q, s.c_q, rows);
-  build_tiles_kernel<<<s.bh, 1024, 0, st>>>(s.c_q, rows, mt, q_sizes, q_offsets, sc.tile_list,
-                                            sc.tile_count);
+  build_tiles_kernel<<<s.bh, 1024, 0, st>>>(s.c_q, rows, mt, exec_mode == SVGEAR_EXEC_FP32_CHECK ? 0 : 128, q_sizes,
+                                            q_offsets, sc.tile_list, sc.tile_count);
   SVG_LAUNCH_OK();
   if (exec_mode == SVGEAR_EXEC_FP32_CHECK) {
     if (s.d == 128)

@@ -94,10 +94,11 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
   constexpr int kTmemCols = 256 * HALVES, kOBase = 128 * HALVES;
   using B = Bars<NS>;
   const int h = blockIdx.y;
-  if ((int)blockIdx.x >= tile_count[h]) return;
-  const int32_t* te = tile_list + ((size_t)h * max_tiles + blockIdx.x) * 4;
+  // two-half tiles fill the tile list from the front, tiles of <= 128 rows from the back (build_tiles_kernel)
+  if ((int)blockIdx.x >= tile_count[(HALVES == 2 ? 0 : gridDim.y) + h]) return;
+  const int slot = HALVES == 2 ? (int)blockIdx.x : max_tiles - 1 - (int)blockIdx.x;
+  const int32_t* te = tile_list + ((size_t)h * max_tiles + slot) * 4;
   const int qcl = te[0], row0 = te[1], nrows = te[2];
-  if ((nrows > 128) != (HALVES == 2)) return;  // the other instantiation owns this tile
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
       const float* bias = s_bias + (kind == 2 ? (t - n_exact) * BN : 0);
       const float mu = (m == -INFINITY) ? 0.f : m;
       float sum0 = 0.f, sum1 = 0.f, sum2 = 0.f, sum3 = 0.f;
-      float x0 = -INFINITY, x1 = -INFINITY, x2 = -INFINITY, x3 = -INFINITY;  // block maxima (log2 domain)
+      float x2 = -INFINITY, x3 = -INFINITY;  // block maxima of the biased tiles (log2 domain)
       tc_wait_ld();                 // sa = columns 0-31 of tile t
       TMEM_LD32(tS + 32, sb);       // columns 32-63 load under the arithmetic on sa
       auto block = [&](uint32_t(&v)[32], int col0, int pk0) {
@@ -328,10 +329,6 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
             float vv[8], p[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) vv[e] = __uint_as_float(v[j + e]);
-            x0 = fmaxf(x0, fmaxf(vv[0], vv[1]));
-            x1 = fmaxf(x1, fmaxf(vv[2], vv[3]));
-            x0 = fmaxf(x0, fmaxf(vv[4], vv[5]));
-            x1 = fmaxf(x1, fmaxf(vv[6], vv[7]));
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const uint64_t xx = ffma2(pack2(vv[2 * q], vv[2 * q + 1]), sc2, nm2);
@@ -387,20 +384,38 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
         fetched = true;
       }
       block(sb, 32, 16);
-      float mt = kind == 0 ? fmaxf(x0, x1) * scale_log2e : fmaxf(x2, x3);
       float sum = (sum0 + sum1) + (sum2 + sum3);
-      // lazy running max: only move it when it grows by more than 2^kRescaleThreshold
+      // Lazy running max: m only moves when a logit exceeds it by more than 2^kRescaleThreshold.  Full
+      // exact tiles do not track their maximum (one FMNMX per logit on the softmax warps' critical
+      // path): while every logit stays below m + 8 the 64 exponentials sum to at most 2^14, so a larger
+      // (or non-finite) row sum is the trigger, and the tile maximum is taken on the redo path only.
+      // Untriggered tiles may hold logits up to m + 14: harmless for fp32 sums and bf16 P.
       float alpha = 1.f;
-      const bool bump = mt > m + kRescaleThreshold || (m == -INFINITY && mt > -INFINITY);
-      const bool redo = __any_sync(0xffffffffu, bump);
+      const float mt_known = fmaxf(x2, x3);
+      const bool maybe = kind == 0 ? !(sum <= 16384.f) || m == -INFINITY
+                                   : (mt_known > m + kRescaleThreshold || (m == -INFINITY && mt_known > -INFINITY));
+      const bool redo = __any_sync(0xffffffffu, maybe);
       if (redo) {
-        // exact path for the whole warp: raise m where needed and take the exponentials again
+        // exact path for the whole warp: tile maximum, raise m where needed, exponentials again
+        tc_wait_ld();  // keep the prefetched block of tile t+1 intact in sa
+        float mt = mt_known;
+        if (kind == 0) {
+          mt = -INFINITY;
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            TMEM_LD32(tS + half * 32, sb);
+            tc_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) mt = fmaxf(mt, __uint_as_float(sb[j]));
+          }
+          mt *= scale_log2e;
+        }
+        const bool bump = mt > m + kRescaleThreshold || (m == -INFINITY && mt > -INFINITY);
         if (bump) {
           alpha = ex2(m - mt);  // m = -inf -> 0
           m = mt;
         }
         const float mu2 = (m == -INFINITY) ? 0.f : m;
-        tc_wait_ld();  // keep the prefetched block of tile t+1 intact in sa
         sum = 0.f;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
@@ -437,9 +452,8 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
           TMEM_ST32(tO + c, sb);
         }
       }
-      tc_wait_st();
+      tc_wait_st();  // .sync.aligned: every lane's stores have landed when any lane is past this
       tc_fence_before();
-      __syncwarp();
       if (lane == 0) mbar_arrive(bar(b_pfull + st));
       if (!fetched) {
         mbar_wait(bar(b_sfull + (st ^ 1)), ((t + 1) >> 1) & 1);
@@ -533,7 +547,7 @@ static int launch_attend_tc_ns(const SvgEarShape& s, const TmaSet& tm, const int
   // forked onto a helper stream so that its CTAs fill the tail of the first instead of following it.
   const size_t smem1 = Smem<D, NS1, 1>::bytes(ckpad);
   SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
-  attend_tc_kernel<D, NS1, 1><<<dim3(mt, s.bh), threads_for(1), smem1, side>>>(
+  attend_tc_kernel<D, NS1, 1><<<dim3(mt < s.c_q ? mt : s.c_q, s.bh), threads_for(1), smem1, side>>>(
       tm, s.bh * s.n_k, sc.lnw, q_perm, k_sizes, k_offsets, mask, sc.tile_list, sc.tile_count, mt, s.n_q, s.n_k,
       s.c_q, s.c_k, ckpad, scale_log2e, out, lse);
   SVG_LAUNCH_OK();

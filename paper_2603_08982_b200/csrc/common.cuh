@@ -171,7 +171,7 @@ struct ErrScratch {
   float* sbar;    // [bh][c_q][c_k] centroid logits
   bf16* kd_hi;    // [bh][n_k][d]   k - k̄ split into bf16 hi / lo (tensor-core path)
   bf16* kd_lo;
-  float4* kstat;  // [bh][n_k]      (A, 2B, C, -) per key
+  float* kstat;   // [3][bh][n_k]   planes A, -2B, C of the per-key scalars
   bf16* qsplit;   // [bh][2][cqpad][d]
   bool carve(Carver& cv, const SvgEarShape& s);
 };

@@ -11,11 +11,19 @@
 //     (the dropped ql.dl term is 2^-18 relative);
 //   * the epilogue owns one query cluster per thread (TMEM lane) and walks the key columns of a
 //     key cluster in order, so the per-block sum and its running-max rescale stay in registers and
-//     each E[i,j] is written exactly once — no atomics, deterministic.
+//     each E[i,j] is written exactly once — no atomics, deterministic.  The epilogue is the bound of
+//     this kernel (fp32 issue slots), so its common case is written in packed arithmetic: when every
+//     |g| of a chunk is <= 1 (a warp-uniform test on the chunk's largest |g|), expm1 is a degree-8
+//     polynomial and two keys go through each fma.rn.f32x2 with no stabiliser; per-key scalars sit in
+//     shared memory as separate arrays so that neighbouring keys load as register pairs.  Chunks
+//     with larger logits take the scalar path with the running-maximum rescale.
 // CTA = (instance, 128 query clusters, a range of key clusters); key clusters stream through in
 // chunks of <= 128 keys (N = chunk rounded up to 16), two TMEM buffers, two epilogue warp groups.
 //   warps 0-3 / 4-7 : epilogue groups (even / odd key clusters of the range)
-//   warp 8 : producer      warp 9 : TMEM allocator + MMA issuer
+//   warp 8 : producer — q̄ tiles once (cp.async), then ONE elected thread streams the chunks: the
+//            k - k̄ tiles as 16-row TMA boxes (rows of a cluster are contiguous), the per-key scalars as
+//            three bulk copies, all completing on mbarriers, so nothing blocks on a load
+//   warp 9 : TMEM allocator + MMA issuer
 #include "tc_common.cuh"
 
 namespace svg {
@@ -25,17 +33,18 @@ using namespace tc;
 namespace {
 constexpr int EM = 128;       // query clusters per CTA (M)
 constexpr int ECH = 128;      // max keys per chunk
-constexpr int ERANGE = 16;    // key clusters per CTA
-constexpr int ETHREADS = 352;
-enum { EB_AFULL = 0, EB_BFULL = 1, EB_BEMPTY = 3, EB_ACCFULL = 5, EB_ACCEMPTY = 7, EB_STATEMPTY = 9 /* [2 groups][2 buffers] */ };
+constexpr int ERANGE = 48;    // key clusters per CTA
+constexpr int ETHREADS = 320;
+enum { EB_AFULL = 0, EB_BFULL = 1, EB_BEMPTY = 3, EB_ACCFULL = 5, EB_ACCEMPTY = 7, EB_STATEMPTY = 9 /* [2 groups][2 buffers] */,
+       EB_STATFULL = 13 /* [2 groups][2 buffers] */ };
 
 template <int D>
 struct ESmem {
   static constexpr int kTile = EM * D * 2;        // one [128 x d] bf16 tile
   static constexpr int kA = 0;                    // qh, ql
   static constexpr int kB = kA + 2 * kTile;       // 2 stages x (dh, dl)
-  static constexpr int kStat = kB + 4 * kTile;     // 2 stages x 128 keys x float4
-  static constexpr int kBars = kStat + 4 * ECH * 16;  // stats: 2 groups x 2 buffers x 128 keys x float4
+  static constexpr int kStat = kB + 4 * kTile;
+  static constexpr int kBars = kStat + 4 * ECH * 16;  // stats: 2 groups x 2 buffers x (A[128], -2B[128], C[128]) f32
   static constexpr size_t bytes() { return 1024 + kBars + 256; }
 };
 
@@ -49,6 +58,21 @@ struct ESmem {
       : "r"(taddr)                                                                                \
       : "memory")
 
+// Per-key scalars live in three planes (A, -2B, C) of `pstride` floats per instance.  Inside a plane
+// the keys of cluster j start at a 16-byte aligned position pos_j = align4(offset_j) + 4 j, so that a
+// chunk of a cluster is one aligned bulk copy (cp.async.bulk needs 16-byte alignment and size).
+__host__ __device__ __forceinline__ size_t stat_plane_stride(int n_k, int c_k) {
+  return (((size_t)n_k + 3) & ~(size_t)3) + 4 * (size_t)c_k + 8;  // a multiple of 4 floats: planes stay 16-byte aligned
+}
+__device__ __forceinline__ int stat_pos(int offset_j, int j) { return ((offset_j + 3) & ~3) + 4 * j; }
+
+// 1-D bulk copy global -> shared, completes `bytes` on `bar` (16-byte aligned addresses and size)
+__device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
 __device__ __forceinline__ float expm1_fast(float g) {
   // |g| < 0.125: degree-4 Taylor (relative error < 3e-6); otherwise 2^(g log2 e) - 1 (< 1e-6)
   const float poly = g * fmaf(g, fmaf(g, fmaf(g, 1.f / 24.f, 1.f / 6.f), 0.5f), 1.f);
@@ -58,12 +82,13 @@ __device__ __forceinline__ float expm1_fast(float g) {
 }  // namespace
 
 // per key: kd = k - k̄_j as bf16 (hi, lo); (A, B, C) = (|v̄-v|^2, (v̄-v).v, |v|^2)  [plain: 0,0,1]
+// stored as three planes A, -2B, C (layout: stat_plane_stride / stat_pos above)
 template <int D>
 __global__ void __launch_bounds__(128)
     key_stats_kernel(int mode, const float* __restrict__ kc, const float* __restrict__ vc,
                      const bf16* __restrict__ kp, const bf16* __restrict__ vp,
                      const int32_t* __restrict__ k_sizes, const int32_t* __restrict__ k_offsets, int n_k,
-                     int c_k, bf16* __restrict__ kd_hi, bf16* __restrict__ kd_lo, float4* __restrict__ kstat) {
+                     int c_k, bf16* __restrict__ kd_hi, bf16* __restrict__ kd_lo, float* __restrict__ kstat) {
   const int h = blockIdx.y, j = blockIdx.x;
   constexpr int EPL = D / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -122,7 +147,13 @@ __global__ void __launch_bounds__(128)
       *reinterpret_cast<uint32_t*>(kd_hi + row * D + lane * 2) = hi[0];
       *reinterpret_cast<uint32_t*>(kd_lo + row * D + lane * 2) = lo[0];
     }
-    if (lane == 0) kstat[row] = make_float4(a, 2.f * b, cc, 0.f);
+    if (lane == 0) {  // planes A, -2B, C (separate arrays: neighbouring keys load as register pairs)
+      const size_t ps = stat_plane_stride(n_k, c_k);
+      float* dst = kstat + (size_t)h * 3 * ps + stat_pos(o, j) + r;
+      dst[0] = a;
+      dst[ps] = -2.f * b;
+      dst[2 * ps] = cc;
+    }
   }
 }
 
@@ -139,8 +170,8 @@ __global__ void split_q_kernel(const float* __restrict__ qc, int d, int c_q, int
 
 template <int D>
 __global__ void __launch_bounds__(ETHREADS, 1)
-    error_table_tc_kernel(const bf16* __restrict__ qsplit, const bf16* __restrict__ kd_hi,
-                          const bf16* __restrict__ kd_lo, const float4* __restrict__ kstat,
+    error_table_tc_kernel(const __grid_constant__ CUtensorMap map_hi, const __grid_constant__ CUtensorMap map_lo,
+                          const bf16* __restrict__ qsplit, const float* __restrict__ kstat,
                           const int32_t* __restrict__ q_sizes, const int32_t* __restrict__ k_sizes,
                           const int32_t* __restrict__ k_offsets, const float* __restrict__ sbar,
                           const float* __restrict__ mref, int n_k, int c_q, int c_k, int cqpad, float scale,
@@ -153,7 +184,7 @@ __global__ void __launch_bounds__(ETHREADS, 1)
   const uint32_t sbase = smem_u32(smem);
   const uint32_t sA = sbase + L::kA, sB = sbase + L::kB, bars = sbase + L::kBars;
   const uint32_t sStat = sbase + L::kStat;
-  const float4* stat_smem = reinterpret_cast<const float4*>(smem + L::kStat);
+  const float* stat_smem = reinterpret_cast<const float*>(smem + L::kStat);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kBars + 192);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto bar = [&](int i) -> uint32_t { return bars + 8u * (uint32_t)i; };
@@ -167,6 +198,8 @@ __global__ void __launch_bounds__(ETHREADS, 1)
       mbar_init(bar(EB_ACCEMPTY + s), 128);
       mbar_init(bar(EB_STATEMPTY + 2 * s), 128);
       mbar_init(bar(EB_STATEMPTY + 2 * s + 1), 128);
+      mbar_init(bar(EB_STATFULL + 2 * s), 1);
+      mbar_init(bar(EB_STATFULL + 2 * s + 1), 1);
     }
     fence_barrier_init();
   }
@@ -178,60 +211,62 @@ __global__ void __launch_bounds__(ETHREADS, 1)
   const int32_t* ksz = k_sizes + (size_t)h * c_k;
   const int32_t* kof = k_offsets + (size_t)h * c_k;
 
-  if (warp == 8 || warp == 10) {
-    // =========================== producers =======================================================
-    // warp 8 stages the q̄ tiles and the even chunks (stage 0), warp 10 the odd chunks (stage 1);
-    // each blocks only on its own loads, so two chunk loads are always in flight.
+  if (warp == 8) {
+    // =========================== producer ========================================================
     constexpr int CPR = D / 8, RPI = 32 / CPR;
     const int sub = lane / CPR, chunk = lane % CPR;
-    const int mine = warp == 8 ? 0 : 1;
-    if (warp == 8) {
-      for (int p = 0; p < 2; ++p) {
-        const bf16* src = qsplit + (((size_t)h * 2 + p) * cqpad + (size_t)mt * EM) * D;
-        for (int r0 = 0; r0 < EM; r0 += RPI) {
-          const int r = r0 + sub;
-          cp_async16(sA + (uint32_t)(p * L::kTile + (chunk >> 3) * (EM * 128)) + swz(r, chunk & 7),
-                     src + (size_t)r * D + chunk * 8);
-        }
+    for (int p = 0; p < 2; ++p) {
+      const bf16* src = qsplit + (((size_t)h * 2 + p) * cqpad + (size_t)mt * EM) * D;
+      for (int r0 = 0; r0 < EM; r0 += RPI) {
+        const int r = r0 + sub;
+        cp_async16(sA + (uint32_t)(p * L::kTile + (chunk >> 3) * (EM * 128)) + swz(r, chunk & 7),
+                   src + (size_t)r * D + chunk * 8);
       }
-      cp_async_commit();
-      cp_async_wait_all();
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar(EB_AFULL));
     }
-    int u = 0, guses[2] = {0, 0};
-    for (int j = j_lo; j < j_hi; ++j) {
-      const int nj = ksz[j], o = kof[j];
-      const int g = (j - j_lo) & 1;
-      for (int s0 = 0; s0 < nj; s0 += ECH, ++u) {
-        const int gu = guses[g]++;  // use number of this chunk within its epilogue group
-        if ((u & 1) != mine) continue;
-        const int st = u & 1;
-        if (u >= 2) mbar_wait(bar(EB_BEMPTY + st), ((u >> 1) + 1) & 1);
-        const int nn = ((min(ECH, nj - s0) + 15) >> 4) << 4;
-        for (int p = 0; p < 2; ++p) {
-          const bf16* src = (p == 0 ? kd_hi : kd_lo) + (size_t)h * n_k * D;
-          const uint32_t dst = sB + (uint32_t)((st * 2 + p) * L::kTile);
-          for (int r0 = 0; r0 < nn; r0 += RPI) {
-            const int r = r0 + sub;
-            const int row = min(o + s0 + r, n_k - 1);
-            cp_async16(dst + (uint32_t)((chunk >> 3) * (EM * 128)) + swz(r, chunk & 7),
-                       src + (size_t)row * D + chunk * 8);
+    cp_async_commit();
+    cp_async_wait_all();
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar(EB_AFULL));
+    if (elect_one()) {
+      const size_t ps = stat_plane_stride(n_k, c_k);
+      const float* planes = kstat + (size_t)h * 3 * ps;
+      int u = 0, guses[2] = {0, 0};
+      for (int j = j_lo; j < j_hi; ++j) {
+        const int nj = ksz[j], o = kof[j];
+        const int g = (j - j_lo) & 1;
+        const int pos = stat_pos(o, j);
+        for (int s0 = 0; s0 < nj; s0 += ECH, ++u) {
+          const int gu = guses[g]++;  // use number of this chunk within its epilogue group
+          const int st = u & 1;
+          if (u >= 2) mbar_wait(bar(EB_BEMPTY + st), ((u >> 1) + 1) & 1);
+          const int valid = min(ECH, nj - s0);
+          const int nn = ((valid + 15) >> 4) << 4;
+          const uint32_t fb = bar(EB_BFULL + st);
+          mbar_expect_tx(fb, (uint32_t)(2 * nn * D * 2));
+          const int row = h * n_k + o + s0;
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            const CUtensorMap* tm = p == 0 ? &map_hi : &map_lo;
+            const uint32_t dst = sB + (uint32_t)((st * 2 + p) * L::kTile);
+            for (int rb = 0; rb < nn; rb += 16)
+#pragma unroll
+              for (int sl = 0; sl < D / 64; ++sl)
+                tma_box(dst + (uint32_t)(sl * (EM * 128) + rb * 128), tm, sl * 64, row + rb, fb);
           }
+          // per-key scalars: stat buffer (group g, use parity); its previous user was use gu-2
+          const int sb = g * 2 + (gu & 1);
+          if (gu >= 2) mbar_wait(bar(EB_STATEMPTY + sb), ((gu >> 1) + 1) & 1);
+          const uint32_t nbytes = (uint32_t)(((valid + 3) >> 2) << 4);
+          const uint32_t sf = bar(EB_STATFULL + sb);
+          mbar_expect_tx(sf, 3 * nbytes);
+#pragma unroll
+          for (int pl = 0; pl < 3; ++pl)
+            bulk_copy(sStat + (uint32_t)((sb * 3 + pl) * ECH * 4), planes + (size_t)pl * ps + pos + s0, nbytes, sf);
         }
-        // per-key scalars: stat buffer (group g, use parity); its previous user was use gu-2
-        const int sb = g * 2 + (gu & 1);
-        if (gu >= 2) mbar_wait(bar(EB_STATEMPTY + sb), ((gu >> 1) + 1) & 1);
-        for (int r = lane; r < nn; r += 32)
-          cp_async16(sStat + (uint32_t)((sb * ECH + r) * 16), kstat + (size_t)h * n_k + min(o + s0 + r, n_k - 1));
-        cp_async_commit();
-        cp_async_wait_all();
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar(EB_BFULL + st));
       }
     }
+    __syncwarp();
   } else if (warp == 9) {
     // =========================== MMA issuer ======================================================
     if (elect_one()) {
@@ -287,41 +322,105 @@ __global__ void __launch_bounds__(ETHREADS, 1)
       for (int s0 = 0; s0 < nj; s0 += ECH, ++uses, ++u) {
         const int valid = min(ECH, nj - s0);
         const int sbuf = g * 2 + (uses & 1);
-        const float4* ks = stat_smem + sbuf * ECH;
+        const float* ksA = stat_smem + sbuf * (3 * ECH);
+        const float* ksB = ksA + ECH;  // -2B
+        const float* ksC = ksB + ECH;
+        mbar_wait(bar(EB_STATFULL + sbuf), (uses >> 1) & 1);
         mbar_wait(bar(EB_ACCFULL + g), uses & 1);
         tc_fence_after();
-        // pass 1: chunk maximum of g for this query cluster -> raise the running maximum once
-        float gmax = -INFINITY;
+        // pass 1: largest |g| of the chunk for this query cluster (columns beyond the chunk masked)
+        float amax = 0.f;
         for (int c0 = 0; c0 < valid; c0 += 16) {
           uint32_t a[16];
           TMEM_LD16(tcol + c0, a);
           tc_wait_ld();
+          if (c0 + 16 <= valid) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
-            gmax = fmaxf(gmax, c0 + q < valid ? __uint_as_float(a[q]) : -INFINITY);
-        }
-        gmax *= scale;
-        if (gmax > M) {
-          const float r = __expf(M - gmax);
-          acc *= r * r;
-          M = gmax;
-          em = __expf(-M);
-          em2 = em * em;
-        }
-        // pass 2: branch-free accumulation at the fixed maximum M:
-        //   xs = exp(g - M) - exp(-M) = em * expm1(g)   (g <= M; the clamp only guards overflow)
-        for (int c0 = 0; c0 < valid; c0 += 16) {
-          uint32_t a[16];
-          TMEM_LD16(tcol + c0, a);
-          tc_wait_ld();
+            for (int q = 0; q < 16; ++q) amax = fmaxf(amax, fabsf(__uint_as_float(a[q])));
+          } else {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float4 st4 = ks[c0 + q];
-            const float gg = fminf(__uint_as_float(a[q]) * scale, 85.f);
-            const float xs = expm1_fast(gg) * em;
-            // A em^2 - 2B (em xs) + C xs^2, Horner in xs
-            const float term = fmaf(fmaf(st4.z, xs, -st4.y * em), xs, st4.x * em2);
-            acc += c0 + q < valid ? term : 0.f;
+            for (int q = 0; q < 16; ++q) amax = fmaxf(amax, c0 + q < valid ? fabsf(__uint_as_float(a[q])) : 0.f);
+          }
+        }
+        if (!__any_sync(0xffffffffu, amax * scale > 1.0f)) {
+          // ---- packed path: |g| <= 1 for every lane of the warp.  x = expm1(g) by the degree-8 series
+          // (g^9/9! < 2.8e-6), two keys per instruction, no stabiliser: S = sum A - 2B x + C x^2, then
+          // acc += exp(-2M) S (M is the block's running maximum; it only moves in the scalar path).
+          const uint64_t sc2 = pack2(scale, scale);
+          uint64_t s2 = pack2(0.f, 0.f);
+          for (int c0 = 0; c0 < valid; c0 += 16) {
+            uint32_t a[16];
+            TMEM_LD16(tcol + c0, a);
+            tc_wait_ld();
+            if (c0 + 16 > valid) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) a[q] = c0 + q < valid ? a[q] : 0u;  // g = 0 where the scalars are 0
+            }
+#pragma unroll
+            for (int q4 = 0; q4 < 16; q4 += 4) {
+              float4 A4 = *reinterpret_cast<const float4*>(ksA + c0 + q4);
+              float4 B4 = *reinterpret_cast<const float4*>(ksB + c0 + q4);
+              float4 C4 = *reinterpret_cast<const float4*>(ksC + c0 + q4);
+              if (c0 + q4 + 4 > valid) {  // past the chunk: whatever follows in the plane (or stale) -> 0
+                const int left = valid - (c0 + q4);
+                if (left < 4) { A4.w = B4.w = C4.w = 0.f; }
+                if (left < 3) { A4.z = B4.z = C4.z = 0.f; }
+                if (left < 2) { A4.y = B4.y = C4.y = 0.f; }
+                if (left < 1) { A4.x = B4.x = C4.x = 0.f; }
+              }
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const uint64_t g2 = fmul2(pack2(__uint_as_float(a[q4 + 2 * hh]), __uint_as_float(a[q4 + 2 * hh + 1])), sc2);
+                uint64_t pz = ffma2(g2, pack2(1.f / 40320.f, 1.f / 40320.f), pack2(1.f / 5040.f, 1.f / 5040.f));
+                pz = ffma2(pz, g2, pack2(1.f / 720.f, 1.f / 720.f));
+                pz = ffma2(pz, g2, pack2(1.f / 120.f, 1.f / 120.f));
+                pz = ffma2(pz, g2, pack2(1.f / 24.f, 1.f / 24.f));
+                pz = ffma2(pz, g2, pack2(1.f / 6.f, 1.f / 6.f));
+                pz = ffma2(pz, g2, pack2(0.5f, 0.5f));
+                pz = ffma2(pz, g2, pack2(1.f, 1.f));
+                const uint64_t x2 = fmul2(pz, g2);
+                const uint64_t A2 = hh ? pack2(A4.z, A4.w) : pack2(A4.x, A4.y);
+                const uint64_t B2 = hh ? pack2(B4.z, B4.w) : pack2(B4.x, B4.y);
+                const uint64_t C2 = hh ? pack2(C4.z, C4.w) : pack2(C4.x, C4.y);
+                s2 = fadd2(s2, ffma2(ffma2(C2, x2, B2), x2, A2));
+              }
+            }
+          }
+          float s_lo, s_hi;
+          unpack2(s2, s_lo, s_hi);
+          acc = fmaf(em2, s_lo + s_hi, acc);
+        } else {
+          // ---- scalar path: chunk maximum of g -> raise the running maximum once, then accumulate at
+          // the fixed maximum M:  xs = exp(g - M) - exp(-M) = em * expm1(g)
+          float gmax = -INFINITY;
+          for (int c0 = 0; c0 < valid; c0 += 16) {
+            uint32_t a[16];
+            TMEM_LD16(tcol + c0, a);
+            tc_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              gmax = fmaxf(gmax, c0 + q < valid ? __uint_as_float(a[q]) : -INFINITY);
+          }
+          gmax *= scale;
+          if (gmax > M) {
+            const float r = __expf(M - gmax);
+            acc *= r * r;
+            M = gmax;
+            em = __expf(-M);
+            em2 = em * em;
+          }
+          for (int c0 = 0; c0 < valid; c0 += 16) {
+            uint32_t a[16];
+            TMEM_LD16(tcol + c0, a);
+            tc_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const float gg = fminf(__uint_as_float(a[q]) * scale, 85.f);
+              const float xs = expm1_fast(gg) * em;
+              // A em^2 - 2B (em xs) + C xs^2, Horner in xs
+              const float term = fmaf(fmaf(ksC[c0 + q], xs, ksB[c0 + q] * em), xs, ksA[c0 + q] * em2);
+              acc += c0 + q < valid ? term : 0.f;
+            }
           }
         }
         tc_fence_before();
@@ -342,16 +441,18 @@ __global__ void __launch_bounds__(ETHREADS, 1)
   }
 }
 
+size_t errtab_stat_floats(const SvgEarShape& s) { return (size_t)s.bh * 3 * stat_plane_stride(s.n_k, s.c_k) + 64; }
+
 size_t errtab_tc_scratch_bytes(const SvgEarShape& s) {
   const int cqpad = ceil_div(s.c_q, EM) * EM;
-  return align_up((size_t)s.bh * s.n_k * s.d * 2, 256) * 2 + align_up((size_t)s.bh * s.n_k * 16, 256) +
+  return align_up((size_t)s.bh * s.n_k * s.d * 2, 256) * 2 + align_up(errtab_stat_floats(s) * 4, 256) +
          align_up((size_t)s.bh * 2 * cqpad * s.d * 2, 256) + 1024;
 }
 
 // key-side half of the estimator (needs only the key clustering): k - k̄ split + per-key scalars
 int launch_key_stats(const SvgEarShape& s, int mode, const float* kc, const float* vc, const bf16* kp,
                      const bf16* vp, const int32_t* k_sizes, const int32_t* k_offsets, bf16* kd_hi, bf16* kd_lo,
-                     float4* kstat, cudaStream_t st) {
+                     float* kstat, cudaStream_t st) {
   if (s.d == 128)
     key_stats_kernel<128><<<dim3(s.c_k, s.bh), 128, 0, st>>>(mode, kc, vc, kp, vp, k_sizes, k_offsets, s.n_k,
                                                             s.c_k, kd_hi, kd_lo, kstat);
@@ -365,7 +466,7 @@ int launch_key_stats(const SvgEarShape& s, int mode, const float* kc, const floa
 int launch_error_table_tc(const SvgEarShape& s, int mode, const float* qc, const float* kc, const float* vc,
                           const bf16* kp, const bf16* vp, const int32_t* q_sizes, const int32_t* k_sizes,
                           const int32_t* k_offsets, const float* sbar, const float* mref, bf16* kd_hi,
-                          bf16* kd_lo, float4* kstat, bf16* qsplit, double* err, bool key_stats_done,
+                          bf16* kd_lo, float* kstat, bf16* qsplit, double* err, bool key_stats_done,
                           cudaStream_t st) {
   const int cqpad = ceil_div(s.c_q, EM) * EM;
   const float scale = 1.0f / sqrtf((float)s.d);
@@ -375,17 +476,21 @@ int launch_error_table_tc(const SvgEarShape& s, int mode, const float* qc, const
     const int rc = launch_key_stats(s, mode, kc, vc, kp, vp, k_sizes, k_offsets, kd_hi, kd_lo, kstat, st);
     if (rc) return rc;
   }
+  CUtensorMap map_hi, map_lo;  // [bh*n_k][d] bf16, box = 64 columns x 16 rows
+  if (!encode_rows_map(&map_hi, kd_hi, (uint64_t)s.bh * s.n_k, s.d, 16) ||
+      !encode_rows_map(&map_lo, kd_lo, (uint64_t)s.bh * s.n_k, s.d, 16))
+    return SVGEAR_ECUDA;
   dim3 grid(ceil_div(s.c_k, ERANGE), cqpad / EM, s.bh);
   if (s.d == 128) {
     const size_t smem = ESmem<128>::bytes();
     SVG_CUDA_OK(cudaFuncSetAttribute(error_table_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    error_table_tc_kernel<128><<<grid, ETHREADS, smem, st>>>(qsplit, kd_hi, kd_lo, kstat, q_sizes, k_sizes,
+    error_table_tc_kernel<128><<<grid, ETHREADS, smem, st>>>(map_hi, map_lo, qsplit, kstat, q_sizes, k_sizes,
                                                              k_offsets, sbar, mref, s.n_k, s.c_q, s.c_k, cqpad,
                                                              scale, err);
   } else {
     const size_t smem = ESmem<64>::bytes();
     SVG_CUDA_OK(cudaFuncSetAttribute(error_table_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    error_table_tc_kernel<64><<<grid, ETHREADS, smem, st>>>(qsplit, kd_hi, kd_lo, kstat, q_sizes, k_sizes,
+    error_table_tc_kernel<64><<<grid, ETHREADS, smem, st>>>(map_hi, map_lo, qsplit, kstat, q_sizes, k_sizes,
                                                             k_offsets, sbar, mref, s.n_k, s.c_q, s.c_k, cqpad,
                                                             scale, err);
   }

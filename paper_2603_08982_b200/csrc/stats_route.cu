@@ -205,11 +205,11 @@ __global__ void __launch_bounds__(256, 1)
 int launch_error_table_tc(const SvgEarShape& s, int mode, const float* qc, const float* kc, const float* vc,
                           const bf16* kp, const bf16* vp, const int32_t* q_sizes, const int32_t* k_sizes,
                           const int32_t* k_offsets, const float* sbar, const float* mref, bf16* kd_hi,
-                          bf16* kd_lo, float4* kstat, bf16* qsplit, double* err, bool key_stats_done,
+                          bf16* kd_lo, float* kstat, bf16* qsplit, double* err, bool key_stats_done,
                           cudaStream_t st);
 int launch_key_stats(const SvgEarShape& s, int mode, const float* kc, const float* vc, const bf16* kp,
                      const bf16* vp, const int32_t* k_sizes, const int32_t* k_offsets, bf16* kd_hi, bf16* kd_lo,
-                     float4* kstat, cudaStream_t st);
+                     float* kstat, cudaStream_t st);
 
 // key-side half of the tensor-core estimator, for callers that overlap it with the query side
 int launch_error_table_keys(const SvgEarShape& s, int mode, const float* kc, const float* vc, const bf16* kp,
@@ -218,12 +218,14 @@ int launch_error_table_keys(const SvgEarShape& s, int mode, const float* kc, con
   return launch_key_stats(s, mode, kc, vc, kp, vp, k_sizes, k_offsets, sc.kd_hi, sc.kd_lo, sc.kstat, st);
 }
 
+size_t errtab_stat_floats(const SvgEarShape& s);
+
 bool ErrScratch::carve(Carver& cv, const SvgEarShape& s) {
   const int cqpad = ceil_div(s.c_q, 128) * 128;
   sbar = cv.take<float>((size_t)s.bh * s.c_q * s.c_k);
   kd_hi = cv.take<bf16>((size_t)s.bh * s.n_k * s.d);
   kd_lo = cv.take<bf16>((size_t)s.bh * s.n_k * s.d);
-  kstat = cv.take<float4>((size_t)s.bh * s.n_k);
+  kstat = cv.take<float>(errtab_stat_floats(s));  // planes A, -2B, C, clusters 16-byte aligned (errtab_tc.cu)
   qsplit = cv.take<bf16>((size_t)s.bh * 2 * cqpad * s.d);
   return cv.ok;
 }

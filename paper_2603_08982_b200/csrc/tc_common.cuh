@@ -36,6 +36,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "}" ::"r"(bar), "r"(parity)
       : "memory");
 }
+// Same wait for warps with slack (producers several stages ahead): the hardware may keep the thread
+// suspended for up to `hint_ns` before it polls again, so the spin does not take issue slots from
+// the compute warps of the same scheduler.
+__device__ __forceinline__ void mbar_wait_relaxed(uint32_t bar, uint32_t parity, uint32_t hint_ns) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "WAIT_LOOP_R:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@p bra WAIT_DONE_R;\n\t"
+      "bra WAIT_LOOP_R;\n\t"
+      "WAIT_DONE_R:\n\t"
+      "}" ::"r"(bar), "r"(parity), "r"(hint_ns)
+      : "memory");
+}
 // 2-D tiled bulk tensor load: box at (col, row) -> shared memory, completes tx bytes on `bar`
 __device__ __forceinline__ void tma_box(uint32_t dst, const CUtensorMap* tm, int col, int row, uint32_t bar) {
   asm volatile(
@@ -171,6 +186,11 @@ __device__ __forceinline__ void unpack2(uint64_t v, float& a, float& b) {
 __device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
   uint64_t d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
 __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {

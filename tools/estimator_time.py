@@ -20,3 +20,14 @@ e0.record()
 for _ in range(10): t2 = P.estimate_errors_streaming(qm, km, kp, vp)
 e1.record(); torch.cuda.synchronize()
 print(json.dumps({"estimator_ms": e0.elapsed_time(e1) / 10, "checksum": float(t2.error_sum.sum())}))
+if os.environ.get("PROFILE"):
+    from torch.profiler import profile, ProfilerActivity
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        P.estimate_errors_streaming(qm, km, kp, vp); torch.cuda.synchronize()
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CUDA:
+            print(f"{e.device_time / 1e3:8.3f} ms  {e.name[:90]}")
+    # against the fp32 check kernel (same quantity on CUDA cores): largest deviation relative to the table's maximum
+    t32 = P.estimate_errors_streaming(qm, km, kp, vp, fp32_check=True)
+    dev = float(((t2.error_sum - t32.error_sum).abs().amax(dim=(1, 2)) / t32.error_sum.amax(dim=(1, 2))).max())
+    print(json.dumps({"max_dev_vs_fp32_check_rel_to_table_max": dev}))

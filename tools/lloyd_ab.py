@@ -15,7 +15,6 @@ ap.add_argument("--inputs", default="blobs")
 ap.add_argument("--iters", type=int, default=25)
 ap.add_argument("--start", default="strided", choices=["strided", "device"])
 ap.add_argument("--no-inertia", action="store_true", help="the one-launch-per-iteration path svgear_forward uses")
-ap.add_argument("--legacy", action="store_true", help="compare against the unfused kernels (SVGEAR_LEGACY_LLOYD)")
 a = ap.parse_args()
 H, S, d, cq, ck = bench.WORKLOADS[a.workload]
 H = a.heads or H
@@ -23,11 +22,7 @@ dev = torch.device("cuda", 0)
 q, k, v = bench.make_heads(torch, 0, H, S, d, cq, ck, 0.1, dev, kind=a.inputs)
 
 
-def run(x, c, legacy_env, full_eval=False):
-    if legacy_env:
-        os.environ["SVGEAR_LEGACY_LLOYD"] = "1"
-    else:
-        os.environ.pop("SVGEAR_LEGACY_LLOYD", None)
+def run(x, c, full_eval=False):
     init = CL.strided_start(x[0], c) if a.start == "strided" else CL.device_start(x[0], c, seed=0)
     go = lambda: CL.run_lloyd(x[0], init, a.iters, full_eval=full_eval, want_inertia=not a.no_inertia)
     go()
@@ -40,20 +35,19 @@ def run(x, c, legacy_env, full_eval=False):
 
 
 for name, x, c in (("query", q, cq), ("key", k, ck)):
-    new, t_new = run(x, c, False)
-    ref, t_ref = run(x, c, a.legacy, full_eval=not a.legacy)
+    new, t_new = run(x, c)
+    ref, t_ref = run(x, c, full_eval=True)
     same = {f: bool(torch.equal(new[f], ref[f])) for f in ("assign", "perm", "sizes", "offsets", "centroids", "iters")}
     it_new = new["iters"]
     rel = float(((new["inertia"] - ref["inertia"]).abs() / ref["inertia"].abs().clamp_min(1e-30)).max())
     same["inertia<=1e-6"] = a.no_inertia or rel <= 1e-6
-    print(f"{name}: fused {t_new:.3f} ms, {'legacy' if a.legacy else 'full-eval'} {t_ref:.3f} ms, "
+    print(f"{name}: fused {t_new:.3f} ms, full-eval {t_ref:.3f} ms, "
           f"iters max {int(it_new.max())} mean {float(it_new.float().mean()):.1f}, identical: {same}", flush=True)
     assert all(same.values()), same
 print("OK")
 
 if os.environ.get("PROFILE"):
     from torch.profiler import profile, ProfilerActivity
-    os.environ.pop("SVGEAR_LEGACY_LLOYD", None)
     for name, x, c in (("query", q, cq), ("key", k, ck)):
         init = CL.device_start(x[0], c, seed=0)
         torch.cuda.synchronize()

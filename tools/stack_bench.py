@@ -4,7 +4,7 @@ fixed blob mixture whose centres random-walk by `--drift` per step, fresh token 
 
 Three schedules are timed (CUDA events around the whole run, inputs resident), all through the
 product scheduler `schedule.SvgEarStack`:
-  cold : every (layer, step) seeds its k-means on the device (svgear_kmeans_seed_gram);
+  cold : every (layer, step) seeds its k-means on the device (svgear_kmeans_seed);
   warm : step t of a layer starts Lloyd from the centroids of step t-1 of the same layer
          (the reference's warm start, clustering.py:158-163) with the iteration
          cap --warm-iters (the first step of a layer is cold);
