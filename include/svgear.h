@@ -135,6 +135,23 @@ int svgear_kmeans_seed(int32_t bh, int32_t n, int32_t d, int32_t c, const void* 
                        int32_t oversample, uint32_t seed, int32_t first_instance, float* centroids,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* The reference's own k-means++ draw, bit for bit, on the device: clustering._kmeans_pp_init
+ * (clustering.py:65-84) under numpy's Generator(PCG64) — rng.integers(n) for the first centre, then
+ * rng.choice(n, p=d2/total) per centre, with every float64 operation in numpy's order (pairwise row
+ * sums and d2.sum(), sequential cumsum, searchsorted(side="right")), and the lowest unused index
+ * when all distances are zero.  The result equals the centres the reference starts from for the
+ * same generator state, at any size, without a host stage; it is the parity path (the sequential
+ * cumsum costs one dependent float64 add per token per centre), not the production seeding.
+ *   pcg64_states [bh][4] u64 (DEVICE): {state_hi, state_lo, inc_hi, inc_lo} of each instance's PCG64
+ *     right after seeding, i.e. numpy.random.PCG64(SeedSequence(entropy=side_seed,
+ *     spawn_key=(restart,))).state (clustering.py:178-180; has_uint32 == 0)
+ *   centroids [bh][c][d] f32 (out)      picks [bh][c] i32 token indices (out, may be NULL)
+ *   workspace: svgear_kmeans_seed_reference_workspace(bh, n) bytes                              */
+int svgear_kmeans_seed_reference(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
+                                 const uint64_t* pcg64_states, float* centroids, int32_t* picks,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+int svgear_kmeans_seed_reference_workspace(int32_t bh, int32_t n, size_t* bytes);
+
 /* out[b][i][:] = x[b][perm[b][i]][:]   — clustering.permute_rows (clustering.py:210-212). */
 int svgear_permute_rows(int32_t bh, int32_t n, int32_t d, const void* x, const int32_t* perm,
                         void* out, void* stream);

@@ -15,7 +15,7 @@ from .analysis import Prepared, build_error_table, prepare
 from .attention import (AttentionResult, FlopCounters, compensation_flops, exact_block_flops,
                         sparse_attend)
 from .clustering import (ClusterModel, cluster_means, device_start, inverse_permute_rows, kmeans, kmeans_pp_init,
-                         permute_rows, segment_means, strided_start)
+                         permute_rows, reference_start, seeded_start, segment_means, strided_start)
 from .estimator import (BlockErrorTable, estimate_errors, estimate_errors_streaming,
                         estimate_errors_value_aware)
 from .operator import operator_workspace_bytes, reference_init, svg_ear_attention

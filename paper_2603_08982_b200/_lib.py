@@ -15,7 +15,7 @@ import threading
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG_DIR, "csrc")
 LIB_PATH = os.path.join(PKG_DIR, "libsvgear.so")
-SOURCES = ("api.cu", "kmeans.cu", "lloyd_step.cu", "kmeans_tc.cu", "seed.cu", "stats_route.cu", "errtab_tc.cu", "attend_ref.cu", "attend_tc.cu", "dit.cu")
+SOURCES = ("api.cu", "kmeans.cu", "lloyd_step.cu", "kmeans_tc.cu", "seed.cu", "seed_ref.cu", "stats_route.cu", "errtab_tc.cu", "attend_ref.cu", "attend_tc.cu", "dit.cu")
 NVCC_FLAGS = (
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-shared", "-Xcompiler", "-fPIC",
@@ -58,6 +58,8 @@ SIGNATURES = {
     "svgear_workspace_bytes": ([C.POINTER(Shape), C.POINTER(_SZ)], C.c_int),
     "svgear_kmeans": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
     "svgear_kmeans_seed": ([_I32, _I32, _I32, _I32, _P, _I32, C.c_uint32, _I32, _P, _P, _SZ, _P], C.c_int),
+    "svgear_kmeans_seed_reference": ([_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),
+    "svgear_kmeans_seed_reference_workspace": ([_I32, _I32, C.POINTER(_SZ)], C.c_int),
     "svgear_permute_rows": ([_I32, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "svgear_segment_means": ([_I32, _I32, _I32, _I32, _P, _P, _P, _P, _P], C.c_int),
     "svgear_error_table": ([C.POINTER(Shape), _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P], C.c_int),

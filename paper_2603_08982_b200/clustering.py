@@ -2,15 +2,17 @@
 
 Same names and argument meaning as the reference (clustering.py:144-257); arrays are torch CUDA
 tensors.  `kmeans` accepts one instance [n, d] (as the reference) or a batch [bh, n, d].
-`kmeans` (the reference's entry point, seed-faithful) draws its k-means++ start on the host with
-the reference's RNG call sequence (clustering.py:65-84, 178-180) so a given `seed` starts from the
-identical centres — the parity path; `device_start` is the device-side seeding the operator uses.
+`kmeans` (the reference's entry point, seed-faithful) starts from the reference's own k-means++
+centres for a given `seed` (clustering.py:65-84, 178-180): `reference_start` reproduces numpy's draw
+bit for bit on the device (svgear_kmeans_seed_reference); `seeded_start` is the same draw in host numpy,
+kept as the cross-check of the tests; `device_start` is the fast device-side seeding the operator uses.
 Lloyd iterations, repair, permutation and means run in libsvgear (svgear_kmeans).
 """
 
 from __future__ import annotations
 
 import ctypes as C
+from ctypes import c_size_t as _SZ
 from dataclasses import dataclass
 
 import numpy as np
@@ -59,6 +61,42 @@ def seeded_start(tokens, k, seed, restart=0):
     """Start centres of restart `restart` for `seed` (clustering.py:178-180)."""
     rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(restart,)))
     return kmeans_pp_init(tokens, k, rng)
+
+
+def pcg64_states(seeds, restart=0):
+    """PCG64 states {state_hi, state_lo, inc_hi, inc_lo} of the generators the reference creates for
+    `seeds` (clustering.py:178-180): numpy.random.PCG64(SeedSequence(entropy=seed, spawn_key=(restart,))).
+    Host side: SeedSequence hashing is a few integer operations; everything after it runs on the device."""
+    out = np.empty((len(seeds), 4), dtype=np.uint64)
+    lo64 = (1 << 64) - 1
+    for i, seed in enumerate(seeds):
+        st = np.random.PCG64(np.random.SeedSequence(entropy=int(seed), spawn_key=(int(restart),))).state["state"]
+        out[i] = (st["state"] >> 64, st["state"] & lo64, st["inc"] >> 64, st["inc"] & lo64)
+    return out
+
+
+def reference_start(tokens, k, seeds, restart=0, return_picks=False):
+    """The reference's k-means++ start centres (clustering._kmeans_pp_init under numpy's PCG64,
+    clustering.py:65-84, 178-180) computed ON THE DEVICE, bit-identical to `seeded_start` on the host
+    (svgear_kmeans_seed_reference: numpy's float64 operation order and RNG reproduced exactly).
+    tokens [bh, n, d] (or [n, d]) bf16 CUDA; seeds: one side seed per instance."""
+    x = (tokens if tokens.ndim == 3 else tokens.unsqueeze(0)).contiguous()
+    bh, n, d = x.shape
+    seeds = [int(seeds)] if np.isscalar(seeds) else [int(s_) for s_ in seeds]
+    if len(seeds) != bh:
+        raise ValueError(f"got {len(seeds)} seeds for {bh} instances")
+    states = torch.from_numpy(pcg64_states(seeds, restart).view(np.int64)).to(x.device)
+    out = torch.empty((bh, int(k), d), dtype=torch.float32, device=x.device)
+    picks = torch.empty((bh, int(k)), dtype=torch.int32, device=x.device)
+    need = _SZ(0)
+    _lib.check("svgear_kmeans_seed_reference_workspace",
+               _lib.lib().svgear_kmeans_seed_reference_workspace(bh, n, C.byref(need)))
+    ws = workspace(int(need.value), x.device)
+    rc = _lib.lib().svgear_kmeans_seed_reference(bh, n, d, int(k), x.data_ptr(), states.data_ptr(), out.data_ptr(),
+                                                 picks.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr())
+    _lib.check("svgear_kmeans_seed_reference", rc)
+    res = out if tokens.ndim == 3 else out[0]
+    return (res, picks if tokens.ndim == 3 else picks[0]) if return_picks else res
 
 
 def strided_start(tokens, k):
@@ -180,14 +218,12 @@ def kmeans(tokens, num_clusters, *, max_iters=25, seed=0, restarts=1, init_centr
     x, was_2d = _validated(tokens, num_clusters, restarts, max_iters)
     bh, n, d = x.shape
     k = int(num_clusters)
-    x_host = x.float().cpu().numpy().astype(np.float64)
     seeds = [int(s_) for s_ in seed] if isinstance(seed, (list, tuple)) else [int(seed) + b for b in range(bh)]
     if len(seeds) != bh:
         raise ValueError(f"got {len(seeds)} seeds for {bh} instances")
-    pool = []  # list over starts of [bh,k,d] f32
+    pool = []  # list over starts of [bh,k,d] f32: the reference's seeded draws, reproduced on the device
     for r in range(restarts):
-        pool.append(torch.from_numpy(np.stack(
-            [seeded_start(x_host[b], k, seeds[b], r) for b in range(bh)])).to(x.device, torch.float32))
+        pool.append(reference_start(x, k, seeds, r))
     if init_centroids is not None:
         ic = torch.as_tensor(np.asarray(init_centroids) if not isinstance(init_centroids, torch.Tensor)
                              else init_centroids)

@@ -220,6 +220,23 @@ int svgear_kmeans_seed(int32_t bh, int32_t n, int32_t d, int32_t c, const void* 
                      (cudaStream_t)stream);
 }
 
+int svgear_kmeans_seed_reference(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,
+                                 const uint64_t* pcg64_states, float* centroids, int32_t* picks, void* workspace,
+                                 size_t workspace_bytes, void* stream) {
+  if (!x || !pcg64_states || !centroids || !workspace) return SVGEAR_EINVAL;
+  if (bh < 1 || n < 1 || (d != 64 && d != 128) || c < 1 || c > n || c > kMaxClusters) return SVGEAR_ESHAPE;
+  if (!device_present()) return SVGEAR_ECUDA;
+  if (workspace_bytes < seed_reference_ws_bytes(bh, n)) return SVGEAR_EWORKSPACE;
+  return launch_seed_reference(bh, n, d, c, (const bf16*)x, pcg64_states, centroids, picks, workspace, workspace_bytes,
+                               (cudaStream_t)stream);
+}
+
+int svgear_kmeans_seed_reference_workspace(int32_t bh, int32_t n, size_t* bytes) {
+  if (!bytes || bh < 1 || n < 1) return SVGEAR_EINVAL;
+  *bytes = seed_reference_ws_bytes(bh, n);
+  return SVGEAR_OK;
+}
+
 int svgear_permute_rows(int32_t bh, int32_t n, int32_t d, const void* x, const int32_t* perm,
                         void* out, void* stream) {
   if (!x || !perm || !out) return SVGEAR_EINVAL;

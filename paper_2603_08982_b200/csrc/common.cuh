@@ -162,6 +162,10 @@ int launch_kmeans(int exec_mode, int bh, int n, int d, int c, const bf16* x, con
 int seed_subsample(int n, int c, int oversample);
 int launch_seed(int bh, int n, int d, int c, int oversample, const bf16* x, uint32_t seed, int first_instance,
                 float* cent, bf16* gram_ws, cudaStream_t st);
+// the reference's numpy k-means++ draw on the device (seed_ref.cu)
+size_t seed_reference_ws_bytes(int bh, int n);
+int launch_seed_reference(int bh, int n, int d, int c, const bf16* x, const uint64_t* pcg_states, float* cent,
+                          int32_t* picks, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_gather_rows(int bh, int n, int d, const bf16* x, const int32_t* perm, bf16* out,
                        cudaStream_t st);
 int launch_segment_means(int bh, int n, int d, int c, const bf16* xp, const int32_t* sizes,

@@ -16,7 +16,7 @@ import torch
 from . import _lib
 from ._tensors import ShapeError, require_cuda, stream_ptr, workspace
 from .analysis import side_seeds
-from .clustering import SEED_OVERSAMPLE, seeded_start, strided_start
+from .clustering import SEED_OVERSAMPLE, reference_start, strided_start
 from .router import _OVERSHOOT, entry_capacity
 
 _EST = {"valueAware": _lib.EST_VALUE_AWARE, "plain": _lib.EST_PLAIN}
@@ -57,17 +57,15 @@ def operator_workspace_bytes(bh, n_q, n_k, d, n_q_clusters, n_k_clusters, head_g
 
 def reference_init(q, k, n_q_clusters, n_k_clusters, seed):
     """k-means++ start centres the reference would draw for `prepare(seed=...)`, for every
-    instance of a [.., S, d] batch (instance index b uses seed + b).  Host-side numpy; meant for
-    parity runs only — it is O(C*S*d) per instance on the CPU (minutes at video scale), which is why
-    the operator's default start is the device-side seeding."""
-    qf = q.reshape(-1, q.shape[-2], q.shape[-1]).float().cpu().numpy().astype(np.float64)
-    kf = k.reshape(-1, k.shape[-2], k.shape[-1]).float().cpu().numpy().astype(np.float64)
-    qi, ki = [], []
-    for b in range(qf.shape[0]):
-        qs, ks = side_seeds(seed + b)
-        qi.append(seeded_start(qf[b], n_q_clusters, qs))
-        ki.append(seeded_start(kf[b], n_k_clusters, ks))
-    return (torch.from_numpy(np.stack(qi)).float(), torch.from_numpy(np.stack(ki)).float())
+    instance of a [.., S, d] batch (instance index b uses seed + b): numpy's draw reproduced bit for
+    bit on the device (clustering.reference_start); the host only derives the per-instance side seeds
+    (analysis.py:227) and generator states.  Exact but sequential (one dependent float64 add per token
+    and centre): the parity start, ~0.4 s per Wan2.2 layer, where the default device seeding takes 1.7 ms."""
+    qb = q.reshape(-1, q.shape[-2], q.shape[-1]).to(torch.bfloat16).contiguous()
+    kb = k.reshape(-1, k.shape[-2], k.shape[-1]).to(torch.bfloat16).contiguous()
+    seeds = [side_seeds(seed + b) for b in range(qb.shape[0])]
+    return (reference_start(qb, n_q_clusters, [s_[0] for s_ in seeds]),
+            reference_start(kb, n_k_clusters, [s_[1] for s_ in seeds]))
 
 
 def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_init=None,
@@ -84,11 +82,11 @@ def svg_ear_attention(q, k, v, n_q_clusters, n_k_clusters, budget, *, seed=0, q_
              budget_mode="perClusterTopP" it is the per-query-cluster score mass p in (0, 1]
              (router.DensityBudget.top_p, router.py:63-65 — the paper's production setting p=0.85).
     init   : "device" (default) -> k-means++ on a strided subsample, on the device, inside the one
-             C-ABI call; "reference" -> k-means++ centres drawn with the reference's RNG recipe
-             from `seed` — the parity switch: it copies Q and K to the HOST and runs O(C*S*d)
-             float64 numpy per instance, so it is for tests at small shapes only; "strided" ->
-             evenly strided tokens; ignored for a side whose q_init / k_init ([.., C, d] float32
-             centres) is given.
+             C-ABI call; "reference" -> the k-means++ centres the reference draws from `seed`
+             (numpy's PCG64 draw reproduced bit for bit on the device, svgear_kmeans_seed_reference) —
+             the parity switch: exact at any scale but sequential (~0.4 s per Wan2.2 layer);
+             "strided" -> evenly strided tokens; ignored for a side whose q_init / k_init
+             ([.., C, d] float32 centres) is given.
     seed   : instance (b, h) of a [B, H, S, d] call is seeded by `seed + g` with the GLOBAL
              instance index g = b * total_heads + head_offset + h.
     head_offset, total_heads : for a caller that holds only heads [head_offset, head_offset + H)

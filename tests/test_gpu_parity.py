@@ -562,6 +562,59 @@ class TestPropertiesAtScale:
             assert bool(torch.isfinite(out.float()).all())
 
 
+class TestReferenceSeedingOnDevice:
+    """the reference's k-means++ draw (numpy PCG64 integers / choice(p=), float64 pairwise
+    sums, sequential cumsum) reproduced on the device must pick the SAME tokens as the reference's own
+    `_kmeans_pp_init` restated in host numpy (`seeded_start`, pinned to the reference in test_oracle_pinned)."""
+
+    @pytest.mark.parametrize("n,d,k,seed,dups", [
+        (9, 64, 3, 0, False), (100, 64, 100, 1, False), (257, 128, 12, 12345, False), (1000, 64, 40, 7, True),
+        (4099, 128, 64, 2**31 - 5, False), (2048, 128, 33, 99, True), (130, 64, 9, 3, False)])
+    def test_picks_equal_numpy(self, n, d, k, seed, dups):
+        rng = np.random.default_rng(n + k)
+        xs = []
+        for h in range(3):
+            x = O.round_to_bf16(rng.normal(size=(n, d)) * rng.uniform(0.2, 3.0))
+            if dups:  # duplicate tokens: zero distances, the "lowest unused index" branch when k is large
+                x[n // 3:] = x[: n - n // 3]
+            xs.append(x)
+        seeds = [seed, seed + 1, 10 * seed + 3]
+        got, picks = P.reference_start(dev(np.stack(xs)), k, seeds, return_picks=True)
+        for h in range(3):
+            want = P.seeded_start(xs[h], k, seeds[h])
+            assert np.array_equal(host(got[h]).astype(np.float64), want), (h, host(picks[h])[:8])
+            assert np.array_equal(xs[h][host(picks[h])], want)
+
+    def test_all_tokens_identical_takes_lowest_unused_indices(self):
+        x = np.tile(O.round_to_bf16(np.random.default_rng(0).normal(size=(1, 64))), (50, 1))
+        got, picks = P.reference_start(dev(x), 5, 4, return_picks=True)
+        first = int(host(picks)[0])
+        rest = [i for i in range(50) if i != first][:4]
+        assert host(picks).tolist() == [first] + rest
+        assert np.array_equal(host(got).astype(np.float64), P.seeded_start(x, 5, 4))
+
+    def test_restart_streams_and_operator_switch(self):
+        rng = np.random.default_rng(5)
+        x = O.round_to_bf16(rng.normal(size=(600, 64)))
+        for restart in (0, 1, 2):
+            want = P.seeded_start(x, 7, 11, restart)
+            assert np.array_equal(host(P.reference_start(dev(x), 7, 11, restart)).astype(np.float64), want)
+        # the operator's init="reference" starts from exactly the centres the oracle derives for the seed
+        q, k, v = (O.round_to_bf16(t) for t in O.blob_instance(800, 800, 64, 6, 10, 0.2, 1))
+        _, _, aux = P.svg_ear_attention(dev(q), dev(k), dev(v), 6, 10, 0.25, seed=21, init="reference", return_aux=True)
+        qi, ki = O.reference_init_centres(q, k, 6, 10, 21)
+        assert np.array_equal(host(aux["q_init"]).astype(np.float64), qi)
+        assert np.array_equal(host(aux["k_init"]).astype(np.float64), ki)
+
+    def test_at_the_benched_token_count(self):
+        """Seed-faithful centres at S = 75,600 (the host draw needs O(k S d) float64 numpy per head)."""
+        rng = np.random.default_rng(8)
+        x = O.round_to_bf16(rng.normal(size=(75600, 128)))
+        got, picks = P.reference_start(dev(x), 6, 2024, return_picks=True)
+        want = P.seeded_start(x, 6, 2024)
+        assert np.array_equal(host(got).astype(np.float64), want), host(picks)
+
+
 class TestBenchedShapes:
     """One head at the shapes bench.py reports (BASELINE configs 2 and 3): the oracle is far too slow
     there, so the checks are the size-independent ones — rho = 1 equals dense attention, the bf16

@@ -16,4 +16,6 @@ run racecheck "TestExecutor and not large" tests/test_gpu_parity.py
 run racecheck "executor_random_masks" tests/test_gpu_fuzz.py
 run racecheck "duplicate_tokens_repair or BoundedLloyd or DeviceSeeding" tests/test_gpu_parity.py
 run racecheck "TestEstimator" tests/test_gpu_parity.py
+run memcheck "ReferenceSeeding and not benched" tests/test_gpu_parity.py
+run racecheck "ReferenceSeeding and picks_equal_numpy and (9-64 or 257 or 1000)" tests/test_gpu_parity.py
 cat $OUT
