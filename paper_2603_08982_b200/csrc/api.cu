@@ -21,7 +21,7 @@ void report_cuda_error(cudaError_t e, const char* file, int line) {
 namespace {
 // Helper streams are keyed by (lane, slot): a lane belongs to one caller stream, so that calls issued
 // on different streams (head groups running concurrently) do not serialise on a shared helper.
-constexpr int kHelperSlots = 2;
+constexpr int kHelperSlots = 3;  // 0: key side, 1: attention remainder tiles, 2: everything before attention ("front")
 constexpr int kHelperLanes = 16;
 std::mutex g_lane_mu;
 cudaStream_t g_lane_owner[kHelperLanes];
@@ -43,15 +43,24 @@ int lane_of(cudaStream_t main) {
 }
 }  // namespace
 
-HelperFork::HelperFork(cudaStream_t main, int slot)
-    : main_(main), side_(nullptr), slot_(lane_of(main) * kHelperSlots + slot), ok_(false), joined_(false) {
+HelperFork::HelperFork(cudaStream_t main, int slot, cudaStream_t from)
+    : main_(from ? from : main), side_(nullptr), slot_(lane_of(main) * kHelperSlots + slot), ok_(false), joined_(false) {
   std::mutex& mu = (&g_helper_mu[0][0])[slot_];
   cudaStream_t& hs = (&g_helper_stream[0][0])[slot_];
   cudaEvent_t& ef = (&g_helper_fork[0][0])[slot_];
   cudaEvent_t& ej = (&g_helper_join[0][0])[slot_];
   mu.lock();
+  (void)slot;
   if (!hs) {
-    if (cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking) != cudaSuccess ||
+    // The streams that carry the work BEFORE the attention kernel (slots 0 and 2) get the highest
+    // priority: when two calls run side by side (head groups on two streams), one call's short
+    // latency-bound kernels are then scheduled into SMs as the other call's attention CTAs retire,
+    // instead of queueing behind its whole grid.  Slot 1 (attention remainder tiles) stays at the
+    // default, lowest, priority, like the caller's stream that carries the main attention kernel.
+    int prio_lo = 0, prio_hi = 0;
+    (void)cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    const int prio = (slot % kHelperSlots) == 1 ? prio_lo : prio_hi;
+    if (cudaStreamCreateWithPriority(&hs, cudaStreamNonBlocking, prio) != cudaSuccess ||
         cudaEventCreateWithFlags(&ef, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ej, cudaEventDisableTiming) != cudaSuccess) {
       hs = nullptr;
@@ -437,8 +446,13 @@ int forward_impl(const SvgEarShape* shape, const void* q, const void* k, const v
   int rc_k = SVGEAR_ECUDA;
   rc = SVGEAR_ECUDA;
   const bool keys_early = exec_mode == SVGEAR_EXEC_BF16_TENSOR;
+  // everything before the attention kernel runs on high-priority helper streams ("front" for the query
+  // side, estimator and routing; slot 0 for the key side), the attention kernel on the caller's stream
+  HelperFork ff(st, 2);
+  if (!ff.ok()) return SVGEAR_ECUDA;
+  cudaStream_t front = ff.side();
   {
-    HelperFork fk(st, 0);
+    HelperFork fk(st, 0, front);
     if (!fk.ok()) return SVGEAR_ECUDA;
     cudaStream_t side = fk.side();
     rc_k = sp ? launch_seed(s.bh, s.n_k, s.d, s.c_k, sp->oversample, (const bf16*)k, sp->seed + 0x9E37u, sp->first,
@@ -456,32 +470,33 @@ int forward_impl(const SvgEarShape* shape, const void* q, const void* k, const v
     if (!rc_k && keys_early)
       rc_k = launch_error_table_keys(s, estimator_mode, k_cent, v_cent, p.kp, p.vp, k_sizes, k_offsets, p.es, side);
     rc = sp ? launch_seed(s.bh, s.n_q, s.d, s.c_q, sp->oversample, (const bf16*)q, sp->seed, sp->first, q_init,
-                          p.q_gram, st)
+                          p.q_gram, front)
             : SVGEAR_OK;
     if (!rc)
       rc = launch_kmeans(exec_mode, s.bh, s.n_q, s.d, s.c_q, (const bf16*)q, q_init, kmeans_iters, q_assign,
-                         q_perm, q_sizes, q_offsets, q_cent, q_iters, nullptr, p.km, st);
-    if (!rc) rc = launch_gather_rows(s.bh, s.n_q, s.d, (const bf16*)q, q_perm, p.qp, st);
+                         q_perm, q_sizes, q_offsets, q_cent, q_iters, nullptr, p.km, front);
+    if (!rc) rc = launch_gather_rows(s.bh, s.n_q, s.d, (const bf16*)q, q_perm, p.qp, front);
     // join unconditionally so that the helper stream never outlives the caller's ordering
     if (fk.join() != SVGEAR_OK) rc = SVGEAR_ECUDA;
   }
   if (rc) return rc;
   if (rc_k) return rc_k;
-  if (a.kmeans_done_event) SVG_CUDA_OK(cudaEventRecord((cudaEvent_t)a.kmeans_done_event, st));
+  if (a.kmeans_done_event) SVG_CUDA_OK(cudaEventRecord((cudaEvent_t)a.kmeans_done_event, front));
   // (2) error table + routing
   rc = launch_error_table(s, exec_mode, estimator_mode, q_cent, k_cent, v_cent, p.kp, p.vp, q_sizes,
-                          k_sizes, k_offsets, err, stab, p.es, st, keys_early);
+                          k_sizes, k_offsets, err, stab, p.es, front, keys_early);
   if (rc) return rc;
   if (top_p > 0.0) {  // per-query-cluster top-p budget (router.py:172-190); the key buffer holds the masses
     double* mass = reinterpret_cast<double*>(p.route_keys);
-    rc = launch_score_mass(s, q_cent, k_cent, k_sizes, mass, st);
+    rc = launch_score_mass(s, q_cent, k_cent, k_sizes, mass, front);
     if (rc) return rc;
     rc = launch_route_top_p(s, err, mass, q_sizes, k_sizes, top_p, overshoot, single_item_fallback ? 1 : 0, mask,
-                            entries, st);
+                            entries, front);
   } else {
     rc = launch_route(s.bh, s.c_q, s.c_k, err, q_sizes, k_sizes, capacity_entries, overshoot,
-                      single_item_fallback ? 1 : 0, 0, mask, entries, p.route_keys, st);
+                      single_item_fallback ? 1 : 0, 0, mask, entries, p.route_keys, front);
   }
+  if (ff.join() != SVGEAR_OK && !rc) rc = SVGEAR_ECUDA;
   if (rc) return rc;
   // (3) fused executor, output scattered to original token order
   return launch_attend(s, exec_mode, p.qp, p.kp, p.vp, q_perm, q_sizes, q_offsets, k_sizes, k_offsets,

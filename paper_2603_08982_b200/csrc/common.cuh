@@ -100,7 +100,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 // Event based, so the pattern is capturable in a CUDA graph.
 class HelperFork {
  public:
-  HelperFork(cudaStream_t main, int slot);
+  // `main` keys the lane (one set of helper streams per caller stream); the helper forks from and joins
+  // back to `from` (default: main) — a helper can itself be forked from another helper of the lane
+  HelperFork(cudaStream_t main, int slot, cudaStream_t from = nullptr);
   ~HelperFork();
   bool ok() const { return ok_; }
   cudaStream_t side() const { return side_; }
