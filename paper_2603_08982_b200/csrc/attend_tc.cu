@@ -18,16 +18,19 @@ using namespace tc;
 namespace {
 
 constexpr int BM = 256;      // query rows per CTA: two M=128 halves that share every K/V tile
-constexpr int BN = 64;       // keys per tile
+constexpr int BN = 64;       // keys per softmax chunk (one S buffer); a K/V tile holds G chunks
 constexpr int threads_for(int halves) { return (4 * halves + 2 + halves) * 32; }  // softmax + 2 producers + issuers
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef SVG_ABL
+#define SVG_ABL 0  // ablation bits for tools/attend_ablate.sh (timing only, results are garbage): 1 no softmax
+#endif             // arithmetic, 2 never redo, 4 no QK^T MMAs, 8 no P.V MMAs, 16 no K/V loads, 32 one box per slab
 
-template <int D, int NS, int HALVES>
+template <int D, int NS, int HALVES, int G>
 struct Smem {
   static constexpr int kQBytes = HALVES * 128 * D * 2;
-  static constexpr int kTileBytes = BN * D * 2;
+  static constexpr int kTileBytes = G * BN * D * 2;
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kQBytes;             // NS stages
   static constexpr int kV = kK + NS * kTileBytes;     // NS stages
@@ -76,10 +79,16 @@ struct TmaSet {
 //   warp  9   : Q tile, then V producer
 //   warps 10,11 : one elected tcgen05.mma issuer per half (warp 10 also allocates TMEM)
 // TMEM columns: S[half][buf] at half*128 + buf*64 (64 fp32 columns; P (bf16) overwrites the first 32
-// and is the A operand of P.V straight from TMEM), O[half] at 256 + half*D.  S is double buffered
-// per half, so QK^T of tile t+1 runs under the softmax of tile t; the two halves interleave on the
-// tensor pipe.  The running maximum is only raised when it grows by more than 2^8 (lazy rescale).
-template <int D, int NS, int HALVES>
+// and is the A operand of P.V straight from TMEM), O[half] at 256 + half*D.  The softmax always works
+// on 64-key CHUNKS, one per S buffer.  The running maximum is only raised when it grows by more than
+// 2^8 (lazy rescale).
+//   G = 1: a K/V tile is one chunk; QK^T (N = 64) of chunk u+1 runs under the softmax of chunk u (S
+//          double buffered per half).  Each N = 64 MMA re-reads its 4 KB slice of Q for 2 KB of K:
+//          192 B/clk of shared-memory operand traffic against 128 available, QK^T runs at 2/3 rate.
+//   G = 2: a K/V tile is two chunks; ONE N = 128 QK^T per tile fills both S buffers (128 B/clk), issued
+//          after the P.V of the previous tile's second chunk; the softmax of a half then alternates
+//          with the other half's MMAs on the tensor pipe (the two halves ping-pong).
+template <int D, int NS, int HALVES, int G>
 __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
     attend_tc_kernel(const __grid_constant__ TmaSet tm, int oob_row,
                      const float* __restrict__ lnw, const int32_t* __restrict__ q_perm,
@@ -88,7 +97,8 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
                      const int32_t* __restrict__ tile_count, int max_tiles, int n_q, int n_k, int c_q,
                      int c_k, int ckpad, float scale_log2e, bf16* __restrict__ out,
                      float* __restrict__ lse) {
-  using L = Smem<D, NS, HALVES>;
+  using L = Smem<D, NS, HALVES, G>;
+  constexpr int TK = G * BN;  // keys per K/V tile
   constexpr int halves = HALVES;
   constexpr int kSoftWarps = 4 * HALVES, kWarpK = kSoftWarps, kWarpV = kSoftWarps + 1, kWarpMma = kSoftWarps + 2;
   constexpr int kTmemCols = 256 * HALVES, kOBase = 128 * HALVES;
@@ -163,7 +173,7 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
       s_total[1] = nsel;
     }
   } else if (warp >= 1 && warp < kSoftWarps) {
-    for (int j = tid - 32; j < ckpad; j += (kSoftWarps - 1) * 32)
+    for (int j = tid - 32; j < ckpad + (G - 1) * BN; j += (kSoftWarps - 1) * 32)
       s_bias[j] = (j < c_k && mrow[j] == 0) ? lnw[(size_t)h * c_k + j] * kLog2e : -INFINITY;
   }
   tc_fence_before();
@@ -171,8 +181,8 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int total_keys = s_total[0];
-  const int n_exact = (total_keys + BN - 1) / BN;
-  const int n_cent = ckpad / BN;
+  const int n_exact = (total_keys + TK - 1) / TK;  // K/V tiles of selected keys
+  const int n_cent = (ckpad + TK - 1) / TK;          // K/V tiles of centroids
   const int T = n_exact + n_cent;
 
   if (warp == kWarpK || warp == kWarpV) {
@@ -201,19 +211,30 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
         if (t >= NS) mbar_wait(bar(b_empty + st), ((t / NS) - 1) & 1);
         const uint32_t dst = sbuf + (uint32_t)st * L::kTileBytes;
         const uint32_t fb = bar(b_full + st);
+        if (SVG_ABL & 16) {  // no K/V traffic at all
+          mbar_arrive(fb);
+          continue;
+        }
         mbar_expect_tx(fb, (uint32_t)L::kTileBytes);
+        if (SVG_ABL & 32) {  // same bytes, one 64-row box per slab
+#pragma unroll
+          for (int sl = 0; sl < SLABS; ++sl)
+            for (int g = 0; g < G; ++g)
+              tma_box(dst + (uint32_t)(g * (BN * 128) + sl * (TK * 128)), maps + 6, sl * 64, rowbase + (int)(((long long)(t * G + g) * 64 + blockIdx.x * 192) % (n_k - 64)), fb);
+          continue;
+        }
         if (t < n_exact) {
-          int u = t * BN;
-          const int uend = min(u + BN, total_keys);
+          int u = t * TK;
+          const int uend = min(u + TK, total_keys);
           while (u < uend) {
             while (s_pre[cur + 1] <= u) ++cur;
             int len = min(s_pre[cur + 1], uend) - u;
             int src = rowbase + s_row[cur] + (u - s_pre[cur]);
             while (len > 0) {  // largest power-of-two box first
-              const int b = 31 - __clz(len), nb = 1 << b;
-              const uint32_t d0 = dst + (uint32_t)((u - t * BN) * 128);
+              const int b = min(31 - __clz(len), 6), nb = 1 << b;
+              const uint32_t d0 = dst + (uint32_t)((u - t * TK) * 128);
 #pragma unroll
-              for (int sl = 0; sl < SLABS; ++sl) tma_box(d0 + (uint32_t)(sl * (BN * 128)), maps + b, sl * 64, src, fb);
+              for (int sl = 0; sl < SLABS; ++sl) tma_box(d0 + (uint32_t)(sl * (TK * 128)), maps + b, sl * 64, src, fb);
               u += nb;
               src += nb;
               len -= nb;
@@ -221,19 +242,24 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
           }
           // ragged last tile: the remaining slots are filled with zeros (out-of-bounds boxes); their
           // logits are masked to -inf, and 0 * finite keeps the P.V accumulation clean
-          int slot = uend - t * BN, pad = BN - slot;
+          int slot = uend - t * TK, pad = TK - slot;
           while (pad > 0) {
-            const int b = 31 - __clz(pad), nb = 1 << b;
+            const int b = min(31 - __clz(pad), 6), nb = 1 << b;
 #pragma unroll
             for (int sl = 0; sl < SLABS; ++sl)
-              tma_box(dst + (uint32_t)(slot * 128 + sl * (BN * 128)), maps + b, sl * 64, oob_row, fb);
+              tma_box(dst + (uint32_t)(slot * 128 + sl * (TK * 128)), maps + b, sl * 64, oob_row, fb);
             slot += nb;
             pad -= nb;
           }
         } else {
+          // (with G = 2 the last centroid tile may run 64 rows into the next instance's centroids, or
+          // past the array: zero filled; those columns carry a -inf bias)
 #pragma unroll
-          for (int sl = 0; sl < SLABS; ++sl)
-            tma_box(dst + (uint32_t)(sl * (BN * 128)), cmap, sl * 64, h * ckpad + (t - n_exact) * BN, fb);
+          for (int g = 0; g < G; ++g)
+#pragma unroll
+            for (int sl = 0; sl < SLABS; ++sl)
+              tma_box(dst + (uint32_t)(g * (BN * 128) + sl * (TK * 128)), cmap, sl * 64,
+                      h * ckpad + (t - n_exact) * TK + g * BN, fb);
         }
       }
     }
@@ -244,7 +270,7 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
     // half never stalls the other half's MMAs; K/V stages are released by both (count = halves).
     const int hf = warp - kWarpMma;
     if (hf < halves && elect_one()) {
-      constexpr uint32_t idesc_qk = make_idesc(128, BN, 0);
+      constexpr uint32_t idesc_qk = make_idesc(128, TK, 0);
       constexpr uint32_t idesc_pv = make_idesc(128, D, 1);
       const uint32_t qb = sQ + (uint32_t)(hf * (128 * D * 2));
       const uint32_t tSb = tmem + (uint32_t)(hf * 128);
@@ -254,35 +280,42 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
         mbar_wait(bar(B::KFULL + st), (t / NS) & 1);
         tc_fence_after();
         const uint32_t kb = sK + (uint32_t)st * L::kTileBytes;
-        const uint32_t tS = tSb + (uint32_t)((t & 1) * 64);
+        const uint32_t tS = tSb + (uint32_t)(G == 1 ? (t & 1) * 64 : 0);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint64_t ad = make_desc(qb + (uint32_t)((kk >> 2) * (128 * 128) + (kk & 3) * 32), 16, 1024);
-          const uint64_t bd = make_desc(kb + (uint32_t)((kk >> 2) * (BN * 128) + (kk & 3) * 32), 16, 1024);
-          umma_ss(tS, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
+          const uint64_t bd = make_desc(kb + (uint32_t)((kk >> 2) * (TK * 128) + (kk & 3) * 32), 16, 1024);
+          if (!(SVG_ABL & 4)) umma_ss(tS, ad, bd, idesc_qk, kk > 0 ? 1u : 0u);
         }
-        umma_commit(bar(B::SFULL + hf * 2 + (t & 1)));
+        umma_commit(bar(B::SFULL + hf * 2 + (G == 1 ? (t & 1) : 0)));
         umma_commit(bar(B::KEMPTY + st));
       };
       mbar_wait(bar(B::QFULL), 0);
       issue_qk(0);
       for (int t = 0; t < T; ++t) {
         const int st = t % NS;
-        if (t + 1 < T) issue_qk(t + 1);
+        if (G == 1 && t + 1 < T) issue_qk(t + 1);
         mbar_wait(bar(B::VFULL + st), (t / NS) & 1);
-        mbar_wait(bar(B::PFULL + hf * 2 + (t & 1)), (t >> 1) & 1);
-        tc_fence_after();
         const uint32_t vb = sV + (uint32_t)st * L::kTileBytes;
-        const uint32_t tP = tSb + (uint32_t)((t & 1) * 64);
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          // V tile [64 keys x D] is the MN-major B operand: 16 keys per MMA = 2048 B along K,
-          // LBO = stride between the 64-column slabs, SBO = stride between 8-key groups
-          const uint64_t bd = make_desc(vb + (uint32_t)(kk * 2048), BN * 128, 1024);
-          umma_ts(tO, tP + (uint32_t)(kk * 8), bd, idesc_pv, (t > 0 || kk > 0) ? 1u : 0u);
+        for (int g = 0; g < G; ++g) {
+          const int u = t * G + g;  // chunk
+          mbar_wait(bar(B::PFULL + hf * 2 + (u & 1)), (u >> 1) & 1);
+          tc_fence_after();
+          const uint32_t tP = tSb + (uint32_t)((u & 1) * 64);
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk) {
+            // V tile [TK keys x D] is the MN-major B operand: 16 keys per MMA = 2048 B along K,
+            // LBO = stride between the 64-column slabs, SBO = stride between 8-key groups
+            const uint64_t bd = make_desc(vb + (uint32_t)((g * (BN / 16) + kk) * 2048), TK * 128, 1024);
+            if (!(SVG_ABL & 8)) umma_ts(tO, tP + (uint32_t)(kk * 8), bd, idesc_pv, (u > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(bar(B::ODONE + hf));
         }
-        umma_commit(bar(B::ODONE + hf));
         umma_commit(bar(B::VEMPTY + st));
+        // the N = 128 QK^T overwrites both S buffers: it follows the P.V of this tile's second chunk
+        // (tensor-pipe order), and the softmax warps have read all of S(t) before they hand over P
+        if (G == 2 && t + 1 < T) issue_qk(t + 1);
       }
       umma_commit(bar(B::OFINAL + hf));
     }
@@ -301,16 +334,21 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
     // block maxima are collected on the side and, only if some row of the warp has to raise m
     // (tile max > m + 2^8, rare after the first tiles), the tile is redone from TMEM the exact way.
     uint32_t sa[32], sb[32], pk[32];
-    const int last_valid = total_keys - (n_exact - 1) * BN;  // valid columns of the last exact tile
+    // chunk t (64 keys) lives in S buffer t & 1.  With G = 1 every chunk has its own QK^T and SFULL
+    // phase; with G = 2 one QK^T fills both buffers and only even chunks wait (one barrier per half).
+    const int U = T * G, u_exact = n_exact * G;  // chunks in all / chunks of selected keys (incl. padding)
+    auto sfull_bar = [&](int t) -> uint32_t { return bar(b_sfull + (G == 1 ? (t & 1) : 0)); };
     mbar_wait(bar(b_sfull), 0);
     tc_fence_after();
     TMEM_LD32(tSb, sa);
-    for (int t = 0; t < T; ++t) {
+    for (int t = 0; t < U; ++t) {
       const int st = t & 1;
       const uint32_t tS = tSb + (uint32_t)(st * 64);
-      // tile kind: 0 = full exact tile (raw logits), 1 = last exact tile (ragged), 2 = centroid tile
-      const int kind = t < n_exact - 1 ? 0 : (t < n_exact ? 1 : 2);
-      const float* bias = s_bias + (kind == 2 ? (t - n_exact) * BN : 0);
+      // chunk kind: 0 = 64 selected keys (raw logits), 1 = ragged or empty tail of the selected keys,
+      // 2 = centroids
+      const int last_valid = total_keys - t * BN;  // valid columns of an exact chunk (may be <= 0)
+      const int kind = t >= u_exact ? 2 : (last_valid >= BN ? 0 : 1);
+      const float* bias = s_bias + (kind == 2 ? (t - u_exact) * BN : 0);
       const float mu = (m == -INFINITY) ? 0.f : m;
       float sum0 = 0.f, sum1 = 0.f, sum2 = 0.f, sum3 = 0.f;
       float x2 = -INFINITY, x3 = -INFINITY;  // block maxima of the biased tiles (log2 domain)
@@ -373,17 +411,22 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
           }
         }
       };
-      block(sa, 0, 0);
+      if (!(SVG_ABL & 1)) block(sa, 0, 0);
       tc_wait_ld();                 // sb landed
       // first block of the next tile: prefetch it under the arithmetic on sb if S(t+1) is already
       // there (warp-uniform decision), otherwise right after this block
-      bool fetched = t + 1 >= T;
-      if (!fetched && __all_sync(0xffffffffu, mbar_test(bar(b_sfull + (st ^ 1)), ((t + 1) >> 1) & 1))) {
+      bool fetched = t + 1 >= U;
+      if (!fetched && ((G == 2 && st == 0) ||
+                       __all_sync(0xffffffffu, mbar_test(sfull_bar(t + 1), ((t + 1) >> 1) & 1)))) {
         tc_fence_after();
         TMEM_LD32(tSb + (uint32_t)((st ^ 1) * 64), sa);
         fetched = true;
       }
-      block(sb, 32, 16);
+      if (!(SVG_ABL & 1)) block(sb, 32, 16);
+      else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pk[j] = sa[j] ^ sb[j];
+      }
       float sum = (sum0 + sum1) + (sum2 + sum3);
       // Lazy running max: m only moves when a logit exceeds it by more than 2^kRescaleThreshold.  Full
       // exact tiles do not track their maximum (one FMNMX per logit on the softmax warps' critical
@@ -394,7 +437,7 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
       const float mt_known = fmaxf(x2, x3);
       const bool maybe = kind == 0 ? !(sum <= 16384.f) || m == -INFINITY
                                    : (mt_known > m + kRescaleThreshold || (m == -INFINITY && mt_known > -INFINITY));
-      const bool redo = __any_sync(0xffffffffu, maybe);
+      const bool redo = (SVG_ABL & 2) ? false : __any_sync(0xffffffffu, maybe);
       if (redo) {
         // exact path for the whole warp: tile maximum, raise m where needed, exponentials again
         tc_wait_ld();  // keep the prefetched block of tile t+1 intact in sa
@@ -456,7 +499,7 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
       tc_fence_before();
       if (lane == 0) mbar_arrive(bar(b_pfull + st));
       if (!fetched) {
-        mbar_wait(bar(b_sfull + (st ^ 1)), ((t + 1) >> 1) & 1);
+        mbar_wait(sfull_bar(t + 1), ((t + 1) >> 1) & 1);
         tc_fence_after();
         TMEM_LD32(tSb + (uint32_t)((st ^ 1) * 64), sa);
       }
@@ -527,7 +570,7 @@ bool encode_rows_map(CUtensorMap* tm, const void* base, uint64_t rows, int d, in
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int D, int NS2, int NS1>
+template <int D, int NS2, int G2, int NS1>
 static int launch_attend_tc_ns(const SvgEarShape& s, const TmaSet& tm, const int32_t* q_perm,
                                const int32_t* k_sizes, const int32_t* k_offsets, const uint8_t* mask, bf16* out,
                                float* lse, AttendScratch& sc, int ckpad, int mt, float scale_log2e,
@@ -536,18 +579,18 @@ static int launch_attend_tc_ns(const SvgEarShape& s, const TmaSet& tm, const int
   if (!fk.ok()) return SVGEAR_ECUDA;
   cudaStream_t side = fk.side();
   // tiles with more than 128 live rows: one CTA per SM, two halves sharing every K/V tile
-  const size_t smem2 = Smem<D, NS2, 2>::bytes(ckpad);
-  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-  attend_tc_kernel<D, NS2, 2><<<dim3(mt, s.bh), threads_for(2), smem2, st>>>(
+  const size_t smem2 = Smem<D, NS2, 2, G2>::bytes(ckpad);
+  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS2, 2, G2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  attend_tc_kernel<D, NS2, 2, G2><<<dim3(mt, s.bh), threads_for(2), smem2, st>>>(
       tm, s.bh * s.n_k, sc.lnw, q_perm, k_sizes, k_offsets, mask, sc.tile_list, sc.tile_count, mt, s.n_q, s.n_k,
       s.c_q, s.c_k, ckpad, scale_log2e, out, lse);
   SVG_LAUNCH_OK();
   // remainder tiles (<= 128 live rows): one half per CTA, two CTAs co-resident per SM so that one
   // CTA's softmax runs under the other's MMAs.  The two kernels write disjoint rows; the second is
   // forked onto a helper stream so that its CTAs fill the tail of the first instead of following it.
-  const size_t smem1 = Smem<D, NS1, 1>::bytes(ckpad);
-  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
-  attend_tc_kernel<D, NS1, 1><<<dim3(mt < s.c_q ? mt : s.c_q, s.bh), threads_for(1), smem1, side>>>(
+  const size_t smem1 = Smem<D, NS1, 1, 1>::bytes(ckpad);
+  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS1, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+  attend_tc_kernel<D, NS1, 1, 1><<<dim3(mt < s.c_q ? mt : s.c_q, s.bh), threads_for(1), smem1, side>>>(
       tm, s.bh * s.n_k, sc.lnw, q_perm, k_sizes, k_offsets, mask, sc.tile_list, sc.tile_count, mt, s.n_q, s.n_k,
       s.c_q, s.c_k, ckpad, scale_log2e, out, lse);
   SVG_LAUNCH_OK();
@@ -573,15 +616,20 @@ int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const
   ok = ok && encode_rows_map(&tm.q, qp, (uint64_t)s.bh * s.n_q, s.d, 64);
   if (!ok) return SVGEAR_ECUDA;
   const size_t cap = 227 * 1024;
-#define SVG_TRY(DD, N2, N1)                                                                               \
-  if (s.d == DD && Smem<DD, N2, 2>::bytes(ckpad) <= cap && Smem<DD, N1, 1>::bytes(ckpad) <= cap)          \
-    return launch_attend_tc_ns<DD, N2, N1>(s, tm, q_perm, k_sizes, k_offsets, mask, out, lse, sc, ckpad, mt, \
-                                           scale_log2e, st);
-  SVG_TRY(128, 4, 2)
-  SVG_TRY(128, 3, 2)
-  SVG_TRY(128, 2, 2)
-  SVG_TRY(64, 4, 4)
-  SVG_TRY(64, 2, 2)
+#define SVG_TRY(DD, N2, GG, N1)                                                                           \
+  if (s.d == DD && (GG == 1 || !force_g1) && Smem<DD, N2, 2, GG>::bytes(ckpad) <= cap &&                   \
+      Smem<DD, N1, 1, 1>::bytes(ckpad) <= cap)                                                             \
+    return launch_attend_tc_ns<DD, N2, GG, N1>(s, tm, q_perm, k_sizes, k_offsets, mask, out, lse, sc, ckpad, mt, \
+                                               scale_log2e, st);
+  // SVGEAR_ATTEND_G=2 selects the 128-key-tile variant of the two-half kernel (measured slower, DESIGN 4.1)
+  static const bool force_g1 = [] { const char* e = getenv("SVGEAR_ATTEND_G"); return !(e && e[0] == '2'); }();
+  SVG_TRY(128, 2, 2, 2)
+  SVG_TRY(128, 4, 1, 2)
+  SVG_TRY(128, 3, 1, 2)
+  SVG_TRY(128, 2, 1, 2)
+  SVG_TRY(64, 3, 2, 4)
+  SVG_TRY(64, 4, 1, 4)
+  SVG_TRY(64, 2, 1, 2)
 #undef SVG_TRY
   return SVGEAR_EUNSUPPORTED;
 }

@@ -399,7 +399,13 @@ int launch_kmeans_assign_tc(int bh, int n, int d, int c, int iter, const bf16* x
   for (int h0 = 0; h0 < bh; h0 += kMaxHeads) {
     const int nb = bh - h0 < kMaxHeads ? bh - h0 : kMaxHeads;
     const int items = nb * ceil_div(n, KM);  // upper bound; the kernel reads the real counts
-    const int grid = items < num_sms ? items : num_sms;
+    // SVGEAR_ASSIGN_GRID / SVGEAR_ASSIGN_GRID0: cap of the persistent grid after / in the first iteration
+    // (experiment knob: a grid below the SM count lets the other side's kernels co-run)
+    static const int cap_late = [] { const char* e = getenv("SVGEAR_ASSIGN_GRID"); return e ? atoi(e) : 0; }();
+    static const int cap_first = [] { const char* e = getenv("SVGEAR_ASSIGN_GRID0"); return e ? atoi(e) : 0; }();
+    const int cap = iter == 0 ? cap_first : cap_late;
+    int grid = items < num_sms ? items : num_sms;
+    if (cap > 0 && grid > cap) grid = cap;
     const bf16* xs = x + (size_t)h0 * n * d;
     const float* cs = sc.cnorm_pad + (size_t)h0 * cpad;
     const float* xns = sc.xnorm + (size_t)h0 * n;

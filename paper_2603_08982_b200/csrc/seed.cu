@@ -192,6 +192,12 @@ __device__ __forceinline__ uint32_t hash_u32(uint32_t a, uint32_t b, uint32_t c)
 
 constexpr int kGramPer = 4;    // samples per thread (m <= 4096)
 constexpr int kGramBatch = 8;  // centres drawn per round while many remain (graded down towards the end)
+#ifndef SVG_SEED_T8
+#define SVG_SEED_T8 256
+#define SVG_SEED_T4 128
+#define SVG_SEED_T2 32
+#endif
+constexpr int kSeedT8 = SVG_SEED_T8, kSeedT4 = SVG_SEED_T4, kSeedT2 = SVG_SEED_T2;  // centres left: 8 / 4 / 2 per round
 
 __global__ void __launch_bounds__(1024)
     seed_gram_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gram, int n, int d, int c, int m,
@@ -277,7 +283,7 @@ __global__ void __launch_bounds__(1024)
     const int left = c - npicked;
     // the draws of a round share one D^2 distribution; the later a centre is drawn the more the
     // distribution it is drawn from matters, so the batch shrinks towards the end
-    const int next = left >= 256 ? kGramBatch : (left >= 128 ? 4 : (left >= 32 ? 2 : 1));
+    const int next = left >= kSeedT8 ? kGramBatch : (left >= kSeedT4 ? 4 : (left >= kSeedT2 ? 2 : 1));
     if (warp == 0) {
       float w = s_warp[lane], wi = w;
 #pragma unroll

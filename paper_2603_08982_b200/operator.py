@@ -8,6 +8,8 @@ Per (batch, head) instance this is exactly the reference's four-call composition
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 
 import numpy as np
@@ -41,6 +43,12 @@ def _auto_groups(bh, n_q, n_k):
 def _group_layout(bh, n_q, n_k, d, c_q, c_k, groups):
     """(instance bounds, per-group workspace bytes, total bytes) of a head-group split."""
     bnd = [bh * g // groups for g in range(groups + 1)]
+    frac = os.environ.get("SVGEAR_GROUP_FRACTIONS")  # experiment knob: "0.3,1.0" = cumulative shares
+    if frac and groups > 1:
+        cum = [float(x) for x in frac.split(",")]
+        if len(cum) == groups:
+            bnd = [0] + [max(1, min(bh, round(bh * c))) for c in cum]
+            bnd[-1] = bh
     nds = [_lib.workspace_bytes(_lib.Shape(bnd[g + 1] - bnd[g], n_q, n_k, d, c_q, c_k)) for g in range(groups)]
     if groups > 1:  # every group's slice starts 256-byte aligned
         nds = [(x + 255) // 256 * 256 for x in nds]
