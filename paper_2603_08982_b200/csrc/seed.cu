@@ -198,15 +198,40 @@ constexpr int kGramBatch = 8;  // centres drawn per round while many remain (gra
 #define SVG_SEED_T2 32
 #endif
 constexpr int kSeedT8 = SVG_SEED_T8, kSeedT4 = SVG_SEED_T4, kSeedT2 = SVG_SEED_T2;  // centres left: 8 / 4 / 2 per round
+// The last centres are drawn GREEDILY (greedy k-means++: several D^2 candidates per round, the one that
+// lowers the potential most is kept).  Plain D^2 sampling spends many of its last draws inside clusters
+// that already hold a centre (when u well-separated clusters are still uncovered, a draw lands in one of
+// them with probability ~ u*R / (u*R + c), R = between / within squared distance), and every such draw
+// leaves one cluster with two centres and one without - the configuration Lloyd's iteration resolves
+// slowest - the larger the clusters, the slower (a split cluster of 250 tokens keeps a Wan2.2 query side
+// iterating for 20 rounds).  A greedy round costs about two plain rounds, so their number follows the
+// cluster size: the last min(c/2, n/(2c)) centres (126 of 300 query-side, 37 of 1000 key-side centres at
+// the Wan2.2 shape).  SVG_SEED_GREEDY (compile time) overrides the count, 0 = plain sampling throughout.
+#ifndef SVG_SEED_GREEDY
+#define SVG_SEED_GREEDY -1
+#endif
+// The draws of a batched round share one D^2 distribution, so two of them can land in the same
+// uncovered cluster (probability ~ batch^2 / 2u per round).  A draw is dropped when an earlier draw of
+// its round lies closer to it than half its distance to the nearest existing centre (one Gram entry per
+// pair, read by one warp): had the round been sequential, the earlier draw would have covered it.
+// Measured at the Wan2.2 shape: query-side Lloyd iterations 438 -> 398 in sum but 15 -> 19 at most, +0.4 ms
+// of key-side seeding, layer time unchanged - off by default.
+#ifndef SVG_SEED_FILTER
+#define SVG_SEED_FILTER 0
+#endif
 
 __global__ void __launch_bounds__(1024)
     seed_gram_kernel(const bf16* __restrict__ x, const bf16* __restrict__ gram, int n, int d, int c, int m,
-                     uint32_t seed, int first, float* __restrict__ cent) {
+                     uint32_t seed, int first, int greedy_left, float* __restrict__ cent) {
   const int h = blockIdx.x;
   __shared__ float s_warp[32];
   __shared__ float s_total;
   __shared__ int s_pick[kGramBatch];
   __shared__ float s_target[kGramBatch];
+  __shared__ float s_red[32][kGramBatch + 1];  // greedy rounds: per-warp potential gains of the candidates
+  __shared__ float s_gain[kGramBatch];
+  __shared__ float s_pmind[kGramBatch];  // D^2 of the round's draws
+  __shared__ int s_cnt;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bf16* xh = x + (size_t)h * n * d;
   const bf16* gh = gram + (size_t)h * m * m;
@@ -283,7 +308,8 @@ __global__ void __launch_bounds__(1024)
     const int left = c - npicked;
     // the draws of a round share one D^2 distribution; the later a centre is drawn the more the
     // distribution it is drawn from matters, so the batch shrinks towards the end
-    const int next = left >= kSeedT8 ? kGramBatch : (left >= kSeedT4 ? 4 : (left >= kSeedT2 ? 2 : 1));
+    const bool greedy = left <= greedy_left;  // kGramBatch candidates, one centre
+    const int next = greedy ? kGramBatch : (left >= kSeedT8 ? kGramBatch : (left >= kSeedT4 ? 4 : (left >= kSeedT2 ? 2 : 1)));
     if (warp == 0) {
       float w = s_warp[lane], wi = w;
 #pragma unroll
@@ -321,6 +347,10 @@ __global__ void __launch_bounds__(1024)
               if (mind[e] > best) { best = mind[e]; chosen = s0 + e; }
           }
           atomicMax(&s_pick[i], chosen);
+          float cm = mind[0];
+#pragma unroll
+          for (int e = 1; e < kGramPer; ++e) cm = chosen == s0 + e ? mind[e] : cm;
+          s_pmind[i] = cm;  // a target lies in exactly one thread's interval
         }
       }
     }
@@ -331,20 +361,111 @@ __global__ void __launch_bounds__(1024)
       for (int i = 0; i < kGramBatch; ++i) {
         if (i < next) {
           int pk = s_pick[i];
-          if (pk < 0 || pk >= m) pk = (int)(hash_u32(seed, (uint32_t)(first + h), (uint32_t)(npicked + i) + 77777u) % (uint32_t)m);
+          if (pk < 0 || pk >= m) {
+            pk = (int)(hash_u32(seed, (uint32_t)(first + h), (uint32_t)(npicked + i) + 77777u) % (uint32_t)m);
+            s_pmind[i] = 0.f;  // fallback draws are never dropped
+          }
 #pragma unroll
           for (int j = 0; j < kGramBatch; ++j)
-            if (j < i && pk_prev[j] == pk) pk = (pk + 1 + i) % m;
+            if (j < i && pk_prev[j] == pk) { pk = (pk + 1 + i) % m; s_pmind[i] = 0.f; }
           pk_prev[i] = pk;
           s_pick[i] = pk;
         }
       }
     }
     __syncthreads();
+    int kept = next;
+    if (SVG_SEED_FILTER && !greedy && next > 1) {
+      if (warp == 0) {
+        // lane = pair (i < j) of the round's draws, i-major
+        int pi = 0, pj = 1, rem = lane;
+#pragma unroll
+        for (int i = 0; i < kGramBatch - 1; ++i) {
+          const int row = kGramBatch - 1 - i;
+          if (rem >= 0 && rem < row) { pi = i; pj = i + 1 + rem; rem = -1; }
+          else if (rem >= 0) rem -= row;
+        }
+        bool close = false;
+        if (rem < 0 && pj < next) {
+          const int a = s_pick[pi], b = s_pick[pj];
+          const float dab = fmaxf(s_diag[a] + s_diag[b] - 2.f * __bfloat162float(gh[(size_t)a * m + b]), 0.f);
+          close = dab < 0.5f * s_pmind[pj];
+        }
+        const unsigned bits = __ballot_sync(0xffffffffu, close);
+        if (lane == 0) {
+          unsigned keep = 1u;
+          int w = 1;
+          for (int j = 1; j < next; ++j) {
+            bool drop = false;
+            int idx = 0;
+            for (int i = 0; i < kGramBatch - 1; ++i)
+              for (int jj = i + 1; jj < kGramBatch; ++jj, ++idx)
+                if (jj == j && (keep >> i & 1u) && (bits >> idx & 1u)) drop = true;
+            if (!drop) {
+              keep |= 1u << j;
+              s_pick[w++] = s_pick[j];
+            }
+          }
+          s_cnt = w;
+        }
+      }
+      __syncthreads();
+      kept = s_cnt;
+    }
 #pragma unroll
     for (int i = 0; i < kGramBatch; ++i)
-      if (i < next) picks[i] = s_pick[i];
-    cnt = next;
+      if (i < kept) picks[i] = s_pick[i];
+    cnt = kept;
+    if (greedy) {
+      // potential gain of candidate i: sum over the samples of max(0, D^2 - d^2(sample, candidate)), in a
+      // fixed summation order (thread-local, warp shuffle tree, 32 warps by one warp per candidate)
+      float gain[kGramBatch];
+#pragma unroll
+      for (int i = 0; i < kGramBatch; ++i) {
+        const float nc = s_diag[picks[i]];
+        float g[kGramPer];
+        if (vec) {
+          const uint2 u = __ldg(reinterpret_cast<const uint2*>(gh + (size_t)picks[i] * m + s0));
+          g[0] = __uint_as_float(u.x << 16); g[1] = __uint_as_float(u.x & 0xffff0000u);
+          g[2] = __uint_as_float(u.y << 16); g[3] = __uint_as_float(u.y & 0xffff0000u);
+        } else {
+          const bf16* grow = gh + (size_t)picks[i] * m;
+#pragma unroll
+          for (int e = 0; e < kGramPer; ++e) g[e] = s0 + e < m ? __bfloat162float(grow[s0 + e]) : 0.f;
+        }
+        float acc = 0.f;
+#pragma unroll
+        for (int e = 0; e < kGramPer; ++e) {
+          const float d2 = (s0 + e == picks[i]) ? 0.f : fmaxf(nrm[e] + nc - 2.f * g[e], 0.f);
+          if (s0 + e < m) acc += fmaxf(mind[e] - d2, 0.f);
+        }
+        gain[i] = acc;
+      }
+#pragma unroll
+      for (int i = 0; i < kGramBatch; ++i) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gain[i] += __shfl_xor_sync(0xffffffffu, gain[i], o);
+        if (lane == 0) s_red[warp][i] = gain[i];
+      }
+      __syncthreads();
+      if (warp < kGramBatch) {
+        float v = s_red[lane][warp];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s_gain[warp] = v;
+      }
+      __syncthreads();
+      int best = 0;
+      float bg = s_gain[0];
+#pragma unroll
+      for (int i = 1; i < kGramBatch; ++i)
+        if (s_gain[i] > bg) { bg = s_gain[i]; best = i; }
+      int pk = picks[0];
+#pragma unroll
+      for (int i = 1; i < kGramBatch; ++i) pk = best == i ? picks[i] : pk;
+      picks[0] = pk;  // the next round loads its Gram row again (an L2 hit now)
+      cnt = 1;
+    }
   }
 }
 
@@ -373,7 +494,8 @@ int launch_seed(int bh, int n, int d, int c, int oversample, const bf16* x, uint
     gram_tc_kernel<64><<<grid, GTHREADS, smem, st>>>(x, n, m, gram_ws);
   }
   SVG_LAUNCH_OK();
-  seed_gram_kernel<<<bh, 1024, 0, st>>>(x, gram_ws, n, d, c, m, seed, first_instance, cent);
+  const int greedy_left = SVG_SEED_GREEDY >= 0 ? SVG_SEED_GREEDY : (c / 2 < n / (2 * c) ? c / 2 : n / (2 * c));
+  seed_gram_kernel<<<bh, 1024, 0, st>>>(x, gram_ws, n, d, c, m, seed, first_instance, greedy_left, cent);
   SVG_LAUNCH_OK();
   return SVGEAR_OK;
 }
