@@ -205,8 +205,8 @@ constexpr int kSeedT8 = SVG_SEED_T8, kSeedT4 = SVG_SEED_T4, kSeedT2 = SVG_SEED_T
 // leaves one cluster with two centres and one without - the configuration Lloyd's iteration resolves
 // slowest - the larger the clusters, the slower (a split cluster of 250 tokens keeps a Wan2.2 query side
 // iterating for 20 rounds).  A greedy round costs about two plain rounds, so their number follows the
-// cluster size: the last min(c/2, n/(2c)) centres (126 of 300 query-side, 37 of 1000 key-side centres at
-// the Wan2.2 shape).  SVG_SEED_GREEDY (compile time) overrides the count, 0 = plain sampling throughout.
+// cluster size: the last min(c/2, (n/c)^2 / 512) centres (124 of 300 query-side, 11 of 1000 key-side
+// centres at the Wan2.2 shape; key-side iteration counts do not react to more).  SVG_SEED_GREEDY (compile time) overrides the count, 0 = plain sampling throughout.
 #ifndef SVG_SEED_GREEDY
 #define SVG_SEED_GREEDY -1
 #endif
@@ -494,7 +494,8 @@ int launch_seed(int bh, int n, int d, int c, int oversample, const bf16* x, uint
     gram_tc_kernel<64><<<grid, GTHREADS, smem, st>>>(x, n, m, gram_ws);
   }
   SVG_LAUNCH_OK();
-  const int greedy_left = SVG_SEED_GREEDY >= 0 ? SVG_SEED_GREEDY : (c / 2 < n / (2 * c) ? c / 2 : n / (2 * c));
+  const long long per = n / c, quad = per * per / 512;  // greedy rounds grow with the square of the cluster size
+  const int greedy_left = SVG_SEED_GREEDY >= 0 ? SVG_SEED_GREEDY : (int)(quad < c / 2 ? quad : c / 2);
   seed_gram_kernel<<<bh, 1024, 0, st>>>(x, gram_ws, n, d, c, m, seed, first_instance, greedy_left, cent);
   SVG_LAUNCH_OK();
   return SVGEAR_OK;
