@@ -128,7 +128,8 @@ int svgear_kmeans(int32_t exec_mode, int32_t bh, int32_t n, int32_t d, int32_t c
  * keyed by (seed, first_instance + b).  This is NOT the reference's numpy draw (the Python shim
  * reproduces that one on the host for parity runs); it is deterministic.  Two kernels: the Gram
  * matrix of the subsample on the tensor cores (tcgen05), then the sequential D^2 rounds, which
- * read only the Gram rows of the centres drawn so far.
+ * read only the Gram rows of the centres drawn so far.  The last min(c/2, (n/c)^2/512) centres are
+ * drawn greedily (8 D^2 candidates per round, the one that lowers the potential most is kept).
  *   centroids [bh][c][d] f32 (out); workspace: >= bh*m*m*2 bytes (svgear_workspace_bytes covers
  *   oversample <= 8)                                                                             */
 int svgear_kmeans_seed(int32_t bh, int32_t n, int32_t d, int32_t c, const void* x,

@@ -19,7 +19,7 @@ namespace {
 
 constexpr int BM = 256;      // query rows per CTA: two M=128 halves that share every K/V tile
 constexpr int BN = 64;       // keys per softmax chunk (one S buffer); a K/V tile holds G chunks
-constexpr int threads_for(int halves) { return (4 * halves + 2 + halves) * 32; }  // softmax + 2 producers + issuers
+constexpr int threads_for(int halves, int tpr = 1) { return (4 * halves * tpr + 2 + halves) * 32; }  // softmax + 2 producers + issuers
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
@@ -27,7 +27,7 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define SVG_ABL 0  // ablation bits for tools/attend_ablate.sh (timing only, results are garbage): 1 no softmax
 #endif             // arithmetic, 2 never redo, 4 no QK^T MMAs, 8 no P.V MMAs, 16 no K/V loads, 32 one box per slab
 
-template <int D, int NS, int HALVES, int G>
+template <int D, int NS, int HALVES, int G, int TPR = 1>
 struct Smem {
   static constexpr int kQBytes = HALVES * 128 * D * 2;
   static constexpr int kTileBytes = G * BN * D * 2;
@@ -35,7 +35,8 @@ struct Smem {
   static constexpr int kK = kQ + kQBytes;             // NS stages
   static constexpr int kV = kK + NS * kTileBytes;     // NS stages
   static constexpr int kBars = kV + NS * kTileBytes;  // mbarriers + tmem ptr + counters
-  static constexpr int kLists = kBars + 512;
+  static constexpr int kXchg = kBars + 512;           // TPR = 2: [row][2] floats exchanged between the two threads of a row
+  static constexpr int kLists = kXchg + (TPR == 2 ? HALVES * 128 * 2 * 4 : 0);
   static size_t bytes(int ckpad) { return 1024 + kLists + (size_t)(ckpad + 64) * 12; }
 };
 
@@ -88,8 +89,11 @@ struct TmaSet {
 //   G = 2: a K/V tile is two chunks; ONE N = 128 QK^T per tile fills both S buffers (128 B/clk), issued
 //          after the P.V of the previous tile's second chunk; the softmax of a half then alternates
 //          with the other half's MMAs on the tensor pipe (the two halves ping-pong).
-template <int D, int NS, int HALVES, int G>
-__global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
+//   TPR = 2 (two threads per query row): 16 softmax warps, four per scheduler; the two warps of a row
+//          group (same TMEM lane quarter, hence same scheduler) take 32 columns of a chunk each and agree
+//          on the rare exact path with one named-barrier OR per chunk (see the softmax section).
+template <int D, int NS, int HALVES, int G, int TPR>
+__global__ void __launch_bounds__(threads_for(HALVES, TPR), 3 - HALVES)
     attend_tc_kernel(const __grid_constant__ TmaSet tm, int oob_row,
                      const float* __restrict__ lnw, const int32_t* __restrict__ q_perm,
                      const int32_t* __restrict__ k_sizes, const int32_t* __restrict__ k_offsets,
@@ -97,10 +101,11 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
                      const int32_t* __restrict__ tile_count, int max_tiles, int n_q, int n_k, int c_q,
                      int c_k, int ckpad, float scale_log2e, bf16* __restrict__ out,
                      float* __restrict__ lse) {
-  using L = Smem<D, NS, HALVES, G>;
+  using L = Smem<D, NS, HALVES, G, TPR>;
+  static_assert(TPR == 1 || HALVES == 2, "two threads per row: two halves");
   constexpr int TK = G * BN;  // keys per K/V tile
   constexpr int halves = HALVES;
-  constexpr int kSoftWarps = 4 * HALVES, kWarpK = kSoftWarps, kWarpV = kSoftWarps + 1, kWarpMma = kSoftWarps + 2;
+  constexpr int kSoftWarps = 4 * HALVES * TPR, kWarpK = kSoftWarps, kWarpV = kSoftWarps + 1, kWarpMma = kSoftWarps + 2;
   constexpr int kTmemCols = 256 * HALVES, kOBase = 128 * HALVES;
   using B = Bars<NS>;
   const int h = blockIdx.y;
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
     }
     for (int s = 0; s < 4; ++s) {
       mbar_init(bar(B::SFULL + s), 1);
-      mbar_init(bar(B::PFULL + s), 4);  // one elected lane per softmax warp
+      mbar_init(bar(B::PFULL + s), 4 * TPR);  // one elected lane per softmax warp
     }
     mbar_init(bar(B::ODONE), 1);
     mbar_init(bar(B::ODONE + 1), 1);
@@ -342,6 +347,193 @@ __global__ void __launch_bounds__(threads_for(HALVES), 3 - HALVES)
       }
     }
     __syncwarp();
+  } else if (TPR == 2) {
+    // =========================== softmax + epilogue, two threads per row ========================
+    // Warp w: lane quarter w & 3 (rows), half (w >> 2) >> 1, column half ch = (w >> 2) & 1: the thread
+    // owns columns 32 ch .. 32 ch + 31 of every chunk of its row.  Its 32 logits stay in registers, so
+    // the exact path re-uses them (no TMEM re-read), and P is only stored after the pair has met at the
+    // named barrier - by then both have loaded their S columns, which P overwrites.
+    const int grp = warp >> 2, hf = grp >> 1, ch = grp & 1, quad = warp & 3;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const uint32_t tSb = tmem + lane_base + (uint32_t)(hf * 128);
+    const uint32_t tO = tmem + lane_base + (uint32_t)(kOBase + hf * D + ch * (D / 2));
+    const int b_sfull = B::SFULL + hf * 2, b_pfull = B::PFULL + hf * 2, b_odone = B::ODONE + hf;
+    const int pair_bar = 1 + hf * 4 + quad;  // named barrier of the two warps of this row group
+    const int row = hf * 128 + quad * 32 + lane;
+    float* xch = reinterpret_cast<float*>(smem + L::kXchg) + row * 2;
+    float m = -INFINITY, l = 0.f;
+    uint32_t sa[32], pk[16];
+    const int U = T * G, u_exact = n_exact * G;
+    for (int t = 0; t < U; ++t) {
+      const int st = t & 1;
+      const int last_valid = total_keys - t * BN;
+      const int kind = t >= u_exact ? 2 : (last_valid >= BN ? 0 : 1);
+      const float* bias = s_bias + (kind == 2 ? (t - u_exact) * BN : 0);
+      if (G == 1 || st == 0) {  // G = 2: one QK^T fills both S buffers of the half
+        mbar_wait(bar(b_sfull + (G == 1 ? st : 0)), (t >> 1) & 1);
+        tc_fence_after();
+      }
+      TMEM_LD32(tSb + (uint32_t)(st * 64 + ch * 32), sa);
+      const float mu = (m == -INFINITY) ? 0.f : m;
+      float sum = 0.f, xk = -INFINITY;
+      tc_wait_ld();
+      if (SVG_ABL & 1) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = sa[j] ^ sa[j + 16];
+      } else if (kind == 0) {
+        const uint64_t sc2 = pack2(scale_log2e, scale_log2e), nm2 = pack2(-mu, -mu);
+        uint64_t acc01 = pack2(0.f, 0.f), acc23 = pack2(0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          float p[8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint64_t xx = ffma2(pack2(__uint_as_float(sa[j + 2 * q]), __uint_as_float(sa[j + 2 * q + 1])), sc2, nm2);
+            if (q == 3) {
+              exp2_poly2(xx, p[6], p[7]);
+            } else {
+              float a0, a1;
+              unpack2(xx, a0, a1);
+              p[2 * q] = ex2(a0);
+              p[2 * q + 1] = ex2(a1);
+            }
+          }
+          acc01 = fadd2(acc01, pack2(p[0], p[1]));
+          acc23 = fadd2(acc23, pack2(p[2], p[3]));
+          acc01 = fadd2(acc01, pack2(p[4], p[5]));
+          acc23 = fadd2(acc23, pack2(p[6], p[7]));
+#pragma unroll
+          for (int q = 0; q < 4; ++q) pk[j / 2 + q] = pack_bf16x2(p[2 * q], p[2 * q + 1]);
+        }
+        float s0, s1, s2, s3;
+        unpack2(acc01, s0, s1);
+        unpack2(acc23, s2, s3);
+        sum = (s0 + s1) + (s2 + s3);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const int c = ch * 32 + j;
+          float b0, b1;
+          if (kind == 2) {
+            b0 = bias[c];
+            b1 = bias[c + 1];
+          } else {
+            b0 = c < last_valid ? 0.f : -INFINITY;
+            b1 = c + 1 < last_valid ? 0.f : -INFINITY;
+          }
+          const float v0 = fmaf(__uint_as_float(sa[j]), scale_log2e, b0);
+          const float v1 = fmaf(__uint_as_float(sa[j + 1]), scale_log2e, b1);
+          xk = fmaxf(xk, fmaxf(v0, v1));
+          const float p0 = ex2(v0 - mu), p1 = ex2(v1 - mu);
+          sum += p0 + p1;
+          pk[j / 2] = pack_bf16x2(p0, p1);
+        }
+      }
+      // same lazy maximum as the one-thread-per-row path; a full chunk triggers on its own 32 columns
+      // (sum <= 2^13 bounds every logit by m + 13).  The OR over the pair also orders the pair's TMEM
+      // loads before the P stores below.
+      const bool maybe = kind == 0 ? !(sum <= 8192.f) || m == -INFINITY
+                                   : (xk > m + kRescaleThreshold || (m == -INFINITY && xk > -INFINITY));
+      uint32_t redo_u;
+      asm volatile(
+          "{\n\t"
+          ".reg .pred p, q;\n\t"
+          "setp.ne.b32 q, %1, 0;\n\t"
+          "barrier.cta.red.or.pred p, %2, 64, q;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t"
+          "}"
+          : "=r"(redo_u)
+          : "r"((uint32_t)maybe), "r"(pair_bar)
+          : "memory");
+      if (SVG_ABL & 2) redo_u = 0;
+      float alpha = 1.f;
+      if (redo_u) {
+        // exact path for the row group: maximum of the chunk over both column halves, raise m where
+        // needed, exponentials again from the logits still in registers
+        float mt = xk;
+        if (kind == 0) {
+          mt = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) mt = fmaxf(mt, __uint_as_float(sa[j]));
+          mt *= scale_log2e;
+        }
+        xch[ch] = mt;
+        asm volatile("barrier.cta.sync %0, 64;" ::"r"(pair_bar) : "memory");
+        mt = fmaxf(mt, xch[ch ^ 1]);
+        asm volatile("barrier.cta.sync %0, 64;" ::"r"(pair_bar) : "memory");  // slot free for the next exchange
+        const bool bump = mt > m + kRescaleThreshold || (m == -INFINITY && mt > -INFINITY);
+        if (bump) {
+          alpha = ex2(m - mt);  // m = -inf -> 0
+          m = mt;
+        }
+        const float mu2 = (m == -INFINITY) ? 0.f : m;
+        sum = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const int c = ch * 32 + j;
+          float v0 = __uint_as_float(sa[j]) * scale_log2e, v1 = __uint_as_float(sa[j + 1]) * scale_log2e;
+          if (kind == 2) {
+            v0 += bias[c];
+            v1 += bias[c + 1];
+          } else if (kind == 1) {
+            if (c >= last_valid) v0 = -INFINITY;
+            if (c + 1 >= last_valid) v1 = -INFINITY;
+          }
+          const float p0 = ex2(v0 - mu2), p1 = ex2(v1 - mu2);
+          sum += p0 + p1;
+          pk[j / 2] = pack_bf16x2(p0, p1);
+        }
+      }
+      l = l * alpha + sum;
+      TMEM_ST16(tSb + (uint32_t)(st * 64 + ch * 16), pk);  // this thread's 32 keys of P (bf16 pairs)
+      // (loading the logits of chunk t+1 here, under the store and the hand-off, was measured slower:
+      // 5.91 vs 5.29 ms per 8 heads)
+      if (redo_u && t > 0) {
+        // rescale this thread's half of the O columns; P.V of chunk t-1 must have landed first
+        mbar_wait(bar(b_odone), (t - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 2; c += 32) {
+          TMEM_LD32(tO + c, sa);
+          tc_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sa[j] = __float_as_uint(__uint_as_float(sa[j]) * alpha);
+          TMEM_ST32(tO + c, sa);
+        }
+      }
+      tc_wait_st();
+      tc_fence_before();
+      if (lane == 0) mbar_arrive(bar(b_pfull + st));
+    }
+    // ---- epilogue: row sum of the pair, then each thread normalises and scatters D/2 columns ------
+    xch[ch] = l;
+    asm volatile("barrier.cta.sync %0, 64;" ::"r"(pair_bar) : "memory");
+    l += xch[ch ^ 1];
+    mbar_wait(bar(B::OFINAL + hf), 0);
+    tc_fence_after();
+    const bool live = row < nrows;
+    const int prow = min(row0 + row, n_q - 1);
+    const int dst = q_perm ? q_perm[(size_t)h * n_q + prow] : prow;
+    const float inv = 1.f / l;
+    uint4* orow = reinterpret_cast<uint4*>(out + ((size_t)h * n_q + dst) * D + ch * (D / 2));
+#pragma unroll
+    for (int c = 0; c < D / 2; c += 32) {
+      TMEM_LD32(tO + c, sa);
+      tc_wait_ld();
+      if (live) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(sa[8 * j]) * inv, __uint_as_float(sa[8 * j + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(sa[8 * j + 2]) * inv, __uint_as_float(sa[8 * j + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(sa[8 * j + 4]) * inv, __uint_as_float(sa[8 * j + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(sa[8 * j + 6]) * inv, __uint_as_float(sa[8 * j + 7]) * inv);
+          orow[c / 8 + j] = w;
+        }
+      }
+    }
+    if (lse && live && ch == 0) lse[(size_t)h * n_q + dst] = (m + log2f(l)) * kLn2;
+    tc_fence_before();
   } else if ((warp >> 2) < halves) {
     // =========================== softmax + epilogue (warps 0-7, thread == row) ==================
     const int hf = warp >> 2;
@@ -595,7 +787,7 @@ bool encode_rows_map(CUtensorMap* tm, const void* base, uint64_t rows, int d, in
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int D, int NS2, int G2, int NS1>
+template <int D, int NS2, int G2, int NS1, int TPR2 = 1>
 static int launch_attend_tc_ns(const SvgEarShape& s, const TmaSet& tm, const int32_t* q_perm,
                                const int32_t* k_sizes, const int32_t* k_offsets, const uint8_t* mask, bf16* out,
                                float* lse, AttendScratch& sc, int ckpad, int mt, float scale_log2e,
@@ -604,9 +796,9 @@ static int launch_attend_tc_ns(const SvgEarShape& s, const TmaSet& tm, const int
   if (!fk.ok()) return SVGEAR_ECUDA;
   cudaStream_t side = fk.side();
   // tiles with more than 128 live rows: one CTA per SM, two halves sharing every K/V tile
-  const size_t smem2 = Smem<D, NS2, 2, G2>::bytes(ckpad);
-  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS2, 2, G2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-  attend_tc_kernel<D, NS2, 2, G2><<<dim3(mt, s.bh), threads_for(2), smem2, st>>>(
+  const size_t smem2 = Smem<D, NS2, 2, G2, TPR2>::bytes(ckpad);
+  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS2, 2, G2, TPR2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+  attend_tc_kernel<D, NS2, 2, G2, TPR2><<<dim3(mt, s.bh), threads_for(2, TPR2), smem2, st>>>(
       tm, s.bh * s.n_k, sc.lnw, q_perm, k_sizes, k_offsets, mask, sc.tile_list, sc.tile_count, mt, s.n_q, s.n_k,
       s.c_q, s.c_k, ckpad, scale_log2e, out, lse);
   SVG_LAUNCH_OK();
@@ -614,8 +806,8 @@ static int launch_attend_tc_ns(const SvgEarShape& s, const TmaSet& tm, const int
   // CTA's softmax runs under the other's MMAs.  The two kernels write disjoint rows; the second is
   // forked onto a helper stream so that its CTAs fill the tail of the first instead of following it.
   const size_t smem1 = Smem<D, NS1, 1, 1>::bytes(ckpad);
-  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS1, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
-  attend_tc_kernel<D, NS1, 1, 1><<<dim3(mt < s.c_q ? mt : s.c_q, s.bh), threads_for(1), smem1, side>>>(
+  SVG_CUDA_OK(cudaFuncSetAttribute(attend_tc_kernel<D, NS1, 1, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1));
+  attend_tc_kernel<D, NS1, 1, 1, 1><<<dim3(mt < s.c_q ? mt : s.c_q, s.bh), threads_for(1), smem1, side>>>(
       tm, s.bh * s.n_k, sc.lnw, q_perm, k_sizes, k_offsets, mask, sc.tile_list, sc.tile_count, mt, s.n_q, s.n_k,
       s.c_q, s.c_k, ckpad, scale_log2e, out, lse);
   SVG_LAUNCH_OK();
@@ -648,6 +840,12 @@ int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const
                                                scale_log2e, st);
   // SVGEAR_ATTEND_G=2 selects the 128-key-tile variant of the two-half kernel (measured slower, DESIGN 4.1)
   static const bool force_g1 = [] { const char* e = getenv("SVGEAR_ATTEND_G"); return !(e && e[0] == '2'); }();
+  // two threads per query row in the two-half kernel (16 softmax warps) is the default at d = 128;
+  // SVGEAR_ATTEND_TPR=1 selects one thread per row (A/B measurements).  (Combined with G = 2: 6.08 ms.)
+  static const bool tpr2 = [] { const char* e = getenv("SVGEAR_ATTEND_TPR"); return !(e && e[0] == '1'); }();
+  if (tpr2 && force_g1 && s.d == 128 && Smem<128, 4, 2, 1, 2>::bytes(ckpad) <= cap && Smem<128, 2, 1, 1>::bytes(ckpad) <= cap)
+    return launch_attend_tc_ns<128, 4, 1, 2, 2>(s, tm, q_perm, k_sizes, k_offsets, mask, out, lse, sc, ckpad, mt,
+                                                scale_log2e, st);
   SVG_TRY(128, 2, 2, 2)
   SVG_TRY(128, 4, 1, 2)
   SVG_TRY(128, 3, 1, 2)

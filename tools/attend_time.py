@@ -21,7 +21,7 @@ vc = P.segment_means(vp, km)
 table = P.estimate_errors_streaming(qm, km, kp, vp)
 mask = R.route_error_aware(table, R.DensityBudget.global_density(rho))
 ts = []
-for rep in range(5):
+for rep in range(int(os.environ.get("REPS", 5))):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     res = P.sparse_attend(qp, kp, vp, qm, km, mask, v_centroids=vc, unpermute=True, dtype=torch.bfloat16)
