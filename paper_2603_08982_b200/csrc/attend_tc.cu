@@ -23,6 +23,9 @@ constexpr int threads_for(int halves, int tpr = 1) { return (4 * halves * tpr + 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef SVG_POLY2
+#define SVG_POLY2 0  // two-threads-per-row path: column pairs (of 4) whose exponential runs on the FMA pipe (0: 5.23, 1: 5.27, 2: 5.65 ms per 8 heads)
+#endif
 #ifndef SVG_ABL
 #define SVG_ABL 0  // ablation bits for tools/attend_ablate.sh (timing only, results are garbage): 1 no softmax
 #endif             // arithmetic, 2 never redo, 4 no QK^T MMAs, 8 no P.V MMAs, 16 no K/V loads, 32 one box per slab
@@ -389,8 +392,8 @@ __global__ void __launch_bounds__(threads_for(HALVES, TPR), 3 - HALVES)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const uint64_t xx = ffma2(pack2(__uint_as_float(sa[j + 2 * q]), __uint_as_float(sa[j + 2 * q + 1])), sc2, nm2);
-            if (q == 3) {
-              exp2_poly2(xx, p[6], p[7]);
+            if (q >= 4 - SVG_POLY2) {
+              exp2_poly2(xx, p[2 * q], p[2 * q + 1]);
             } else {
               float a0, a1;
               unpack2(xx, a0, a1);
