@@ -456,11 +456,12 @@ def run_ours(args):
         rest = hl - first
         bounds = [0] + [first + rest * g // (n_groups - 1) for g in range(n_groups)]
     else:
-        # seven groups, small at both ends: compute starts after a short first copy, and only a short
+        # nine groups, small at both ends: compute starts after a short first copy, and only a short
         # group is left to compute after the last copy has landed (the 2.3 GB host->device copy, ~44 ms
-        # on this PCIe link, is the floor of the leg); measured 56.5 ms against 58.5 ms with five groups
-        n_groups = 7
-        fr = (0.0, 0.075, 0.225, 0.425, 0.625, 0.8, 0.925, 1.0)
+        # on this PCIe link, is the floor of the leg); measured 53.2-53.7 ms against 54.9 ms with seven
+        # groups and 58.5 ms with five (more, smaller groups lose again: 54.2-54.6 ms with ten or eleven)
+        n_groups = 9
+        fr = (0.0, 0.05, 0.15, 0.275, 0.425, 0.575, 0.725, 0.85, 0.95, 1.0)
         bounds = sorted({min(hl, max(0, int(round(f * hl)))) for f in fr})
         n_groups = len(bounds) - 1
     copy_stream = torch.cuda.Stream(device=dev)   # host -> device
