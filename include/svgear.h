@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define SVGEAR_VERSION 110 /* 0.1.1: seeding computes its own Gram matrix; fused Lloyd step */
+#define SVGEAR_VERSION 111 /* 0.1.2: greedy tail of the device seeding; executor variants */
 
 enum {
   SVGEAR_OK = 0,
@@ -58,6 +58,15 @@ enum {
  * iteration.  Without it the tensor-core mode skips tokens whose distance bounds (Hamerly) prove
  * that their cluster cannot change — the assignments are identical, only the work differs. */
 enum { SVGEAR_KMEANS_FULL_EVAL = 0x100 };
+
+/* OR-ed into svgear_sparse_attend's exec_mode (SVGEAR_EXEC_BF16_TENSOR only): select a measured
+ * alternative of the fused attention kernel instead of the default (two threads per query row, 64-key
+ * tiles).  Same semantics, results equal up to the fp32 summation order of the row sums; kept callable so
+ * that the parity suite covers them (DESIGN.md 4.1 has their timings). */
+enum {
+  SVGEAR_ATTEND_ONE_THREAD_PER_ROW = 0x200, /* 8 softmax warps, thread == query row                 */
+  SVGEAR_ATTEND_TILE128 = 0x400             /* one N = 128 QK^T per 128-key tile (one thread per row) */
+};
 
 /* Problem shape of one call (all `bh` instances share it). */
 typedef struct SvgEarShape {

@@ -26,6 +26,7 @@ EST_VALUE_AWARE, EST_PLAIN = 0, 1
 FILL_REMAINDER, STOP_AT_FIRST_OVERFLOW = 0, 1
 EXEC_BF16_TENSOR, EXEC_FP32_CHECK = 0, 1
 KMEANS_FULL_EVAL = 0x100
+ATTEND_ONE_THREAD_PER_ROW, ATTEND_TILE128 = 0x200, 0x400
 NORM_NONE, NORM_HEAD, NORM_TOKEN = 0, 1, 2
 ROPE_NONE, ROPE_INTERLEAVED, ROPE_HALF_SPLIT = 0, 1, 2
 

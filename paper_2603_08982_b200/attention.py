@@ -47,13 +47,19 @@ def compensation_flops(d: int, q_sizes, compensated_per_row) -> int:  # attentio
 
 
 def sparse_attend(q, k, v, q_model: ClusterModel, k_model: ClusterModel, mask: BlockMask, *,
-                  dtype=torch.bfloat16, v_centroids=None, unpermute=False) -> AttentionResult:
+                  dtype=torch.bfloat16, v_centroids=None, unpermute=False, variant=None) -> AttentionResult:
     """Full executor (attention.py:160-192).  Inputs cluster-contiguous for their models.
 
     dtype=torch.bfloat16 -> tcgen05 tensor-core executor (bf16 output);
     dtype=torch.float32  -> CUDA-core fp32 executor (the fp32 check mode).
     `unpermute=True` scatters rows back to original token order (inverse_permute_rows).
+    `variant` (bf16 only) selects a measured alternative of the fused kernel instead of the default
+    (two threads per query row, 64-key tiles): "one_thread_per_row" or "tile128".
     """
+    if variant not in (None, "one_thread_per_row", "tile128"):
+        raise ValueError(f"unknown executor variant {variant!r}")
+    if variant is not None and dtype != torch.bfloat16:
+        raise ValueError("executor variants exist for the bf16 tensor-core executor only")
     if mask.selected.shape[-1] == 0:
         raise ValueError("no key clusters: softmax over an empty set is undefined")
     if dtype not in (torch.bfloat16, torch.float32):
@@ -81,7 +87,8 @@ def sparse_attend(q, k, v, q_model: ClusterModel, k_model: ClusterModel, mask: B
     shape = _lib.Shape(bh, n_q, n_k, d, c_q, c_k)
     ws = workspace(_lib.workspace_bytes(shape), dev)
     rc = _lib.lib().svgear_sparse_attend(
-        C.byref(shape), _lib.EXEC_FP32_CHECK if dtype == torch.float32 else _lib.EXEC_BF16_TENSOR,
+        C.byref(shape), _lib.EXEC_FP32_CHECK if dtype == torch.float32 else (_lib.EXEC_BF16_TENSOR | {
+            None: 0, "one_thread_per_row": _lib.ATTEND_ONE_THREAD_PER_ROW, "tile128": _lib.ATTEND_TILE128}[variant]),
         qp.data_ptr(), kp.data_ptr(), vp.data_ptr(), perm.data_ptr() if perm is not None else None,
         qs.data_ptr(), qo.data_ptr(), ks.data_ptr(), ko.data_ptr(), kc.data_ptr(), vc.data_ptr(),
         sel.data_ptr(), out.data_ptr(), lse.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr())

@@ -372,8 +372,10 @@ int svgear_sparse_attend(const SvgEarShape* shape, int32_t exec_mode, const void
   if (!shape || !q_permuted || !k_permuted || !v_permuted || !q_sizes || !q_offsets || !k_sizes ||
       !k_offsets || !k_centroids || !v_centroids || !mask || !out || !workspace)
     return SVGEAR_EINVAL;
-  if (exec_mode != SVGEAR_EXEC_BF16_TENSOR && exec_mode != SVGEAR_EXEC_FP32_CHECK)
-    return SVGEAR_EINVAL;
+  const int32_t variant = exec_mode & (SVGEAR_ATTEND_ONE_THREAD_PER_ROW | SVGEAR_ATTEND_TILE128);
+  const int32_t base_mode = exec_mode & ~variant;
+  if (base_mode != SVGEAR_EXEC_BF16_TENSOR && base_mode != SVGEAR_EXEC_FP32_CHECK) return SVGEAR_EINVAL;
+  if (variant && base_mode != SVGEAR_EXEC_BF16_TENSOR) return SVGEAR_EINVAL;
   if (!shape_ok(shape)) return SVGEAR_ESHAPE;
   if (!device_present()) return SVGEAR_ECUDA;
   Carver cv(workspace, workspace_bytes);

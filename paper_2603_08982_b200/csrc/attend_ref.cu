@@ -247,6 +247,8 @@ int launch_attend(const SvgEarShape& s, int exec_mode, const bf16* qp, const bf1
                   const int32_t* q_offsets, const int32_t* k_sizes, const int32_t* k_offsets,
                   const float* kc, const float* vc, const uint8_t* mask, void* out, float* lse,
                   AttendScratch& sc, cudaStream_t st) {
+  const int variant = exec_mode & (SVGEAR_ATTEND_ONE_THREAD_PER_ROW | SVGEAR_ATTEND_TILE128);
+  exec_mode &= ~variant;
   const int ckpad = ceil_div(s.c_k, 64) * 64;  // rows of the bf16 centroid arrays (zero padded)
   const float scale = 1.0f / sqrtf((float)s.d);
   prep_centroids_kernel<<<dim3(ceil_div(ckpad * s.d, 256), s.bh), 256, 0, st>>>(
@@ -269,7 +271,7 @@ int launch_attend(const SvgEarShape& s, int exec_mode, const bf16* qp, const bf1
     SVG_LAUNCH_OK();
     return SVGEAR_OK;
   }
-  return launch_attend_tc(s, qp, kp, vp, q_perm, k_sizes, k_offsets, mask, (bf16*)out, lse, sc, st);
+  return launch_attend_tc(s, qp, kp, vp, q_perm, k_sizes, k_offsets, mask, (bf16*)out, lse, sc, variant, st);
 }
 
 }  // namespace svg

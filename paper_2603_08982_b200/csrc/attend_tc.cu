@@ -819,7 +819,8 @@ static int launch_attend_tc_ns(const SvgEarShape& s, const TmaSet& tm, const int
 
 int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const bf16* vp,
                      const int32_t* q_perm, const int32_t* k_sizes, const int32_t* k_offsets,
-                     const uint8_t* mask, bf16* out, float* lse, AttendScratch& sc, cudaStream_t st) {
+                     const uint8_t* mask, bf16* out, float* lse, AttendScratch& sc, int variant,
+                     cudaStream_t st) {
   const int ckpad = ceil_div(s.c_k, 64) * 64;
   const int mt = AttendScratch::max_tiles(s.n_q, s.c_q, BM);
   const float scale_log2e = kLog2e / sqrtf((float)s.d);
@@ -841,11 +842,14 @@ int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const
       Smem<DD, N1, 1, 1>::bytes(ckpad) <= cap)                                                             \
     return launch_attend_tc_ns<DD, N2, GG, N1>(s, tm, q_perm, k_sizes, k_offsets, mask, out, lse, sc, ckpad, mt, \
                                                scale_log2e, st);
-  // SVGEAR_ATTEND_G=2 selects the 128-key-tile variant of the two-half kernel (measured slower, DESIGN 4.1)
-  static const bool force_g1 = [] { const char* e = getenv("SVGEAR_ATTEND_G"); return !(e && e[0] == '2'); }();
-  // two threads per query row in the two-half kernel (16 softmax warps) is the default at d = 128;
-  // SVGEAR_ATTEND_TPR=1 selects one thread per row (A/B measurements).  (Combined with G = 2: 6.08 ms.)
-  static const bool tpr2 = [] { const char* e = getenv("SVGEAR_ATTEND_TPR"); return !(e && e[0] == '1'); }();
+  // Default at d = 128: two threads per query row (16 softmax warps), 64-key tiles.  The measured
+  // alternatives stay selectable - per call with the SVGEAR_ATTEND_* bits of svgear_sparse_attend's
+  // exec_mode, per process with SVGEAR_ATTEND_TPR=1 (one thread per row) / SVGEAR_ATTEND_G=2 (128-key tiles,
+  // one thread per row) for A/B measurements of whole layers (DESIGN 4.1).
+  static const bool env_g2 = [] { const char* e = getenv("SVGEAR_ATTEND_G"); return e && e[0] == '2'; }();
+  static const bool env_tpr1 = [] { const char* e = getenv("SVGEAR_ATTEND_TPR"); return e && e[0] == '1'; }();
+  const bool force_g1 = !(env_g2 || (variant & SVGEAR_ATTEND_TILE128));
+  const bool tpr2 = !(env_tpr1 || (variant & SVGEAR_ATTEND_ONE_THREAD_PER_ROW));
   if (tpr2 && force_g1 && s.d == 128 && Smem<128, 4, 2, 1, 2>::bytes(ckpad) <= cap && Smem<128, 2, 1, 1>::bytes(ckpad) <= cap)
     return launch_attend_tc_ns<128, 4, 1, 2, 2>(s, tm, q_perm, k_sizes, k_offsets, mask, out, lse, sc, ckpad, mt,
                                                 scale_log2e, st);

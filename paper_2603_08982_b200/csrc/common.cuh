@@ -218,7 +218,7 @@ int launch_attend(const SvgEarShape& s, int exec_mode, const bf16* qp, const bf1
 int attend_tc_rows_per_tile();
 int launch_attend_tc(const SvgEarShape& s, const bf16* qp, const bf16* kp, const bf16* vp,
                      const int32_t* q_perm, const int32_t* k_sizes, const int32_t* k_offsets,
-                     const uint8_t* mask, bf16* out, float* lse, AttendScratch& sc,
+                     const uint8_t* mask, bf16* out, float* lse, AttendScratch& sc, int variant,
                      cudaStream_t st);
 
 }  // namespace svg

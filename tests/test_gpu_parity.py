@@ -421,6 +421,31 @@ class TestExecutor:
         assert rel_l2(host(res.output.float()), O.dense_attention(qp, kp, vp)) <= tol
         assert res.flops.exact_block == 4 * 128 * 300 * 300 and res.flops.compensation == 0
 
+    @pytest.mark.parametrize("variant", [None, "one_thread_per_row", "tile128"])
+    def test_kernel_variants_match_mixed_logit_reference(self, variant):
+        """The default fused kernel (two threads per query row) and its two measured alternatives, d = 128,
+        query clusters that span several 256-row tiles plus <= 128-row remainders, ragged and empty masks:
+        each against the Eq.1 mixed-logit oracle, and the alternatives against the default."""
+        for seed, (n_q, n_k, c_q, c_k) in ((3, (1500, 1300, 3, 9)), (4, (700, 900, 5, 7))):
+            prep, qm, km, qp, kp, vp = self._instance(seed, n_q=n_q, n_k=n_k, d=128, c_q=c_q, c_k=c_k)
+            rng = np.random.default_rng(seed)
+            for rho in (0.0, 0.4, 1.0):
+                sel = rng.random((c_q, c_k)) < rho
+                mask = P.mask_from_selected(torch.from_numpy(sel).cuda(), self._sizes(prep))
+                res = P.sparse_attend(prep.q, prep.k, prep.v, prep.q_model, prep.k_model, mask, variant=variant)
+                want = O.mixed_logit_output(qp, kp, vp, qm, km, sel)
+                assert rel_l2(host(res.output.float()), want) <= TOL_BF16, (variant, seed, rho)
+                _, o_lse = O.sparse_attend(qp, kp, vp, qm, km, sel)
+                assert np.abs(host(res.lse) - o_lse).max() <= 2e-2, (variant, seed, rho)
+                if variant is not None:
+                    base = P.sparse_attend(prep.q, prep.k, prep.v, prep.q_model, prep.k_model, mask)
+                    assert rel_l2(host(res.output.float()), host(base.output.float())) <= 5e-3
+        with pytest.raises(ValueError):
+            P.sparse_attend(prep.q, prep.k, prep.v, prep.q_model, prep.k_model, mask, variant="nope")
+        with pytest.raises(ValueError):
+            P.sparse_attend(prep.q, prep.k, prep.v, prep.q_model, prep.k_model, mask, dtype=torch.float32,
+                            variant="tile128")
+
     @pytest.mark.parametrize("dtype,tol", [(torch.float32, TOL_FP32), (torch.bfloat16, TOL_BF16)])
     def test_empty_mask_is_centroid_attention(self, dtype, tol):  # test_attention.py:96-107
         prep, qm, km, qp, kp, vp = self._instance(8)

@@ -30,7 +30,7 @@ class TestCAbi:
 
     def test_version_and_strerror(self):
         lib = P.load_library()
-        assert lib.svgear_version() == 110
+        assert lib.svgear_version() == 111
         assert lib.svgear_strerror(0) == b"ok"
         assert b"workspace" in lib.svgear_strerror(_lib.EWORKSPACE)
 
