@@ -700,6 +700,26 @@ class TestDeviceSeeding:
             assert len({int(i) for i in d2.argmin(dim=1)}) == 40
         assert not torch.equal(a, P.device_start(x, 40, seed=6))
 
+    def test_greedy_tail_covers_separated_blobs(self):
+        """The device seeding draws its last min(c/2, (n/c)^2/512) centres greedily (8 D^2 candidates per
+        round, the one that lowers the potential most is kept): on well separated blobs with as many
+        centres as blobs nearly every blob gets exactly one centre (plain D^2 sampling leaves several
+        blobs without a centre, which is what keeps Lloyd iterating on a cluster split in two)."""
+        rng = np.random.default_rng(11)
+        nb, per, d = 48, 160, 64          # n/c = 160 -> the last 24 of 48 centres are greedy
+        centres = rng.normal(size=(nb, d))
+        lab = np.repeat(np.arange(nb), per)
+        perm = rng.permutation(nb * per)
+        heads = [O.round_to_bf16(centres[lab] + 0.1 * rng.normal(size=(nb * per, d)))[perm] for _ in range(4)]
+        x = dev(np.stack(heads))
+        starts = P.device_start(x, nb, seed=0)
+        assert torch.equal(starts, P.device_start(x, nb, seed=0))
+        covered = []
+        for h in range(4):
+            near = torch.cdist(starts[h].double(), torch.from_numpy(centres).cuda()).argmin(dim=1)
+            covered.append(len(set(near.tolist())))
+        assert min(covered) >= nb - 2 and sum(covered) >= 4 * nb - 3, covered
+
     def test_device_start_converges_fast_on_blobs(self):
         q, k, v = (O.round_to_bf16(t) for t in O.blob_instance(4096, 4096, 64, 32, 64, 0.1, 0))
         out, mask, aux = P.svg_ear_attention(dev(q), dev(k), dev(v), 32, 64, 0.25, init="device",
