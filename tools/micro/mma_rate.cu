@@ -30,8 +30,13 @@ __global__ void __launch_bounds__(128) k(long long* clk, int M, int N, int ts, i
       for (int kk = 0; kk < 8; ++kk) {
         const uint64_t ad = make_desc(sA + (uint32_t)((kk >> 2) * (128 * 128) + (kk & 3) * 32), 16, 1024);
         const uint64_t bd = make_desc(sB + (uint32_t)((kk >> 2) * (256 * 128) + (kk & 3) * 32), 16, 1024);
-        if (ts) umma_ts(tmem + (uint32_t)((r & 1) * 256 % 256), tmem + 256 + (uint32_t)(kk * 8), bd, idesc, kk > 0);
-        else umma_ss(tmem + (uint32_t)((r & 1) * 0), ad, bd, idesc, kk > 0);
+        if (ts == 1) umma_ts(tmem, tmem + 256 + (uint32_t)(kk * 8), bd, idesc, kk > 0);
+        else if (ts == 0) umma_ss(tmem, ad, bd, idesc, kk > 0);
+        else {  // ts == 2: SS, two independent accumulations interleaved k-step by k-step (A and D differ)
+          umma_ss(tmem, ad, bd, idesc, kk > 0);
+          const uint64_t ad2 = make_desc(sA + 64 * 128 + (uint32_t)((kk >> 2) * (128 * 128) + (kk & 3) * 32), 16, 1024);
+          umma_ss(tmem + 256, ad2, bd, idesc, kk > 0);
+        }
       }
     }
     umma_commit(bar);
@@ -48,14 +53,15 @@ int main() {
   const size_t smem = 1024 + 128 * 128 * 2 + 256 * 128 * 2 + 256;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int reps = 2000;
-  for (int ts = 0; ts < 2; ++ts)
+  for (int ts = 0; ts < 3; ++ts)
     for (int M : {64, 128})
       for (int N : {32, 64, 128, 256}) {
         k<<<148, 128, smem>>>(clk, M, N, ts, reps);
         cudaError_t e = cudaDeviceSynchronize();
         long long h = 0; cudaMemcpy(&h, clk, 8, cudaMemcpyDeviceToHost);
-        printf("%s M=%3d N=%3d: %7.1f clk per MMA (floor 128*N/256 = %d)%s\n", ts ? "TS" : "SS", M, N,
-               (double)h / (reps * 8.0), 128 * N / 256, e == cudaSuccess ? "" : cudaGetErrorString(e));
+        printf("%s M=%3d N=%3d: %7.1f clk per MMA (floor 128*N/256 = %d)%s\n",
+               ts == 0 ? "SS" : (ts == 1 ? "TS" : "SS two interleaved accumulators"), M, N,
+               (double)h / (reps * (ts == 2 ? 16.0 : 8.0)), 128 * N / 256, e == cudaSuccess ? "" : cudaGetErrorString(e));
       }
   return 0;
 }
